@@ -1,0 +1,961 @@
+// kvsim_oracle.cpp — CPU ORACLE for parity tests and the CPU baseline.
+//
+// TEST INFRASTRUCTURE ONLY: the product path (paper_2411_05555_b200/csrc) never
+// links this file. It restates the reference's kvsim behaviour (reference
+// SPEC.md modules perfmodel 24-134, workload 136-190, engine 192-274,
+// policy 276-350, metrics 352-398) as a deliberately plain, sequential
+// discrete-event simulation: explicit per-request structs, std::vector
+// batches, a linear scan for the next event, per-request token timestamps.
+// Every rule follows docs/SEMANTICS.md; section numbers (§) refer to it.
+//
+// Build: g++ -O3 -std=gnu++20 -ffp-contract=off -fPIC -shared (oracle/Makefile),
+// mirroring the reference's Release flags (reference proj/CMakeLists.txt:7-9).
+#include "kvsim_oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <thread>
+#include <vector>
+
+namespace {
+
+constexpr double kInf = std::numeric_limits<double>::infinity();
+constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
+
+// ---------------------------------------------------------------- RNG (§2)
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t draw(uint64_t seed, int64_t i, int s) {
+  uint64_t key = mix64(seed ^ 0x243F6A8885A308D3ull);
+  return mix64(key + 0x9E3779B97F4A7C15ull * (uint64_t)(4 * i + s + 1));
+}
+int32_t uniform_int(uint64_t x, int32_t lo, int32_t hi) {
+  unsigned __int128 prod = (unsigned __int128)x * (uint64_t)((int64_t)hi - lo + 1);
+  return lo + (int32_t)(uint64_t)(prod >> 64);
+}
+
+// fdlibm-style natural log (restated; only IEEE +,-,*,/ and bit fiddling).
+double bits_to_d(uint64_t b) { double d; std::memcpy(&d, &b, 8); return d; }
+uint64_t d_to_bits(double d) { uint64_t b; std::memcpy(&b, &d, 8); return b; }
+double klog(double x) {
+  const double ln2_hi = bits_to_d(0x3fe62e42fee00000ull), ln2_lo = bits_to_d(0x3dea39ef35793c76ull);
+  const double Lg1 = bits_to_d(0x3FE5555555555593ull), Lg2 = bits_to_d(0x3FD999999997FA04ull),
+               Lg3 = bits_to_d(0x3FD2492494229359ull), Lg4 = bits_to_d(0x3FCC71C51D8E78AFull),
+               Lg5 = bits_to_d(0x3FC7466496CB03DEull), Lg6 = bits_to_d(0x3FC39A09D078C69Full),
+               Lg7 = bits_to_d(0x3FC2F112DF3E5244ull);
+  uint64_t b = d_to_bits(x);
+  int32_t hx = (int32_t)(b >> 32);
+  uint32_t lx = (uint32_t)b;
+  int32_t k = 0;
+  if (hx < 0x00100000) {  // subnormal or zero / negative
+    if (((hx & 0x7fffffff) | lx) == 0) return -kInf;
+    if (hx < 0) return kNaN;
+    k -= 54;
+    x = x * 18014398509481984.0;  // 2^54
+    b = d_to_bits(x);
+    hx = (int32_t)(b >> 32);
+  }
+  if (hx >= 0x7ff00000) return x + x;
+  k += (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  int32_t i = (hx + 0x95f64) & 0x100000;
+  b = d_to_bits(x);
+  b = ((uint64_t)(uint32_t)(hx | (i ^ 0x3ff00000)) << 32) | (b & 0xffffffffull);
+  x = bits_to_d(b);
+  k += (i >> 20);
+  double f = x - 1.0;
+  double dk = (double)k;
+  if ((0x000fffff & (2 + hx)) < 3) {
+    if (f == 0.0) return k == 0 ? 0.0 : dk * ln2_hi + dk * ln2_lo;
+    double R = f * f * (0.5 - 0.33333333333333333 * f);
+    return k == 0 ? f - R : dk * ln2_hi - ((R - dk * ln2_lo) - f);
+  }
+  double s = f / (2.0 + f);
+  double z = s * s;
+  i = hx - 0x6147a;
+  double w = z * z;
+  int32_t j = 0x6b851 - hx;
+  double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
+  double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
+  i |= j;
+  double R = t2 + t1;
+  if (i > 0) {
+    double hfsq = 0.5 * f * f;
+    if (k == 0) return f - (hfsq - s * (hfsq + R));
+    return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
+  }
+  if (k == 0) return f - s * (f - R);
+  return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
+}
+
+// ---------------------------------------------------------- perfmodel (§1)
+struct Perf {
+  double kvb, kvb_layer, W, pf_den, mem_den, comp_den, two_p, attn_coef, link_bw;
+  int64_t cap;
+  bool fits;
+};
+Perf make_perf(const kvsim_point_desc& p) {
+  Perf f{};
+  int64_t kvb = 2ll * p.num_layers * p.num_kv_heads * p.head_dim * p.bytes_per_value;
+  f.kvb = (double)kvb;
+  f.kvb_layer = (double)(2ll * p.num_kv_heads * p.head_dim * p.bytes_per_value);
+  f.W = p.param_count * (double)p.bytes_per_value;
+  f.pf_den = ((double)p.num_devices * p.peak_flops) * p.compute_eff;
+  f.mem_den = ((double)p.num_devices * p.hbm_bandwidth) * p.mem_bw_eff;
+  f.comp_den = f.pf_den;
+  f.two_p = 2.0 * p.param_count;
+  f.attn_coef = (double)(4ll * p.hidden_dim * p.num_layers);
+  f.link_bw = p.link_mode == KVSIM_LINK_SINGLE ? p.link_bandwidth * p.link_eff
+                                               : ((double)p.num_devices * p.link_bandwidth) * p.link_eff;
+  double usable = (double)p.num_devices * p.hbm_capacity * (1.0 - p.memory_reserve_fraction);
+  double room = usable - f.W;
+  f.fits = room >= 0.0;
+  f.cap = f.fits ? (int64_t)std::floor(room / f.kvb) : 0;
+  return f;
+}
+double prefill_lat(const Perf& f, int64_t s1, int64_t s2) {
+  return (f.two_p * (double)s1 + f.attn_coef * (double)s2) / f.pf_den;
+}
+double decode_lat(const Perf& f, int64_t batch, int64_t sum_kv) {
+  double mem = (f.W + (double)sum_kv * f.kvb) / f.mem_den;
+  double comp = (f.two_p * (double)batch) / f.comp_den;
+  return mem > comp ? mem : comp;
+}
+double transfer_lat(const Perf& f, double bytes) { return bytes / f.link_bw; }
+
+// ------------------------------------------------------------- engine (§3-6)
+enum Role { DECODE = 0, PREFILL = 1 };
+enum Job { NONE = 0, JOB_PREFILL = 1, JOB_STEP = 2 };
+
+struct Req {
+  double arrival = 0;
+  int32_t prompt = 0, decode = 0;
+  int32_t emitted = 0;
+  int32_t qlen = 0;           // length of the pending (re)prefill
+  int primary = -1, copy = -1;
+  bool stepping = false;      // member of its primary's in-flight step (+1 reserved)
+  double fresh_at = 0;        // copy is complete at this time
+  double last_t = 0, first_t = kNaN, done_t = kNaN, tbt_max = 0;
+  int32_t n_moves = 0, n_preempt = 0;
+  bool done = false;
+  int64_t kv() const { return (int64_t)prompt + emitted - 1; }
+  int64_t held() const { return kv() + (stepping ? 1 : 0); }
+};
+
+struct Incoming { int rid; double ready; };
+
+struct Inst {
+  int role = DECODE;
+  int job = NONE;
+  double busy_until = 0, job_start = 0;
+  std::vector<int> batch;
+  std::vector<Incoming> incoming;
+  std::vector<int> job_reqs;   // prefill admitted (splitwise/accellm) or co-batched (unified)
+  int64_t job_s1 = 0;
+  int64_t used = 0, peak = 0;
+  double busy_time = 0;
+  bool switch_pending = false;
+};
+
+struct Sim {
+  const kvsim_point_desc& P;
+  Perf f;
+  int n;
+  int policy;
+  int n_prefill = 0;
+  int64_t budget;
+  std::vector<Req> R;
+  int64_t N = 0;
+  int64_t next_arrival = 0;
+  std::vector<Inst> I;
+  std::vector<std::deque<int>> Q;         // queues: unified per inst, splitwise 1, accellm per pair
+  std::vector<int64_t> qtokens;
+  std::vector<double> link_busy;          // n*n directed
+  // counters
+  int64_t n_events = 0, n_steps = 0, n_prefills = 0, n_moves = 0, n_preempt = 0, n_evict = 0;
+  int64_t tokens_total = 0, tokens_window = 0, prefill_tokens = 0, mirror_tokens = 0;
+  double now = 0;
+  // event log
+  kvsim_event_record* ev;
+  int64_t ev_cap, ev_n = 0;
+  int status = KVSIM_OK;
+
+  Sim(const kvsim_point_desc& p, kvsim_event_record* e, int64_t ecap)
+      : P(p), f(make_perf(p)), n(p.num_instances), policy(p.policy), ev(e), ev_cap(ecap) {
+    budget = p.prefill_token_budget > 0 ? p.prefill_token_budget : 8192;
+    I.resize(n);
+    link_busy.assign((size_t)n * n, 0.0);
+    if (policy == KVSIM_POLICY_UNIFIED) Q.resize(n);
+    else if (policy == KVSIM_POLICY_SPLITWISE) {
+      Q.resize(1);
+      n_prefill = p.num_prefill_instances > 0 ? p.num_prefill_instances : (n + 2) / 4;
+      for (int i = 0; i < n_prefill; ++i) I[i].role = PREFILL;
+    } else Q.resize(n / 2);
+    qtokens.assign(Q.size(), 0);
+  }
+
+  void log(int kind, int inst, int a, int b, int64_t c) {
+    if (ev && ev_n < ev_cap) ev[ev_n] = kvsim_event_record{now, kind, inst, a, b, c};
+    ++ev_n;
+  }
+  void bump(int i, int64_t tok) {
+    I[i].used += tok;
+    if (I[i].used > I[i].peak) I[i].peak = I[i].used;
+  }
+  int queue_of(int i) const {
+    return policy == KVSIM_POLICY_UNIFIED ? i : policy == KVSIM_POLICY_SPLITWISE ? 0 : i / 2;
+  }
+  void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; }
+  void push_front(int q, int rid) { Q[q].push_front(rid); qtokens[q] += R[rid].qlen; }
+  int pop_front(int q) { int r = Q[q].front(); Q[q].pop_front(); qtokens[q] -= R[r].qlen; return r; }
+
+  // token emission at time t (first token, recompute token or decode token)
+  void emit(Req& r, double t) {
+    if (r.emitted == 0) r.first_t = t;
+    else { double gap = t - r.last_t; if (gap > r.tbt_max) r.tbt_max = gap; }
+    r.last_t = t;
+    r.emitted += 1;
+    ++tokens_total;
+    if (t >= P.warmup_s) ++tokens_window;
+  }
+  void finish_req(Req& r, double t) { r.done = true; r.done_t = t; }
+
+  void account_job(Inst& x, double t) {
+    if (x.job_start >= P.warmup_s) x.busy_time += t - x.job_start;
+  }
+
+  // ---- memory helpers (§5)
+  // free everything a request holds (primary + copy)
+  void free_req(int rid) {
+    Req& r = R[rid];
+    int64_t h = r.held();
+    if (r.primary >= 0) I[r.primary].used -= h;
+    if (r.copy >= 0) I[r.copy].used -= h;
+  }
+  // largest copy held on instance x: candidates are requests whose primary is
+  // the partner (batch + incoming). Returns rid or -1.
+  int largest_copy_on(int x) {
+    int y = x ^ 1;
+    int best = -1;
+    auto consider = [&](int rid) {
+      const Req& r = R[rid];
+      if (r.copy != x) return;
+      if (best < 0 || r.kv() > R[best].kv() || (r.kv() == R[best].kv() && rid < best)) best = rid;
+    };
+    for (int rid : I[y].batch) consider(rid);
+    for (auto& in : I[y].incoming) consider(in.rid);
+    return best;
+  }
+  void evict_copy(int rid) {
+    Req& r = R[rid];
+    int holder = r.copy;
+    I[holder].used -= r.held();
+    r.copy = -1;
+    ++n_evict;
+    log(KVSIM_EV_EVICT, holder, rid, 0, 0);
+  }
+  // preempt the highest-rid member of x's batch (P9, recompute)
+  void preempt_newest(int x) {
+    Inst& X = I[x];
+    auto it = std::max_element(X.batch.begin(), X.batch.end());
+    int rid = *it;
+    X.batch.erase(it);
+    Req& r = R[rid];
+    free_req(rid);
+    r.primary = -1;
+    r.copy = -1;
+    r.qlen = r.prompt + r.emitted;
+    r.n_preempt += 1;
+    ++n_preempt;
+    log(KVSIM_EV_PREEMPT, x, rid, r.qlen, 0);
+    push_front(queue_of(x), rid);
+  }
+
+  double fresh_at(int rid) const { return R[rid].fresh_at; }
+
+  // ---- link FIFO (§5)
+  double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
+    double& busy = link_busy[(size_t)s * n + d];
+    double tail = t_done + transfer_lat(f, (double)s1 * f.kvb_layer);
+    double start = t_start > busy ? t_start : busy;
+    double full = start + transfer_lat(f, (double)s1 * f.kvb);
+    double fin = tail > full ? tail : full;
+    busy = fin;
+    prefill_tokens += s1;
+    log(KVSIM_EV_TRANSFER, s, d, 0, s1);
+    return fin;
+  }
+
+  // ---- joins
+  void join(int x, double t) {
+    Inst& X = I[x];
+    int cnt = 0;
+    std::vector<Incoming> keep;
+    for (auto& in : X.incoming) {
+      if (in.ready <= t) { X.batch.push_back(in.rid); ++cnt; }
+      else keep.push_back(in);
+    }
+    X.incoming.swap(keep);
+    if (cnt) log(KVSIM_EV_JOIN, x, cnt, 0, 0);
+  }
+
+  // ---- decode step (splitwise / accellm decode instances)
+  void step_start(int x, double t) {
+    Inst& X = I[x];
+    bool preempted = false;
+    if (X.batch.empty()) return;
+    while (X.used + (int64_t)X.batch.size() > f.cap) {
+      int victim = policy == KVSIM_POLICY_ACCELLM ? largest_copy_on(x) : -1;
+      if (victim >= 0) evict_copy(victim);
+      else { preempt_newest(x); preempted = true; if (X.batch.empty()) break; }
+    }
+    if (X.batch.empty()) {
+      if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(x / 2, t);
+      return;
+    }
+    int64_t m = 0;
+    if (policy == KVSIM_POLICY_ACCELLM) {
+      int y = x ^ 1;
+      for (;;) {
+        m = 0;
+        for (int rid : X.batch) if (R[rid].copy == y) ++m;
+        if (I[y].used + m <= f.cap) break;
+        int v = largest_copy_on(y);
+        evict_copy(v);
+      }
+      bump(y, m);
+    }
+    int64_t B = (int64_t)X.batch.size(), K = 0;
+    for (int rid : X.batch) { K += R[rid].kv(); R[rid].stepping = true; }
+    bump(x, B);
+    X.job = JOB_STEP;
+    X.job_start = t;
+    X.busy_until = t + decode_lat(f, B, K);
+    log(KVSIM_EV_STEP_START, x, (int)B, 0, K);
+    if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(x / 2, t);
+  }
+
+  void step_end(int x, double t) {
+    Inst& X = I[x];
+    account_job(X, t);
+    ++n_steps;
+    X.job = NONE;
+    int y = x ^ 1;
+    int64_t m = 0;
+    if (policy == KVSIM_POLICY_ACCELLM)
+      for (int rid : X.batch) if (R[rid].copy == y) ++m;
+    std::vector<int> keep;
+    int completed = 0;
+    int B = (int)X.batch.size();
+    for (int rid : X.batch) {
+      Req& r = R[rid];
+      emit(r, t);
+      r.stepping = false;
+      if (r.emitted == r.decode) {
+        // held after the step == kv() with the new emitted count
+        I[x].used -= r.kv();
+        if (r.copy >= 0) I[r.copy].used -= r.kv();
+        finish_req(r, t);
+        ++completed;
+      } else {
+        keep.push_back(rid);
+      }
+    }
+    X.batch.swap(keep);
+    if (policy == KVSIM_POLICY_ACCELLM && m > 0) {
+      double& busy = link_busy[(size_t)x * n + y];
+      double start = t > busy ? t : busy;
+      double fin = start + transfer_lat(f, (double)m * f.kvb);
+      busy = fin;
+      mirror_tokens += m;
+      for (int rid : X.batch) if (R[rid].copy == y) R[rid].fresh_at = fin;
+      log(KVSIM_EV_TRANSFER, x, y, 1, m);
+    }
+    log(KVSIM_EV_STEP_END, x, B, completed, 0);
+  }
+
+  // ---------------------------------------------------------------- unified
+  void unified_start(int x, double t) {
+    Inst& X = I[x];
+    while (X.used + (int64_t)X.batch.size() > f.cap) preempt_newest(x);
+    int64_t B = (int64_t)X.batch.size(), K = 0;
+    for (int rid : X.batch) { K += R[rid].kv(); R[rid].stepping = true; }
+    bump(x, B);
+    X.job_reqs.clear();
+    int64_t s1 = 0, s2 = 0;
+    while (!Q[x].empty()) {
+      int head = Q[x].front();
+      int64_t len = R[head].qlen;
+      if (!X.job_reqs.empty() && s1 + len > budget) break;
+      if (X.used + len > f.cap) break;
+      pop_front(x);
+      bump(x, len);
+      X.job_reqs.push_back(head);
+      s1 += len;
+      s2 += len * len;
+    }
+    if (B == 0 && X.job_reqs.empty()) return;
+    double lat = (X.job_reqs.empty() ? 0.0 : prefill_lat(f, s1, s2)) + (B ? decode_lat(f, B, K) : 0.0);
+    X.job = JOB_STEP;
+    X.job_start = t;
+    X.busy_until = t + lat;
+    log(KVSIM_EV_STEP_START, x, (int)B, (int)X.job_reqs.size(), K);
+  }
+  void unified_end(int x, double t) {
+    Inst& X = I[x];
+    account_job(X, t);
+    ++n_steps;
+    X.job = NONE;
+    std::vector<int> keep;
+    int completed = 0;
+    int B = (int)X.batch.size();
+    for (int rid : X.batch) {
+      Req& r = R[rid];
+      emit(r, t);
+      r.stepping = false;
+      if (r.emitted == r.decode) { X.used -= r.kv(); finish_req(r, t); ++completed; }
+      else keep.push_back(rid);
+    }
+    for (int rid : X.job_reqs) {
+      Req& r = R[rid];
+      emit(r, t);
+      if (r.emitted == r.decode) { X.used -= r.kv(); finish_req(r, t); ++completed; }
+      else { r.primary = x; keep.push_back(rid); }
+    }
+    if (!X.job_reqs.empty()) ++n_prefills;
+    X.job_reqs.clear();
+    X.batch.swap(keep);
+    log(KVSIM_EV_STEP_END, x, B, completed, 0);
+    unified_start(x, t);
+  }
+
+  // -------------------------------------------------------------- splitwise
+  void sw_try_start(double t) {
+    for (int p = 0; p < n_prefill; ++p) {
+      Inst& X = I[p];
+      if (X.job != NONE || Q[0].empty()) continue;
+      X.job_reqs.clear();
+      int64_t s1 = 0, s2 = 0;
+      while (!Q[0].empty()) {
+        int head = Q[0].front();
+        int64_t len = R[head].qlen;
+        if (!X.job_reqs.empty() && s1 + len > budget) break;
+        int d = -1;
+        int64_t best = 0;
+        for (int j = n_prefill; j < n; ++j) {
+          int64_t fr = f.cap - I[j].used;
+          if (d < 0 || fr > best) { d = j; best = fr; }
+        }
+        if (best < len) break;
+        pop_front(0);
+        bump(d, len);
+        R[head].primary = d;
+        X.job_reqs.push_back(head);
+        s1 += len;
+        s2 += len * len;
+      }
+      if (X.job_reqs.empty()) continue;
+      X.job_s1 = s1;
+      bump(p, s1);
+      X.job = JOB_PREFILL;
+      X.job_start = t;
+      X.busy_until = t + prefill_lat(f, s1, s2);
+      log(KVSIM_EV_PREFILL_START, p, (int)X.job_reqs.size(), X.job_reqs[0], s1);
+    }
+  }
+  void sw_prefill_done(int p, double t) {
+    Inst& X = I[p];
+    account_job(X, t);
+    ++n_prefills;
+    X.job = NONE;
+    X.used -= X.job_s1;
+    int completed = 0;
+    std::vector<int64_t> per_dst(n, 0);
+    for (int rid : X.job_reqs) {
+      Req& r = R[rid];
+      emit(r, t);
+      if (r.emitted == r.decode) {
+        I[r.primary].used -= r.kv();
+        finish_req(r, t);
+        ++completed;
+      } else per_dst[r.primary] += r.qlen;
+    }
+    log(KVSIM_EV_PREFILL_DONE, p, (int)X.job_reqs.size(), completed, 0);
+    for (int d = n_prefill; d < n; ++d) {
+      if (per_dst[d] == 0) continue;
+      double fin = prefill_transfer(p, d, per_dst[d], X.job_start, t);
+      for (int rid : X.job_reqs)
+        if (!R[rid].done && R[rid].primary == d) I[d].incoming.push_back({rid, fin});
+    }
+    X.job_reqs.clear();
+  }
+
+  // ---------------------------------------------------------------- accellm
+  int64_t load_of(int x) const {
+    int64_t s = 0;
+    for (int rid : I[x].batch) s += R[rid].kv();
+    for (auto& in : I[x].incoming) s += R[in.rid].kv();
+    return s;
+  }
+  // head of the pair queue admissible on x after evicting every copy on x?
+  bool head_admissible(int x) {
+    int q = x / 2;
+    if (Q[q].empty()) return false;
+    int64_t len = R[Q[q].front()].qlen;
+    int64_t copies = 0;
+    int y = x ^ 1;
+    for (int rid : I[y].batch) if (R[rid].copy == x) copies += R[rid].held();
+    for (auto& in : I[y].incoming) if (R[in.rid].copy == x) copies += R[in.rid].held();
+    return I[x].used - copies + len <= f.cap;
+  }
+  void move_req(int rid, int from, int to, double t) {
+    Req& r = R[rid];
+    double ready = r.fresh_at > t ? r.fresh_at : t;
+    r.primary = to;
+    r.copy = from;
+    r.fresh_at = t;
+    r.n_moves += 1;
+    ++n_moves;
+    I[to].incoming.push_back({rid, ready});
+    log(KVSIM_EV_MOVE, from, rid, to, 0);
+  }
+  // move every request with primary x that holds a copy on the partner
+  void move_all_to_partner(int x, double t) {
+    Inst& X = I[x];
+    int y = x ^ 1;
+    std::vector<int> keep;
+    for (int rid : X.batch) {
+      if (R[rid].copy == y) move_req(rid, x, y, t);
+      else keep.push_back(rid);
+    }
+    X.batch.swap(keep);
+    std::vector<Incoming> keepin;
+    for (auto& in : X.incoming) {
+      if (R[in.rid].copy == y) {
+        // already complete on y (old primary): ready at max(t, fresh_at)
+        move_req(in.rid, x, y, t);
+      } else keepin.push_back(in);
+    }
+    X.incoming.swap(keepin);
+  }
+  void acc_start_job(int x, double t) {
+    Inst& X = I[x];
+    int q = x / 2;
+    X.job_reqs.clear();
+    int64_t s1 = 0, s2 = 0;
+    while (!Q[q].empty()) {
+      int head = Q[q].front();
+      int64_t len = R[head].qlen;
+      if (!X.job_reqs.empty() && s1 + len > budget) break;
+      while (X.used + len > f.cap) {
+        int v = largest_copy_on(x);
+        if (v < 0) break;
+        evict_copy(v);
+      }
+      if (X.used + len > f.cap) break;
+      pop_front(q);
+      bump(x, len);
+      R[head].primary = x;
+      X.job_reqs.push_back(head);
+      s1 += len;
+      s2 += len * len;
+    }
+    X.job_s1 = s1;
+    X.job = JOB_PREFILL;
+    X.job_start = t;
+    X.busy_until = t + prefill_lat(f, s1, s2);
+    log(KVSIM_EV_PREFILL_START, x, (int)X.job_reqs.size(), X.job_reqs.empty() ? -1 : X.job_reqs[0], s1);
+  }
+  bool try_switch(int x, double t) {
+    if (!head_admissible(x)) return false;
+    Inst& X = I[x];
+    X.switch_pending = false;
+    move_all_to_partner(x, t);
+    X.role = PREFILL;
+    log(KVSIM_EV_ROLE, x, PREFILL, 0, 0);
+    acc_start_job(x, t);
+    return true;
+  }
+  void ensure_prefill(int q, double t) {
+    if (Q[q].empty()) return;
+    int a = 2 * q, b = a + 1;
+    if (I[a].role == PREFILL || I[b].role == PREFILL || I[a].switch_pending || I[b].switch_pending) return;
+    int m = load_of(b) < load_of(a) ? b : a;
+    if (I[m].job == NONE) try_switch(m, t);
+    else I[m].switch_pending = true;
+  }
+  void rebalance(int x, double t) {
+    int y = x ^ 1;
+    Inst& X = I[x];
+    Inst& Y = I[y];
+    if (Y.role != DECODE || Y.switch_pending) return;
+    int64_t c = (int64_t)X.batch.size() + (int64_t)X.incoming.size() - (int64_t)Y.batch.size() -
+                (int64_t)Y.incoming.size();
+    int64_t d = load_of(x) - load_of(y);
+    std::vector<int> cand;
+    for (int rid : X.batch) if (R[rid].copy == y) cand.push_back(rid);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+      if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
+      return a < b;
+    });
+    std::vector<int> moved;
+    for (int rid : cand) {
+      int64_t k = R[rid].kv();
+      int64_t v = std::max<int64_t>(0, std::llabs(c) - 1), D = std::llabs(d);
+      int64_t c2 = c - 2, d2 = d - 2 * k;
+      int64_t v2 = std::max<int64_t>(0, std::llabs(c2) - 1), D2 = std::llabs(d2);
+      if (v2 <= v && D2 <= D && (v2 < v || D2 < D)) {
+        moved.push_back(rid);
+        c = c2;
+        d = d2;
+      }
+    }
+    if (moved.empty()) return;
+    std::vector<int> keep;
+    for (int rid : X.batch)
+      if (std::find(moved.begin(), moved.end(), rid) == moved.end()) keep.push_back(rid);
+    X.batch.swap(keep);
+    for (int rid : moved) move_req(rid, x, y, t);
+  }
+  void acc_boundary(int x, double t) {
+    Inst& X = I[x];
+    join(x, t);
+    if (X.switch_pending) {
+      X.switch_pending = false;
+      if (try_switch(x, t)) return;
+    }
+    ensure_prefill(x / 2, t);
+    if (X.role == PREFILL) return;  // ensure_prefill switched x
+    rebalance(x, t);
+    step_start(x, t);
+  }
+  void acc_prefill_done(int x, double t) {
+    Inst& X = I[x];
+    account_job(X, t);
+    ++n_prefills;
+    X.job = NONE;
+    int y = x ^ 1;
+    int completed = 0;
+    std::vector<int> survivors;
+    for (int rid : X.job_reqs) {
+      Req& r = R[rid];
+      emit(r, t);
+      if (r.emitted == r.decode) {
+        X.used -= r.kv();
+        finish_req(r, t);
+        ++completed;
+      } else survivors.push_back(rid);
+    }
+    log(KVSIM_EV_PREFILL_DONE, x, (int)X.job_reqs.size(), completed, 0);
+    int64_t s1c = 0;
+    int ncopy = 0;
+    for (int rid : survivors) {
+      Req& r = R[rid];
+      if (I[y].used + r.kv() <= f.cap) {
+        bump(y, r.kv());
+        r.copy = y;
+        s1c += r.kv();
+        ++ncopy;
+      }
+    }
+    if (ncopy) log(KVSIM_EV_COPY, y, ncopy, 0, s1c);
+    if (s1c > 0) {
+      double fin = prefill_transfer(x, y, s1c, X.job_start, t);
+      for (int rid : survivors) if (R[rid].copy == y) R[rid].fresh_at = fin;
+    }
+    for (int rid : survivors) X.batch.push_back(rid);
+    X.job_reqs.clear();
+    if (head_admissible(x)) {
+      move_all_to_partner(x, t);
+      acc_start_job(x, t);
+      return;
+    }
+    X.role = DECODE;
+    log(KVSIM_EV_ROLE, x, DECODE, 0, 0);
+    acc_boundary(x, t);
+  }
+
+  // ---------------------------------------------------------------- arrival
+  void arrive(int rid, double t) {
+    Req& r = R[rid];
+    r.qlen = r.prompt;
+    if (policy == KVSIM_POLICY_UNIFIED) {
+      int best = 0;
+      int64_t bf = 0;
+      for (int i = 0; i < n; ++i) {
+        int64_t fr = f.cap - I[i].used - qtokens[i];
+        if (i == 0 || fr > bf) { best = i; bf = fr; }
+      }
+      log(KVSIM_EV_ARRIVE, best, rid, r.prompt, 0);
+      push_back(best, rid);
+      if (I[best].job == NONE) unified_start(best, t);
+    } else if (policy == KVSIM_POLICY_SPLITWISE) {
+      log(KVSIM_EV_ARRIVE, 0, rid, r.prompt, 0);
+      push_back(0, rid);
+    } else {
+      int best = 0;
+      int64_t bf = 0;
+      for (int q = 0; q < n / 2; ++q) {
+        int64_t fr = (f.cap - I[2 * q].used) + (f.cap - I[2 * q + 1].used) - qtokens[q];
+        if (q == 0 || fr > bf) { best = q; bf = fr; }
+      }
+      log(KVSIM_EV_ARRIVE, best, rid, r.prompt, 0);
+      push_back(best, rid);
+      ensure_prefill(best, t);
+    }
+  }
+
+  // ------------------------------------------------------------- main loop
+  void run() {
+    int64_t dmax = 1;
+    for (int64_t i = 0; i < N; ++i) dmax = std::max<int64_t>(dmax, R[i].decode);
+    int64_t budget_events = 4 * N * (dmax + 2) + 4096;
+    for (;;) {
+      double bt = kInf;
+      int bk = 9, bid = 0;
+      auto cand = [&](double t, int k, int id) {
+        if (t < bt || (t == bt && (k < bk || (k == bk && id < bid)))) { bt = t; bk = k; bid = id; }
+      };
+      if (next_arrival < N) cand(R[next_arrival].arrival, 0, (int)next_arrival);
+      for (int i = 0; i < n; ++i) {
+        const Inst& X = I[i];
+        if (X.job != NONE) cand(X.busy_until, X.job == JOB_PREFILL ? 2 : 3, i);
+        else if (X.role == DECODE && !X.incoming.empty()) {
+          double mr = kInf;
+          for (auto& in : X.incoming) mr = std::min(mr, in.ready);
+          cand(mr, 1, i);
+        }
+      }
+      if (bk == 9) break;
+      if (++n_events > budget_events) { status = KVSIM_E_EVENT_BUDGET; break; }
+      now = bt;
+      double t = bt;
+      switch (bk) {
+        case 0:
+          ++next_arrival;
+          arrive(bid, t);
+          break;
+        case 1:
+          log(KVSIM_EV_WAKE, bid, 0, 0, 0);
+          if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(bid, t);
+          else { join(bid, t); step_start(bid, t); }
+          break;
+        case 2:
+          if (policy == KVSIM_POLICY_SPLITWISE) sw_prefill_done(bid, t);
+          else acc_prefill_done(bid, t);
+          break;
+        case 3:
+          if (policy == KVSIM_POLICY_UNIFIED) unified_end(bid, t);
+          else {
+            step_end(bid, t);
+            if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(bid, t);
+            else { join(bid, t); step_start(bid, t); }
+          }
+          break;
+      }
+      if (policy == KVSIM_POLICY_SPLITWISE) sw_try_start(t);
+    }
+  }
+};
+
+int check_point(const kvsim_point_desc& p) {
+  if (p.num_instances < 1 || p.num_instances > KVSIM_MAX_INSTANCES) return KVSIM_E_INVALID;
+  if (p.policy == KVSIM_POLICY_ACCELLM && (p.num_instances % 2)) return KVSIM_E_ODD_INSTANCES;
+  if (p.policy == KVSIM_POLICY_SPLITWISE) {
+    int np = p.num_prefill_instances > 0 ? p.num_prefill_instances : (p.num_instances + 2) / 4;
+    if (p.num_instances < 2 || np >= p.num_instances) return KVSIM_E_INVALID;
+  }
+  if (p.policy < 0 || p.policy > 2) return KVSIM_E_INVALID;
+  if (!make_perf(p).fits) return KVSIM_E_MODEL_FIT;
+  return KVSIM_OK;
+}
+
+int64_t gen_trace(const kvsim_point_desc& p, double* arr, int32_t* pr, int32_t* de, int64_t cap) {
+  if (!(p.rate > 0.0)) return 0;
+  int64_t lim = std::min<int64_t>(cap, p.num_requests);
+  double t = 0.0;
+  int64_t i = 0;
+  for (; i < lim; ++i) {
+    if (p.arrival_process == KVSIM_ARRIVAL_FIXED) t = (double)i / p.rate;
+    else {
+      uint64_t x = draw(p.seed, i, 2);
+      double u = (double)((x >> 11) + 1) * 0x1.0p-53;
+      double gap = -klog(u) / p.rate;
+      t = i == 0 ? gap : t + gap;
+    }
+    if (!(t < p.duration_s)) break;
+    arr[i] = t;
+    pr[i] = uniform_int(draw(p.seed, i, 0), p.prompt_min, p.prompt_max);
+    de[i] = uniform_int(draw(p.seed, i, 1), p.decode_min, p.decode_max);
+  }
+  return i;
+}
+
+int64_t nearest_rank(int64_t n, int pct) { return (pct * n + 99) / 100 - 1; }
+
+void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
+  const kvsim_point_desc& p = S.P;
+  std::memset(out, 0, sizeof(*out));
+  out->status = S.status;
+  out->num_instances = S.n;
+  out->user_tag = p.user_tag;
+  out->n_requests = S.N;
+  out->n_events = S.n_events;
+  out->n_steps = S.n_steps;
+  out->n_prefills = S.n_prefills;
+  out->n_moves = S.n_moves;
+  out->n_preemptions = S.n_preempt;
+  out->n_evictions = S.n_evict;
+  out->tokens_total = S.tokens_total;
+  out->tokens_window = S.tokens_window;
+  out->link_prefill_tokens = S.prefill_tokens;
+  out->link_mirror_tokens = S.mirror_tokens;
+  out->makespan_s = S.now;
+  int64_t peak = 0;
+  double busy = 0;
+  for (auto& x : S.I) { peak = std::max(peak, x.peak); busy += x.busy_time; }
+  out->peak_kv_tokens = peak;
+  out->busy_s_total = busy;
+  out->peak_kv_gb = (double)peak * S.f.kvb / 1e9;
+  out->link_prefill_gb = (double)S.prefill_tokens * S.f.kvb / 1e9;
+  out->link_mirror_gb = (double)S.mirror_tokens * S.f.kvb / 1e9;
+  std::vector<double> ttft, jct;
+  double s_ttft = 0, s_jct = 0, s_tbt = 0, tbt_max = 0;
+  int64_t n_tbt = 0, completed = 0;
+  for (int64_t i = 0; i < S.N; ++i) {
+    const Req& r = S.R[i];
+    if (recs) {
+      recs[i] = kvsim_request_record{r.arrival, r.first_t, r.done_t, r.tbt_max, r.prompt, r.decode,
+                                     r.n_moves, r.n_preempt};
+    }
+    if (!r.done) continue;
+    ++completed;
+    if (r.arrival < p.warmup_s) continue;
+    double a = r.first_t - r.arrival, b = r.done_t - r.arrival;
+    ttft.push_back(a);
+    jct.push_back(b);
+    s_ttft += a;
+    s_jct += b;
+    if (r.decode > 1) {
+      s_tbt += r.done_t - r.first_t;
+      n_tbt += r.decode - 1;
+      if (r.tbt_max > tbt_max) tbt_max = r.tbt_max;
+    }
+  }
+  out->n_completed = completed;
+  int64_t m = (int64_t)ttft.size();
+  out->n_measured = m;
+  if (m > 0) {
+    out->ttft_mean = s_ttft / (double)m;
+    out->jct_mean = s_jct / (double)m;
+    std::sort(ttft.begin(), ttft.end());
+    std::sort(jct.begin(), jct.end());
+    out->ttft_p50 = ttft[nearest_rank(m, 50)];
+    out->ttft_p95 = ttft[nearest_rank(m, 95)];
+    out->ttft_max = ttft[m - 1];
+    out->jct_p50 = jct[nearest_rank(m, 50)];
+    out->jct_p95 = jct[nearest_rank(m, 95)];
+    out->jct_max = jct[m - 1];
+  } else {
+    out->ttft_mean = out->jct_mean = out->ttft_p50 = out->ttft_p95 = out->ttft_max = kNaN;
+    out->jct_p50 = out->jct_p95 = out->jct_max = kNaN;
+  }
+  out->tbt_mean = n_tbt > 0 ? s_tbt / (double)n_tbt : kNaN;
+  out->tbt_max = n_tbt > 0 ? tbt_max : kNaN;
+  double window = S.now - p.warmup_s;
+  if (window > 0) {
+    out->cost_eff = (double)S.tokens_window / (window * (double)S.n);
+    out->idle_frac = 1.0 - busy / ((double)S.n * window);
+  } else {
+    out->cost_eff = out->idle_frac = kNaN;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t kvo_rng_draw(uint64_t seed, int64_t i, int stream) { return draw(seed, i, stream); }
+double kvo_klog(double x) { return klog(x); }
+double kvo_kv_bytes_per_token(const kvsim_point_desc* p) { return make_perf(*p).kvb; }
+double kvo_weight_bytes(const kvsim_point_desc* p) { return make_perf(*p).W; }
+double kvo_prefill_latency(const kvsim_point_desc* p, int64_t s1, int64_t s2) {
+  return prefill_lat(make_perf(*p), s1, s2);
+}
+double kvo_decode_step_latency(const kvsim_point_desc* p, int64_t b, int64_t k) {
+  return decode_lat(make_perf(*p), b, k);
+}
+double kvo_transfer_latency(const kvsim_point_desc* p, double bytes) {
+  return transfer_lat(make_perf(*p), bytes);
+}
+int kvo_kv_capacity_tokens(const kvsim_point_desc* p, int64_t* out) {
+  Perf f = make_perf(*p);
+  *out = f.cap;
+  return f.fits ? KVSIM_OK : KVSIM_E_MODEL_FIT;
+}
+int64_t kvo_gen_trace(const kvsim_point_desc* p, double* a, int32_t* pr, int32_t* de, int64_t cap) {
+  return gen_trace(*p, a, pr, de, cap);
+}
+
+int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsim_point_summary* out,
+                  kvsim_request_record* recs, kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count) {
+  int st = check_point(*p);
+  if (st != KVSIM_OK) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = st;
+    out->user_tag = p->user_tag;
+    if (ev_count) *ev_count = 0;
+    return st;
+  }
+  Sim S(*p, ev, ev_cap);
+  int64_t N;
+  std::vector<double> arr;
+  std::vector<int32_t> pr, de;
+  if (trace) {
+    N = std::min<int64_t>(trace->n, p->num_requests);
+    arr.assign(trace->arrival_s, trace->arrival_s + N);
+    pr.assign(trace->prompt_len, trace->prompt_len + N);
+    de.assign(trace->decode_len, trace->decode_len + N);
+  } else {
+    arr.resize(p->num_requests);
+    pr.resize(p->num_requests);
+    de.resize(p->num_requests);
+    N = gen_trace(*p, arr.data(), pr.data(), de.data(), p->num_requests);
+  }
+  S.N = N;
+  S.R.resize(N);
+  for (int64_t i = 0; i < N; ++i) {
+    S.R[i].arrival = arr[i];
+    S.R[i].prompt = pr[i];
+    S.R[i].decode = de[i];
+  }
+  S.run();
+  summarize(S, out, recs);
+  if (ev_count) *ev_count = S.ev_n;
+  return S.status;
+}
+
+int kvo_run_sweep(const kvsim_point_desc* pts, int64_t n, int threads, kvsim_point_summary* out) {
+  if (threads < 1) threads = 1;
+  std::atomic<int64_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      kvo_run_point(&pts[i], nullptr, &out[i], nullptr, nullptr, 0, nullptr);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 0; k < threads; ++k) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  return KVSIM_OK;
+}
+
+}  // extern "C"
