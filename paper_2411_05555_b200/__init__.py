@@ -1,0 +1,168 @@
+"""kvsim on B200: warp-per-point sweep of the AcceLLM serving simulator.
+
+Python host mirror of the reference-facing C-ABI (include/kvsim_gpu.h). The
+reference's own entry points are C++ (`kvsim run|sweep`, reference
+SPEC.md:400-455; perfmodel API reference proj/include/kvsim/perfmodel.hpp);
+this module exposes the same operations for tests and benchmarks:
+
+    sim = KvSim(device=0)
+    summaries = sim.run(points)                       # cmd_sweep point loop
+    summaries, records, events = sim.run(points, records=True, events=4096)
+
+There is no CPU fallback: if the CUDA library is missing or no sm_100 device
+is visible, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .abi import (EventRecord, PointDesc, PointSummary, RequestRecord, TraceView,  # noqa: F401
+                  make_point, points_array, summary_dict, STATUS, POLICY, POLICY_NAME,
+                  DEVICES, MODELS, WORKLOADS, SUMMARY_CSV)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libkvsim_gpu.so")
+CLI_PATH = os.path.join(_HERE, "_build", "kvsim")
+
+_lib = None
+
+
+class KvSimError(RuntimeError):
+    pass
+
+
+def load_library() -> C.CDLL:
+    """Load the sm_100a library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise KvSimError(f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    L.kvsim_gpu_abi_version.restype = C.c_int
+    L.kvsim_gpu_device_count.restype = C.c_int
+    L.kvsim_gpu_open.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_close.argtypes = [C.c_void_p]
+    L.kvsim_point_defaults.argtypes = [C.POINTER(PointDesc)]
+    L.kvsim_point_validate.argtypes = [C.POINTER(PointDesc), C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_run.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(TraceView), C.c_size_t,
+                                C.POINTER(PointSummary), C.POINTER(RequestRecord), C.POINTER(EventRecord),
+                                C.c_size_t, C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                       C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_last_launches.argtypes = [C.c_void_p]
+    L.kvsim_gpu_last_launches.restype = C.c_int64
+    L.kvsim_gpu_perf_batch.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_double), C.c_size_t, C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_gen_trace.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                      C.c_char_p, C.c_size_t]
+    _lib = L
+    return L
+
+
+class KvSim:
+    """One device context (kvsim_gpu_open)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        self.err = C.create_string_buffer(512)
+        h = C.c_void_p()
+        rc = self.lib.kvsim_gpu_open(device, C.byref(h), self.err, 512)
+        if rc != 0:
+            raise KvSimError(f"kvsim_gpu_open({device}) failed [{rc}]: {self.err.value.decode()}")
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.kvsim_gpu_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise KvSimError(f"{what} failed [{rc}]: {self.err.value.decode()}")
+
+    def run(self, points, traces=None, records: bool = False, events: int = 0):
+        """Run points (list of PointDesc). Returns summaries, or (summaries,
+        records per point, events per point) when records/events requested."""
+        n = len(points)
+        P = (PointDesc * n)(*points)
+        S = (PointSummary * n)()
+        tot = sum(max(int(p.num_requests), 0) for p in points)
+        R = (RequestRecord * max(tot, 1))() if records else None
+        E = (EventRecord * max(events * n, 1))() if events else None
+        cnt = (C.c_int64 * n)() if events else None
+        T, nt = None, 0
+        if traces:
+            nt = len(traces)
+            T = (TraceView * nt)(*traces)
+        rc = self.lib.kvsim_gpu_run(self.h, P, n, T, nt, S, R, E, events, cnt, self.err, 512)
+        self._check(rc, "kvsim_gpu_run")
+        summaries = list(S)
+        if not records and not events:
+            return summaries
+        recs_out, ev_out, off = [], [], 0
+        for i, p in enumerate(points):
+            nr = max(int(p.num_requests), 0)
+            recs_out.append(list(R)[off:off + summaries[i].n_requests] if records else None)
+            off += nr
+            ev_out.append(list(E)[i * events:i * events + min(cnt[i], events)] if events else None)
+        return summaries, recs_out, ev_out
+
+    def reserve(self, points):
+        n = len(points)
+        P = (PointDesc * n)(*points)
+        self._check(self.lib.kvsim_gpu_reserve(self.h, P, n, self.err, 512), "kvsim_gpu_reserve")
+
+    def run_device(self, d_points_ptr: int, n: int, d_out_ptr: int, stream_ptr: int = 0):
+        rc = self.lib.kvsim_gpu_run_device(self.h, C.c_void_p(d_points_ptr), n, C.c_void_p(d_out_ptr),
+                                           C.c_void_p(stream_ptr), self.err, 512)
+        self._check(rc, "kvsim_gpu_run_device")
+
+    def last_launches(self) -> int:
+        return int(self.lib.kvsim_gpu_last_launches(self.h))
+
+    def perf_batch(self, points, pidx, ops, s1, s2):
+        n = len(pidx)
+        P = (PointDesc * len(points))(*points)
+        a = (C.c_int32 * n)(*pidx)
+        o = (C.c_int32 * n)(*ops)
+        x = (C.c_int64 * n)(*s1)
+        y = (C.c_int64 * n)(*s2)
+        out = (C.c_double * n)()
+        rc = self.lib.kvsim_gpu_perf_batch(self.h, P, len(points), a, o, x, y, out, n, self.err, 512)
+        self._check(rc, "kvsim_gpu_perf_batch")
+        return list(out)
+
+    def gen_trace(self, point):
+        cap = max(int(point.num_requests), 1)
+        arr = (C.c_double * cap)()
+        pl = (C.c_int32 * cap)()
+        dl = (C.c_int32 * cap)()
+        nn = C.c_int64(0)
+        rc = self.lib.kvsim_gpu_gen_trace(self.h, C.byref(point), arr, pl, dl, C.byref(nn), self.err, 512)
+        self._check(rc, "kvsim_gpu_gen_trace")
+        k = nn.value
+        return list(arr)[:k], list(pl)[:k], list(dl)[:k]
+
+
+def trace_view(arrival, prompt, decode):
+    """Build a TraceView (keeps the backing arrays alive on the object)."""
+    n = len(arrival)
+    a = (C.c_double * max(n, 1))(*arrival)
+    p = (C.c_int32 * max(n, 1))(*prompt)
+    d = (C.c_int32 * max(n, 1))(*decode)
+    tv = TraceView(C.cast(a, C.POINTER(C.c_double)), C.cast(p, C.POINTER(C.c_int32)),
+                   C.cast(d, C.POINTER(C.c_int32)), n)
+    tv._keep = (a, p, d)
+    return tv

@@ -1,0 +1,1608 @@
+// kvsim_sim.cuh — warp-per-point discrete-event simulation core (kernel K3).
+//
+// One warp simulates one sweep point (one reference `run()`).
+// Lane x owns instance x's scalar state in registers (busy time, ledger,
+// batch counters); lane q also owns queue q. All control flow is
+// warp-uniform: every lane executes the same event handler and reads other
+// lanes' state with shuffles. Data-parallel work — advancing every request of
+// a decode batch, joins, moves, admission scans, argmax
+// searches for eviction / preemption / rebalancing —
+// runs across the 32 lanes over SoA arrays in the per-warp HBM arena with
+// coalesced accesses.
+//
+// Semantics: docs/SEMANTICS.md (identical decisions to the CPU oracle, which
+// is written independently with per-request structs and std::vector
+// batches). The code compiles both for sm_100a and, with KVSIM_EMU, for the
+// host SIMT emulator used by the CPU test-suite.
+#pragma once
+#include "kvsim_gpu.h"
+#include "kvsim_math.cuh"
+#include "kvsim_simt.cuh"
+
+namespace kvsim_dev {
+using namespace kvsim_math;
+
+constexpr int kMaxInst = 32;
+constexpr int32_t kRemMask = 0x1fffffff;
+constexpr int32_t kJoin = 0x40000000;  // no decode step since joining the batch
+constexpr int32_t kCopy = 0x20000000;  // holds a redundant copy on the partner
+enum { ROLE_DECODE = 0, ROLE_PREFILL = 1 };
+enum { JOB_NONE = 0, JOB_PREFILL = 1, JOB_STEP = 2 };
+
+// Per-warp shared scratch (atomics and radix histograms only; all simulation
+// state lives in registers or the HBM arena).
+struct WarpScratch {
+  int64_t acc_a[kMaxInst];
+  int64_t acc_b[kMaxInst];
+  int32_t cnt[kMaxInst];
+  uint32_t hist[2][256];
+};
+
+// Kernel arguments: inputs, outputs and the arena (one slot per resident warp).
+struct SweepArgs {
+  const kvsim_point_desc* pts;
+  const int64_t* order;  // nullable: launch order (LPT) -> point index
+  int64_t n_pts;
+  kvsim_point_summary* out;
+  // caller traces (concatenated), per-trace offset / count / max decode
+  const double* tr_arr;
+  const int32_t* tr_pl;
+  const int32_t* tr_dl;
+  const int64_t* tr_off;
+  const int64_t* tr_n;
+  const int32_t* tr_dmax;
+  // optional outputs
+  kvsim_request_record* recs;
+  const int64_t* rec_off;
+  kvsim_event_record* ev;
+  int64_t ev_cap;
+  int64_t* ev_count;
+  // arena geometry
+  int64_t Ncap, Bcap, Jcap;
+  int32_t Imax, slots;
+  // cold per-request arrays [slot][Ncap]
+  double *c_arr, *c_last, *c_tbt, *c_fresh, *c_first, *c_done;
+  int32_t *c_pl, *c_dl, *c_qlen, *c_em, *c_cpy, *c_nmv, *c_npre;
+  int32_t* q_rid;  // [slot][Imax][Ncap] queue rings
+  int32_t *b_rid, *b_rem, *b_kvb;
+  double* b_tbt;  // [slot][Imax][Bcap] batch SoA
+  int32_t* i_rid;
+  double* i_ready;  // [slot][Imax][Bcap] incoming lists
+  int32_t *j_rid, *j_dst;  // [slot][Imax][Jcap] prefill job members
+  double* link;            // [slot][Imax][Imax] directed link busy-until
+  unsigned long long* next_point;
+};
+
+struct Sim {
+  const SweepArgs& A;
+  WarpScratch* W;
+  int lane;
+  int64_t point;
+  // arena (slot-local)
+  double *c_arr, *c_last, *c_tbt, *c_fresh, *c_first, *c_done;
+  int32_t *c_pl, *c_dl, *c_qlen, *c_em, *c_cpy, *c_nmv, *c_npre;
+  int32_t* q_rid;
+  int32_t *b_rid_, *b_rem_, *b_kvb_;
+  double* b_tbt_;
+  int32_t* i_rid_;
+  double* i_ready_;
+  int32_t *j_rid_, *j_dst_;
+  double* link_;
+  int64_t Ncap, Bcap, Jcap;
+  // point constants
+  Perf f;
+  int32_t policy, n, n_prefill, fixed_arrivals;
+  int32_t pmin, pmax, dmin, dmax;
+  int64_t budget, n_limit, event_budget;
+  double warmup, duration, rate;
+  uint64_t key;
+  const double* tr_arr;
+  const int32_t *tr_pl, *tr_dl;
+  // arrival generator
+  double t_next, t_prev;
+  int64_t next_rid;
+  bool has_next;
+  // uniform counters
+  int64_t n_events, n_steps, n_prefills, n_moves, n_preempt, n_evict;
+  int64_t tok_total, tok_window, pf_tokens, mir_tokens, ev_n;
+  double now;
+  int32_t status;
+  kvsim_event_record* ev;
+  int64_t ev_cap;
+  // lane-owned instance state (lane x <-> instance x)
+  double L_busy_until, L_job_start, L_prev_end, L_mirror_fin, L_busy_time, L_min_ready, L_link;
+  int64_t L_used, L_peak, L_skv, L_skv_in, L_job_s1, L_copy_tok;
+  int32_t L_role, L_job, L_nb, L_ni, L_pend, L_njob, L_ncopy;
+  // lane-owned queue state (lane q <-> queue q)
+  int32_t Q_head, Q_n;
+  int64_t Q_tok;
+
+  KV_DEV Sim(const SweepArgs& a, WarpScratch* w, int64_t slot) : A(a), W(w) {
+    lane = simt::lane_id();
+    Ncap = a.Ncap;
+    Bcap = a.Bcap;
+    Jcap = a.Jcap;
+    const int64_t cs = slot * Ncap;
+    c_arr = a.c_arr + cs; c_last = a.c_last + cs; c_tbt = a.c_tbt + cs; c_fresh = a.c_fresh + cs;
+    c_first = a.c_first + cs; c_done = a.c_done + cs;
+    c_pl = a.c_pl + cs; c_dl = a.c_dl + cs; c_qlen = a.c_qlen + cs; c_em = a.c_em + cs;
+    c_cpy = a.c_cpy + cs; c_nmv = a.c_nmv + cs; c_npre = a.c_npre + cs;
+    q_rid = a.q_rid + slot * (int64_t)a.Imax * Ncap;
+    const int64_t bs = slot * (int64_t)a.Imax * Bcap;
+    b_rid_ = a.b_rid + bs; b_rem_ = a.b_rem + bs; b_kvb_ = a.b_kvb + bs; b_tbt_ = a.b_tbt + bs;
+    i_rid_ = a.i_rid + bs; i_ready_ = a.i_ready + bs;
+    const int64_t js = slot * (int64_t)a.Imax * Jcap;
+    j_rid_ = a.j_rid + js; j_dst_ = a.j_dst + js;
+    link_ = a.link + slot * (int64_t)a.Imax * a.Imax;
+  }
+
+  // ------------------------------------------------------------ accessors
+  KV_DEV int32_t* b_rid(int x) { return b_rid_ + (int64_t)x * Bcap; }
+  KV_DEV int32_t* b_rem(int x) { return b_rem_ + (int64_t)x * Bcap; }
+  KV_DEV int32_t* b_kvb(int x) { return b_kvb_ + (int64_t)x * Bcap; }
+  KV_DEV double* b_tbt(int x) { return b_tbt_ + (int64_t)x * Bcap; }
+  KV_DEV int32_t* i_rid(int x) { return i_rid_ + (int64_t)x * Bcap; }
+  KV_DEV double* i_ready(int x) { return i_ready_ + (int64_t)x * Bcap; }
+  KV_DEV int32_t* j_rid(int x) { return j_rid_ + (int64_t)x * Jcap; }
+  KV_DEV int32_t* j_dst(int x) { return j_dst_ + (int64_t)x * Jcap; }
+  KV_DEV int32_t* ring(int q) { return q_rid + (int64_t)q * Ncap; }
+
+  template <class T>
+  KV_DEV T get(T v, int x) { return simt::shfl(v, x); }
+  KV_DEV bool own(int x) const { return lane == x; }
+  KV_DEV int queue_of(int x) const {
+    return policy == KVSIM_POLICY_UNIFIED ? x : policy == KVSIM_POLICY_SPLITWISE ? 0 : (x >> 1);
+  }
+  KV_DEV void add_used(int x, int64_t tok) {
+    if (own(x)) {
+      L_used += tok;
+      if (L_used > L_peak) L_peak = L_used;
+    }
+  }
+
+  KV_DEV void log(int kind, int inst, int a, int b, int64_t c) {
+    if (ev != nullptr && lane == 0 && ev_n < ev_cap) {
+      kvsim_event_record r;
+      r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
+      ev[ev_n] = r;
+    }
+    ev_n += 1;
+  }
+  // lane-parallel logging: lanes with `p` log one record each (moves)
+  KV_DEV void log_lanes(bool p, int kind, int inst, int a, int b, int64_t c) {
+    unsigned m = simt::ballot(p);
+    if (ev != nullptr && p) {
+      int64_t k = ev_n + simt::popc(m & simt::lanemask_lt());
+      if (k < ev_cap) {
+        kvsim_event_record r;
+        r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
+        ev[k] = r;
+      }
+    }
+    ev_n += simt::popc(m);
+  }
+
+  // ------------------------------------------------------------- queues
+  KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
+    int32_t h = get(Q_head, q), c = get(Q_n, q);
+    int64_t idx = (int64_t)h + c;
+    if (idx >= Ncap) idx -= Ncap;
+    if (lane == 0) ring(q)[idx] = rid;
+    simt::sync();
+    if (own(q)) { Q_n += 1; Q_tok += len; }
+  }
+  KV_DEV void q_push_front(int q, int32_t rid, int64_t len) {
+    int32_t h = get(Q_head, q);
+    int32_t nh = h == 0 ? (int32_t)(Ncap - 1) : h - 1;
+    if (lane == 0) ring(q)[nh] = rid;
+    simt::sync();
+    if (own(q)) { Q_head = nh; Q_n += 1; Q_tok += len; }
+  }
+  KV_DEV int32_t q_at(int q, int32_t h, int64_t k) {
+    int64_t idx = (int64_t)h + k;
+    if (idx >= Ncap) idx -= Ncap;
+    return ring(q)[idx];
+  }
+  KV_DEV void q_pop(int q, int32_t k, int64_t tokens) {
+    if (own(q)) {
+      int64_t nh = (int64_t)Q_head + k;
+      if (nh >= Ncap) nh -= Ncap;
+      Q_head = (int32_t)nh;
+      Q_n -= k;
+      Q_tok -= tokens;
+    }
+  }
+
+  // ------------------------------------------------------------ point init
+  KV_DEV bool init_point(int64_t p) {
+    point = p;
+    const kvsim_point_desc& d = A.pts[p];
+    f = make_perf(d);
+    policy = d.policy;
+    n = d.num_instances;
+    n_prefill = 0;
+    if (policy == KVSIM_POLICY_SPLITWISE)
+      n_prefill = d.num_prefill_instances > 0 ? d.num_prefill_instances : (n + 2) / 4;
+    budget = d.prefill_token_budget > 0 ? d.prefill_token_budget : 8192;
+    fixed_arrivals = d.arrival_process == KVSIM_ARRIVAL_FIXED;
+    pmin = d.prompt_min; pmax = d.prompt_max; dmin = d.decode_min; dmax = d.decode_max;
+    warmup = d.warmup_s;
+    duration = d.duration_s;
+    rate = d.rate;
+    key = stream_key(d.seed);
+    status = KVSIM_OK;
+    int64_t nreq = d.num_requests < Ncap ? d.num_requests : Ncap;
+    int32_t evd = dmax;
+    if (d.trace_index >= 0) {
+      const int64_t off = A.tr_off[d.trace_index];
+      tr_arr = A.tr_arr + off; tr_pl = A.tr_pl + off; tr_dl = A.tr_dl + off;
+      int64_t tn = A.tr_n[d.trace_index];
+      n_limit = tn < nreq ? tn : nreq;
+      evd = A.tr_dmax[d.trace_index];
+    } else {
+      tr_arr = nullptr; tr_pl = nullptr; tr_dl = nullptr;
+      n_limit = rate > 0.0 ? nreq : 0;
+    }
+    event_budget = 4 * n_limit * ((int64_t)(evd > 1 ? evd : 1) + 2) + 4096;
+    // validity (perfmodel validate())
+    if (n < 1 || n > kMaxInst || n > A.Imax || policy < 0 || policy > 2) status = KVSIM_E_INVALID;
+    else if (policy == KVSIM_POLICY_ACCELLM && (n & 1)) status = KVSIM_E_ODD_INSTANCES;
+    else if (policy == KVSIM_POLICY_SPLITWISE && (n < 2 || n_prefill >= n)) status = KVSIM_E_INVALID;
+    else if (!f.fits) status = KVSIM_E_MODEL_FIT;
+    n_events = n_steps = n_prefills = n_moves = n_preempt = n_evict = 0;
+    tok_total = tok_window = pf_tokens = mir_tokens = ev_n = 0;
+    now = 0.0;
+    ev = A.ev ? A.ev + p * A.ev_cap : nullptr;
+    ev_cap = A.ev_cap;
+    L_busy_until = L_job_start = L_prev_end = L_mirror_fin = L_busy_time = 0.0;
+    L_min_ready = as_f64(0x7ff0000000000000ull);
+    L_link = 0.0;
+    L_used = L_peak = L_skv = L_skv_in = L_job_s1 = L_copy_tok = 0;
+    L_role = (policy == KVSIM_POLICY_SPLITWISE && lane < n_prefill) ? ROLE_PREFILL : ROLE_DECODE;
+    L_job = JOB_NONE;
+    L_nb = L_ni = L_pend = L_njob = L_ncopy = 0;
+    Q_head = 0; Q_n = 0; Q_tok = 0;
+    // splitwise directed links
+    if (policy == KVSIM_POLICY_SPLITWISE)
+      for (int i = lane; i < n * n; i += 32) link_[i] = 0.0;
+    next_rid = 0;
+    t_prev = 0.0;
+    has_next = false;
+    if (status == KVSIM_OK) gen_next();
+    simt::sync();
+    return status == KVSIM_OK;
+  }
+
+  // arrival generator (SEMANTICS §2); uniform across lanes
+  KV_DEV void gen_next() {
+    has_next = false;
+    if (next_rid >= n_limit) return;
+    double t;
+    if (tr_arr != nullptr) {
+      t = tr_arr[next_rid];
+    } else if (fixed_arrivals) {
+      t = kdiv((double)next_rid, rate);
+      if (!(t < duration)) return;
+    } else {
+      const double g = poisson_gap(key, next_rid, rate);
+      t = next_rid == 0 ? g : kadd(t_prev, g);
+      if (!(t < duration)) return;
+    }
+    t_next = t;
+    has_next = true;
+  }
+
+  // ------------------------------------------------------------- emission
+  // token emission for a request leaving a prefill (first or recompute token)
+  // by this lane; returns emitted count after.
+  KV_DEV int32_t emit_prefill_token(int32_t rid, double t) {
+    int32_t em = c_em[rid];
+    if (em == 0) {
+      c_first[rid] = t;
+    } else {
+      double gap = ksub(t, c_last[rid]);
+      if (gap > c_tbt[rid]) c_tbt[rid] = gap;
+    }
+    c_last[rid] = t;
+    em += 1;
+    c_em[rid] = em;
+    return em;
+  }
+  KV_DEV void count_tokens(int64_t k, double t) {
+    tok_total += k;
+    if (t >= warmup) tok_window += k;
+  }
+  KV_DEV void account_job(int x, double t) {
+    double js = get(L_job_start, x);
+    if (own(x) && js >= warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
+  }
+
+  // ------------------------------------------------------- hot decode loop
+  // Advances every member of x's batch by one token at time t
+  // and compacts completions away. Returns completed count; accumulates the
+  // kv (before the step) of completed requests, the kv-after of completed
+  // requests holding a copy, and the number of members holding a copy.
+  struct StepOut {
+    int32_t nb_old, completed, m_copies, copy_done;
+    int64_t kv_done, copy_free;
+  };
+  KV_DEV StepOut step_loop(int x, double t) {
+    StepOut o;
+    const int32_t nb = get(L_nb, x);
+    const double prev = get(L_prev_end, x);
+    int32_t* rid_a = b_rid(x);
+    int32_t* rem_a = b_rem(x);
+    int32_t* kvb_a = b_kvb(x);
+    double* tbt_a = b_tbt(x);
+    int32_t wpos = 0, completed = 0, m = 0, copy_done = 0;
+    int64_t kv_done = 0, copy_free = 0;  // per-lane partials
+    for (int32_t j0 = 0; j0 < nb; j0 += 32) {
+      const int32_t j = j0 + lane;
+      const bool act = j < nb;
+      int32_t rf = 0, rid = 0, kvb = 0;
+      double tb = 0.0;
+      if (act) {
+        rf = rem_a[j];
+        tb = tbt_a[j];
+      }
+      const int32_t rem = (rf & kRemMask) - 1;
+      const bool joiner = (rf & kJoin) != 0;
+      const bool hasc = (rf & kCopy) != 0;
+      const bool done = act && rem == 0;
+      const bool surv = act && rem != 0;
+      const unsigned sm = simt::ballot(surv);
+      const int32_t dst = wpos + simt::popc(sm & simt::lanemask_lt());
+      const bool moved = surv && dst != j;
+      if (act && (joiner || done || moved)) rid = rid_a[j];
+      double gap = 0.0;
+      bool upd = false;
+      if (act) {
+        const double last = joiner ? c_last[rid] : prev;
+        gap = ksub(t, last);
+        upd = gap > tb;
+        if (upd) tb = gap;
+      }
+      if (done || moved) kvb = kvb_a[j];
+      m += simt::popc(simt::ballot(act && hasc));
+      simt::sync();  // all reads of this chunk precede its compaction writes
+      if (surv) {
+        rem_a[dst] = rem | (rf & kCopy);
+        if (moved) {
+          rid_a[dst] = rid;
+          kvb_a[dst] = kvb;
+          tbt_a[dst] = tb;
+        } else if (upd) {
+          tbt_a[dst] = tb;
+        }
+      }
+      if (done) {
+        c_done[rid] = t;
+        c_tbt[rid] = tb;
+        c_em[rid] = c_dl[rid];
+        const int64_t kvbef = (int64_t)kvb - 1;  // kv before the step: kvb - (rem+1), rem == 0
+        kv_done += kvbef;
+        if (hasc) copy_free += kvbef + 1;
+      }
+      const unsigned dm = simt::ballot(done);
+      completed += simt::popc(dm);
+      copy_done += simt::popc(simt::ballot(done && hasc));
+      wpos += simt::popc(sm);
+    }
+    o.nb_old = nb;
+    o.completed = completed;
+    o.m_copies = m;
+    o.copy_done = copy_done;
+    o.kv_done = simt::warp_sum(kv_done);
+    o.copy_free = simt::warp_sum(copy_free);
+    simt::sync();
+    return o;
+  }
+
+  // -------------------------------------------------------------- joins
+  KV_DEV void join(int x, double t) {
+    const int32_t ni = get(L_ni, x);
+    if (ni == 0) return;
+    if (get(L_min_ready, x) > t) return;
+    const int32_t nb = get(L_nb, x);
+    int32_t* irid = i_rid(x);
+    double* irdy = i_ready(x);
+    int32_t keep = 0, add = 0, ncopy = 0;
+    int64_t kvsum = 0;
+    double mn = as_f64(0x7ff0000000000000ull);
+    for (int32_t j0 = 0; j0 < ni; j0 += 32) {
+      const int32_t j = j0 + lane;
+      const bool act = j < ni;
+      int32_t rid = 0;
+      double rd = 0.0;
+      if (act) { rid = irid[j]; rd = irdy[j]; }
+      const bool go = act && rd <= t;
+      const bool stay = act && !go;
+      const unsigned gm = simt::ballot(go), sm = simt::ballot(stay);
+      simt::sync();
+      if (stay) {
+        const int32_t k = keep + simt::popc(sm & simt::lanemask_lt());
+        irid[k] = rid;
+        irdy[k] = rd;
+        if (rd < mn) mn = rd;
+      }
+      if (go) {
+        const int32_t k = nb + add + simt::popc(gm & simt::lanemask_lt());
+        const int32_t em = c_em[rid], dl = c_dl[rid], pl = c_pl[rid];
+        const bool hasc = c_cpy[rid] >= 0;
+        b_rid(x)[k] = rid;
+        b_rem(x)[k] = (dl - em) | kJoin | (hasc ? kCopy : 0);
+        b_kvb(x)[k] = pl + dl - 1;
+        b_tbt(x)[k] = c_tbt[rid];
+        kvsum += (int64_t)pl + em - 1;
+      }
+      ncopy += simt::popc(simt::ballot(go && c_cpy[go ? rid : 0] >= 0));
+      keep += simt::popc(sm);
+      add += simt::popc(gm);
+    }
+    kvsum = simt::warp_sum(kvsum);
+    mn = simt::warp_min(mn);
+    simt::sync();
+    if (own(x)) {
+      L_nb += add;
+      L_ni -= add;
+      L_skv += kvsum;
+      L_skv_in -= kvsum;
+      L_ncopy += ncopy;
+      L_min_ready = mn;
+    }
+    if (add) log(KVSIM_EV_JOIN, x, add, 0, 0);
+  }
+
+  // remove batch slot idx of instance x by moving the last slot into it
+  KV_DEV void batch_remove(int x, int32_t idx) {
+    const int32_t last = get(L_nb, x) - 1;
+    if (lane == 0 && idx != last) {
+      b_rid(x)[idx] = b_rid(x)[last];
+      b_rem(x)[idx] = b_rem(x)[last];
+      b_kvb(x)[idx] = b_kvb(x)[last];
+      b_tbt(x)[idx] = b_tbt(x)[last];
+    }
+    simt::sync();
+    if (own(x)) L_nb -= 1;
+  }
+  KV_DEV void incoming_remove(int x, int32_t idx) {
+    const int32_t last = get(L_ni, x) - 1;
+    if (lane == 0 && idx != last) {
+      i_rid(x)[idx] = i_rid(x)[last];
+      i_ready(x)[idx] = i_ready(x)[last];
+    }
+    simt::sync();
+    if (own(x)) L_ni -= 1;
+  }
+  KV_DEV void incoming_append(int y, int32_t rid, double ready) {
+    const int32_t k = get(L_ni, y);
+    if (lane == 0) {
+      i_rid(y)[k] = rid;
+      i_ready(y)[k] = ready;
+    }
+    simt::sync();
+    if (own(y)) {
+      L_ni += 1;
+      if (ready < L_min_ready) L_min_ready = ready;
+    }
+  }
+
+  // ------------------------------------------------------- copies (AcceLLM)
+  struct Found {
+    int32_t rid, idx, where;  // where: 0 none, 1 batch of partner, 2 incoming of partner
+    int64_t kv;
+  };
+  // largest redundant copy held on instance x (max kv, ties lowest rid)
+  KV_DEV Found largest_copy_on(int x) {
+    const int y = x ^ 1;
+    uint64_t best = 0;
+    int32_t bidx = -1, bwhere = 0;
+    const int32_t nb = get(L_nb, y), ni = get(L_ni, y);
+    for (int32_t j = lane; j < nb; j += 32) {
+      const int32_t rf = b_rem(y)[j];
+      if (rf & kCopy) {
+        const int64_t kv = (int64_t)b_kvb(y)[j] - (rf & kRemMask);
+        const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(y)[j]);
+        if (k > best) { best = k; bidx = j; bwhere = 1; }
+      }
+    }
+    for (int32_t j = lane; j < ni; j += 32) {
+      const int32_t rid = i_rid(y)[j];
+      if (c_cpy[rid] == x) {
+        const int64_t kv = (int64_t)c_pl[rid] + c_em[rid] - 1;
+        const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - rid);
+        if (k > best) { best = k; bidx = j; bwhere = 2; }
+      }
+    }
+    const uint64_t wbest = simt::warp_max(best);
+    Found r;
+    r.where = 0; r.idx = -1; r.rid = -1; r.kv = 0;
+    if (wbest == 0) return r;
+    const unsigned holder = simt::ballot(best == wbest);
+    const int src = simt::ffs(holder) - 1;
+    r.idx = simt::shfl(bidx, src);
+    r.where = simt::shfl(bwhere, src);
+    r.rid = 0x7fffffff - (int32_t)(uint32_t)(wbest & 0xffffffffu);
+    r.kv = (int64_t)(wbest >> 32);
+    return r;
+  }
+  KV_DEV void evict(int x, const Found& v) {
+    const int y = x ^ 1;
+    int64_t held = v.kv;
+    if (v.where == 1) {
+      if (get(L_job, y) == JOB_STEP) held += 1;
+      if (lane == 0) b_rem(y)[v.idx] &= ~kCopy;
+      if (own(y)) L_ncopy -= 1;
+    } else {
+      if (lane == 0) c_cpy[v.rid] = -1;
+    }
+    simt::sync();
+    if (own(x)) { L_used -= held; L_copy_tok -= held; }
+    n_evict += 1;
+    log(KVSIM_EV_EVICT, x, v.rid, 0, 0);
+  }
+
+  // ------------------------------------------------------ preemption (P9)
+  KV_DEV void preempt_newest(int x) {
+    const int32_t nb = get(L_nb, x);
+    int32_t best = -1, bidx = -1;
+    for (int32_t j = lane; j < nb; j += 32) {
+      const int32_t r = b_rid(x)[j];
+      if (r > best) { best = r; bidx = j; }
+    }
+    const int32_t rid = simt::warp_max(best);
+    const int src = simt::ffs(simt::ballot(best == rid)) - 1;
+    const int32_t idx = simt::shfl(bidx, src);
+    const int32_t rf = b_rem(x)[idx];
+    const int32_t rem = rf & kRemMask;
+    const int64_t kv = (int64_t)b_kvb(x)[idx] - rem;
+    const int32_t dl = c_dl[rid], pl = c_pl[rid];
+    const int32_t em = dl - rem;
+    const double tb = b_tbt(x)[idx];
+    const double last = (rf & kJoin) ? c_last[rid] : get(L_prev_end, x);
+    const int32_t qlen = pl + em;
+    simt::sync();
+    if (lane == 0) {
+      c_em[rid] = em;
+      c_tbt[rid] = tb;
+      c_last[rid] = last;
+      c_cpy[rid] = -1;
+      c_qlen[rid] = qlen;
+      c_npre[rid] += 1;
+    }
+    if (own(x)) { L_used -= kv; L_skv -= kv; }
+    if (rf & kCopy) {
+      const int y = x ^ 1;
+      if (own(y)) { L_used -= kv; L_copy_tok -= kv; }
+      if (own(x)) L_ncopy -= 1;
+    }
+    batch_remove(x, idx);
+    n_preempt += 1;
+    log(KVSIM_EV_PREEMPT, x, rid, qlen, 0);
+    q_push_front(queue_of(x), rid, qlen);
+  }
+
+  // ------------------------------------------------------------ link FIFO
+  KV_DEV double link_get(int s, int d) {
+    if (policy == KVSIM_POLICY_ACCELLM) return get(L_link, s);  // only (s, s^1)
+    return link_[s * n + d];
+  }
+  KV_DEV void link_set(int s, int d, double v) {
+    if (policy == KVSIM_POLICY_ACCELLM) {
+      if (own(s)) L_link = v;
+    } else {
+      simt::sync();  // every lane has read the old value
+      if (lane == 0) link_[s * n + d] = v;
+      simt::sync();
+    }
+  }
+  KV_DEV double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
+    const double busy = link_get(s, d);
+    const double tail = kadd(t_done, transfer_latency(f, kmul((double)s1, f.kvb_layer)));
+    const double start = t_start > busy ? t_start : busy;
+    const double full = kadd(start, transfer_latency(f, kmul((double)s1, f.kvb)));
+    const double fin = tail > full ? tail : full;
+    link_set(s, d, fin);
+    pf_tokens += s1;
+    log(KVSIM_EV_TRANSFER, s, d, 0, s1);
+    return fin;
+  }
+
+  // ------------------------------------------- decode step (splitwise/accellm)
+  KV_DEV void step_start(int x, double t) {
+    int32_t nb = get(L_nb, x);
+    if (nb == 0) return;
+    const bool acc = policy == KVSIM_POLICY_ACCELLM;
+    bool preempted = false;
+    for (;;) {
+      if (get(L_used, x) + nb <= f.cap) break;
+      if (acc) {
+        Found v = largest_copy_on(x);
+        if (v.where) { evict(x, v); continue; }
+      }
+      preempt_newest(x);
+      preempted = true;
+      nb -= 1;
+      if (nb == 0) break;
+    }
+    if (nb == 0) {
+      if (preempted && acc) ensure_prefill(x >> 1, t);
+      return;
+    }
+    if (acc) {
+      const int y = x ^ 1;
+      for (;;) {
+        const int32_t m = get(L_ncopy, x);
+        if (get(L_used, y) + m <= f.cap) {
+          add_used(y, m);
+          if (own(y)) L_copy_tok += m;
+          break;
+        }
+        Found v = largest_copy_on(y);
+        evict(y, v);
+      }
+    }
+    const int64_t K = get(L_skv, x);
+    add_used(x, nb);
+    const double lat = decode_latency(f, nb, K);
+    if (own(x)) {
+      L_job = JOB_STEP;
+      L_job_start = t;
+      L_busy_until = kadd(t, lat);
+    }
+    log(KVSIM_EV_STEP_START, x, nb, 0, K);
+    if (preempted && acc) ensure_prefill(x >> 1, t);
+  }
+
+  KV_DEV void step_end(int x, double t) {
+    account_job(x, t);
+    n_steps += 1;
+    const StepOut o = step_loop(x, t);
+    const int32_t surv = o.nb_old - o.completed;
+    if (own(x)) {
+      L_job = JOB_NONE;
+      L_used -= o.kv_done + o.completed;
+      L_skv = L_skv - o.kv_done + surv;
+      L_nb = surv;
+      L_prev_end = t;
+    }
+    count_tokens(o.nb_old, t);
+    if (policy == KVSIM_POLICY_ACCELLM) {
+      const int y = x ^ 1;
+      if (own(y)) { L_used -= o.copy_free; L_copy_tok -= o.copy_free; }
+      if (own(x)) L_ncopy -= o.copy_done;
+      if (o.m_copies > 0) {
+        const double busy = get(L_link, x);
+        const double start = t > busy ? t : busy;
+        const double fin = kadd(start, transfer_latency(f, kmul((double)o.m_copies, f.kvb)));
+        if (own(x)) { L_link = fin; L_mirror_fin = fin; }
+        mir_tokens += o.m_copies;
+        log(KVSIM_EV_TRANSFER, x, y, 1, o.m_copies);
+      }
+    }
+    log(KVSIM_EV_STEP_END, x, o.nb_old, o.completed, 0);
+  }
+
+  // ------------------------------------------------------------- unified
+  KV_DEV void unified_start(int x, double t) {
+    int32_t nb = get(L_nb, x);
+    while (get(L_used, x) + nb > f.cap) {
+      preempt_newest(x);
+      nb -= 1;
+    }
+    add_used(x, nb);
+    const int64_t K = get(L_skv, x);
+    // FCFS admission under budget and memory (prefix-closed tests)
+    const int32_t h = get(Q_head, x), qn = get(Q_n, x);
+    int64_t used = get(L_used, x);
+    int32_t k = 0;
+    int64_t s1 = 0, s2 = 0;
+    while (k < qn) {
+      const int32_t i = k + lane;
+      const bool valid = i < qn;
+      int32_t rid = 0;
+      int64_t len = 0;
+      if (valid) { rid = q_at(x, h, i); len = c_qlen[rid]; }
+      const int64_t incl = simt::warp_incl_scan(len);
+      const bool okb = (k == 0 && lane == 0) || s1 + incl <= budget;
+      const bool okm = used + incl <= f.cap;
+      const unsigned fail = simt::ballot(valid && !(okb && okm));
+      const int32_t nvalid = simt::popc(simt::ballot(valid));
+      const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
+      if (lane < take) j_rid(x)[k + lane] = rid;
+      const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
+      const int64_t tsq = simt::warp_sum(lane < take ? len * len : (int64_t)0);
+      s1 += tsum;
+      s2 += tsq;
+      used += tsum;
+      k += take;
+      if (take < nvalid || fail) break;
+    }
+    simt::sync();
+    if (k > 0) {
+      q_pop(x, k, s1);
+      add_used(x, s1);
+    }
+    if (nb == 0 && k == 0) return;
+    const double lat = kadd(k ? prefill_latency(f, s1, s2) : 0.0, nb ? decode_latency(f, nb, K) : 0.0);
+    if (own(x)) {
+      L_job = JOB_STEP;
+      L_job_start = t;
+      L_busy_until = kadd(t, lat);
+      L_njob = k;
+      L_job_s1 = s1;
+    }
+    log(KVSIM_EV_STEP_START, x, nb, k, K);
+  }
+
+  KV_DEV void unified_end(int x, double t) {
+    account_job(x, t);
+    n_steps += 1;
+    const StepOut o = step_loop(x, t);
+    int32_t nb = o.nb_old - o.completed;
+    int64_t skv = get(L_skv, x) - o.kv_done + nb;
+    int64_t freed = o.kv_done + o.completed;
+    count_tokens(o.nb_old, t);
+    // co-batched prefills emit and join (non-joiners: their last token is t)
+    const int32_t k = get(L_njob, x);
+    int32_t completed = o.completed, add = 0;
+    int64_t kvadd = 0, kvfree = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      int32_t rid = 0, em = 0, dl = 0, pl = 0;
+      if (act) {
+        rid = j_rid(x)[i];
+        em = emit_prefill_token(rid, t);
+        dl = c_dl[rid];
+        pl = c_pl[rid];
+      }
+      const bool done = act && em == dl;
+      const bool join = act && !done;
+      if (done) { c_done[rid] = t; kvfree += (int64_t)pl + em - 1; }
+      const unsigned jm = simt::ballot(join);
+      if (join) {
+        const int32_t pos = nb + add + simt::popc(jm & simt::lanemask_lt());
+        b_rid(x)[pos] = rid;
+        b_rem(x)[pos] = dl - em;
+        b_kvb(x)[pos] = pl + dl - 1;
+        b_tbt(x)[pos] = c_tbt[rid];
+        kvadd += (int64_t)pl + em - 1;
+      }
+      add += simt::popc(jm);
+      completed += simt::popc(simt::ballot(done));
+    }
+    kvadd = simt::warp_sum(kvadd);
+    kvfree = simt::warp_sum(kvfree);
+    simt::sync();
+    count_tokens(k, t);
+    if (k > 0) n_prefills += 1;
+    if (own(x)) {
+      L_job = JOB_NONE;
+      L_used -= freed + kvfree;
+      L_skv = skv + kvadd;
+      L_nb = nb + add;
+      L_prev_end = t;
+      L_njob = 0;
+    }
+    log(KVSIM_EV_STEP_END, x, o.nb_old, completed, 0);
+    unified_start(x, t);
+  }
+
+  // ------------------------------------------------------------ splitwise
+  KV_DEV void sw_try_start(double t) {
+    for (int p = 0; p < n_prefill; ++p) {
+      if (get(L_job, p) != JOB_NONE) continue;
+      int32_t qn = get(Q_n, 0);
+      if (qn == 0) continue;
+      const int32_t h = get(Q_head, 0);
+      int32_t k = 0;
+      int64_t s1 = 0, s2 = 0;
+      bool stop = false;
+      while (!stop && k < qn) {
+        // prefetch a chunk of queue entries into lanes
+        const int32_t i = k + lane;
+        const bool valid = i < qn;
+        int32_t crid = 0, clen = 0;
+        if (valid) { crid = q_at(0, h, i); clen = c_qlen[crid]; }
+        const int32_t nvalid = simt::popc(simt::ballot(valid));
+        for (int32_t c = 0; c < nvalid; ++c) {
+          const int32_t rid = simt::shfl(crid, c);
+          const int64_t len = simt::shfl(clen, c);
+          if (k > 0 && s1 + len > budget) { stop = true; break; }
+          // destination: decode instance with most free tokens, ties lowest id
+          int64_t fr = (lane >= n_prefill && lane < n) ? f.cap - L_used : INT64_MIN;
+          const int64_t best = simt::warp_max(fr);
+          const int d = simt::ffs(simt::ballot(fr == best)) - 1;
+          if (best < len) { stop = true; break; }
+          add_used(d, len);
+          if (lane == 0) { j_rid(p)[k] = rid; j_dst(p)[k] = d; }
+          s1 += len;
+          s2 += len * len;
+          k += 1;
+        }
+      }
+      simt::sync();
+      if (k == 0) continue;
+      q_pop(0, k, s1);
+      add_used(p, s1);
+      const double lat = prefill_latency(f, s1, s2);
+      if (own(p)) {
+        L_job = JOB_PREFILL;
+        L_job_start = t;
+        L_busy_until = kadd(t, lat);
+        L_njob = k;
+        L_job_s1 = s1;
+      }
+      log(KVSIM_EV_PREFILL_START, p, k, j_rid(p)[0], s1);
+    }
+  }
+
+  KV_DEV void sw_prefill_done(int p, double t) {
+    account_job(p, t);
+    n_prefills += 1;
+    const int32_t k = get(L_njob, p);
+    const int64_t s1 = get(L_job_s1, p);
+    const double jstart = get(L_job_start, p);
+    if (own(p)) { L_job = JOB_NONE; L_used -= s1; }
+    if (lane < kMaxInst) { W->acc_a[lane] = 0; W->acc_b[lane] = 0; W->cnt[lane] = 0; }
+    simt::sync();
+    int32_t completed = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      bool done = false;
+      if (act) {
+        const int32_t rid = j_rid(p)[i];
+        const int32_t d = j_dst(p)[i];
+        const int32_t em = emit_prefill_token(rid, t);
+        const int32_t dl = c_dl[rid];
+        const int64_t kv = (int64_t)c_pl[rid] + em - 1;
+        done = em == dl;
+        if (done) {
+          c_done[rid] = t;
+          simt::atomic_add_smem(&W->acc_b[d], kv);
+        } else {
+          simt::atomic_add_smem(&W->acc_a[d], kv);
+          simt::atomic_add_smem(&W->cnt[d], 1);
+        }
+      }
+      completed += simt::popc(simt::ballot(done));
+    }
+    simt::sync();
+    count_tokens(k, t);
+    log(KVSIM_EV_PREFILL_DONE, p, k, completed, 0);
+    // one transfer per destination, ascending id; lane d keeps the finish time
+    double fin_mine = 0.0;
+    int32_t base_mine = 0;
+    for (int d = n_prefill; d < n; ++d) {
+      const int64_t tok = W->acc_a[d];
+      const int64_t fr = W->acc_b[d];
+      if (own(d)) { L_used -= fr; }
+      if (tok == 0) continue;
+      const double fin = prefill_transfer(p, d, tok, jstart, t);
+      if (own(d)) {
+        fin_mine = fin;
+        base_mine = L_ni;
+        L_ni += W->cnt[d];
+        L_skv_in += tok;
+        if (fin < L_min_ready) L_min_ready = fin;
+      }
+    }
+    simt::sync();
+    if (lane < kMaxInst) W->cnt[lane] = 0;
+    simt::sync();
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      int32_t rid = 0, d = 0;
+      if (act) { rid = j_rid(p)[i]; d = j_dst(p)[i]; }
+      const double fin_d = simt::shfl(fin_mine, d);
+      const int32_t base_d = simt::shfl(base_mine, d);
+      if (act && c_em[rid] != c_dl[rid]) {
+        const int32_t pos = base_d + simt::atomic_add_smem(&W->cnt[d], 1);
+        i_rid(d)[pos] = rid;
+        i_ready(d)[pos] = fin_d;
+        c_cpy[rid] = -1;
+      }
+    }
+    simt::sync();
+  }
+
+  // -------------------------------------------------------------- accellm
+  KV_DEV int64_t load_of(int x) { return get(L_skv, x) + get(L_skv_in, x); }
+  KV_DEV bool head_admissible(int x) {
+    const int q = x >> 1;
+    if (get(Q_n, q) == 0) return false;
+    const int32_t rid = q_at(q, get(Q_head, q), 0);
+    const int64_t len = c_qlen[rid];
+    return get(L_used, x) - get(L_copy_tok, x) + len <= f.cap;
+  }
+  // move every request whose primary is x and that holds a copy on x^1
+  KV_DEV void move_all_to_partner(int x, double t) {
+    const int y = x ^ 1;
+    const double mfin = get(L_mirror_fin, x);
+    const double pend = get(L_prev_end, x);
+    int32_t nb = get(L_nb, x);
+    int32_t ni_y = get(L_ni, y);
+    int32_t keep = 0, moved = 0;
+    int64_t kv_moved = 0;
+    double mn = as_f64(0x7ff0000000000000ull);
+    // batch members
+    for (int32_t j0 = 0; j0 < nb; j0 += 32) {
+      const int32_t j = j0 + lane;
+      const bool act = j < nb;
+      int32_t rid = 0, rf = 0, kvb = 0;
+      double tb = 0.0;
+      if (act) { rid = b_rid(x)[j]; rf = b_rem(x)[j]; kvb = b_kvb(x)[j]; tb = b_tbt(x)[j]; }
+      const bool mv = act && (rf & kCopy);
+      const bool st = act && !mv;
+      const unsigned mm = simt::ballot(mv), sm = simt::ballot(st);
+      simt::sync();
+      if (st) {
+        const int32_t k = keep + simt::popc(sm & simt::lanemask_lt());
+        b_rid(x)[k] = rid; b_rem(x)[k] = rf; b_kvb(x)[k] = kvb; b_tbt(x)[k] = tb;
+      }
+      if (mv) {
+        const int32_t rem = rf & kRemMask;
+        const bool joiner = (rf & kJoin) != 0;
+        const double fresh = joiner ? c_fresh[rid] : mfin;
+        const double ready = fresh > t ? fresh : t;
+        const int32_t dl = c_dl[rid];
+        c_em[rid] = dl - rem;
+        c_tbt[rid] = tb;
+        if (!joiner) c_last[rid] = pend;
+        c_cpy[rid] = x;
+        c_fresh[rid] = t;
+        c_nmv[rid] += 1;
+        const int32_t pos = ni_y + moved + simt::popc(mm & simt::lanemask_lt());
+        i_rid(y)[pos] = rid;
+        i_ready(y)[pos] = ready;
+        kv_moved += (int64_t)kvb - rem;
+        if (ready < mn) mn = ready;
+      }
+      log_lanes(mv, KVSIM_EV_MOVE, x, rid, y, 0);
+      keep += simt::popc(sm);
+      moved += simt::popc(mm);
+    }
+    const int32_t moved_b = moved;
+    const int64_t kv_b = simt::warp_sum(kv_moved);
+    kv_moved = 0;
+    // incoming entries of x that hold a copy on y
+    const int32_t ni = get(L_ni, x);
+    int32_t ikeep = 0;
+    for (int32_t j0 = 0; j0 < ni; j0 += 32) {
+      const int32_t j = j0 + lane;
+      const bool act = j < ni;
+      int32_t rid = 0;
+      double rd = 0.0;
+      if (act) { rid = i_rid(x)[j]; rd = i_ready(x)[j]; }
+      const bool mv = act && c_cpy[act ? rid : 0] == y;
+      const bool st = act && !mv;
+      const unsigned mm = simt::ballot(mv), sm = simt::ballot(st);
+      simt::sync();
+      if (st) {
+        const int32_t k = ikeep + simt::popc(sm & simt::lanemask_lt());
+        i_rid(x)[k] = rid;
+        i_ready(x)[k] = rd;
+      }
+      if (mv) {
+        const double fresh = c_fresh[rid];
+        const double ready = fresh > t ? fresh : t;
+        c_cpy[rid] = x;
+        c_fresh[rid] = t;
+        c_nmv[rid] += 1;
+        const int32_t pos = ni_y + moved + simt::popc(mm & simt::lanemask_lt());
+        i_rid(y)[pos] = rid;
+        i_ready(y)[pos] = ready;
+        kv_moved += (int64_t)c_pl[rid] + c_em[rid] - 1;
+        if (ready < mn) mn = ready;
+      }
+      log_lanes(mv, KVSIM_EV_MOVE, x, rid, y, 0);
+      ikeep += simt::popc(sm);
+      moved += simt::popc(mm);
+    }
+    const int64_t kv_i = simt::warp_sum(kv_moved);
+    mn = simt::warp_min(mn);
+    // min ready of what stays in x's incoming
+    double mx = as_f64(0x7ff0000000000000ull);
+    for (int32_t j = lane; j < ikeep; j += 32) {
+      const double r = i_ready(x)[j];
+      if (r < mx) mx = r;
+    }
+    mx = simt::warp_min(mx);
+    simt::sync();
+    const int64_t kv_all = kv_b + kv_i;
+    n_moves += moved;
+    if (own(x)) {
+      L_nb = keep;
+      L_ni = ikeep;
+      L_skv -= kv_b;
+      L_skv_in -= kv_i;
+      L_ncopy -= moved_b;
+      L_copy_tok += kv_all;
+      L_min_ready = mx;
+    }
+    if (own(y)) {
+      L_ni += moved;
+      L_skv_in += kv_all;
+      L_copy_tok -= kv_all;
+      if (mn < L_min_ready) L_min_ready = mn;
+    }
+  }
+
+  KV_DEV void acc_start_job(int x, double t) {
+    const int q = x >> 1;
+    const int32_t h = get(Q_head, q);
+    int32_t k = 0;
+    int64_t s1 = 0, s2 = 0;
+    for (;;) {
+      const int32_t qn = get(Q_n, q);
+      if (k >= qn) break;
+      const int32_t i = k + lane;
+      const bool valid = i < qn;
+      int32_t rid = 0;
+      int64_t len = 0;
+      if (valid) { rid = q_at(q, h, i); len = c_qlen[rid]; }
+      const int64_t incl = simt::warp_incl_scan(len);
+      const int64_t used = get(L_used, x);
+      const bool okb = (k == 0 && lane == 0) || s1 + incl <= budget;
+      const bool okm = used + incl <= f.cap;
+      const unsigned fail = simt::ballot(valid && !(okb && okm));
+      const int32_t nvalid = simt::popc(simt::ballot(valid));
+      const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
+      if (lane < take) j_rid(x)[k + lane] = rid;
+      const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
+      const int64_t tsq = simt::warp_sum(lane < take ? len * len : (int64_t)0);
+      s1 += tsum;
+      s2 += tsq;
+      k += take;
+      add_used(x, tsum);
+      if (!fail) continue;
+      const int f0 = simt::ffs(fail) - 1;
+      const bool fb = simt::shfl((int32_t)okb, f0) != 0;
+      const int64_t lenf = simt::shfl(len, f0);
+      if (!fb) break;
+      // memory: evict copies held on x, largest first
+      while (get(L_used, x) + lenf > f.cap) {
+        Found v = largest_copy_on(x);
+        if (!v.where) break;
+        evict(x, v);
+      }
+      if (get(L_used, x) + lenf > f.cap) break;
+    }
+    simt::sync();
+    q_pop(q, k, s1);
+    const double lat = prefill_latency(f, s1, s2);
+    if (own(x)) {
+      L_job = JOB_PREFILL;
+      L_job_start = t;
+      L_busy_until = kadd(t, lat);
+      L_njob = k;
+      L_job_s1 = s1;
+    }
+    log(KVSIM_EV_PREFILL_START, x, k, k ? j_rid(x)[0] : -1, s1);
+  }
+
+  KV_DEV bool try_switch(int x, double t) {
+    if (!head_admissible(x)) return false;
+    if (own(x)) L_pend = 0;
+    move_all_to_partner(x, t);
+    if (own(x)) L_role = ROLE_PREFILL;
+    log(KVSIM_EV_ROLE, x, ROLE_PREFILL, 0, 0);
+    acc_start_job(x, t);
+    return true;
+  }
+
+  KV_DEV void ensure_prefill(int q, double t) {
+    if (get(Q_n, q) == 0) return;
+    const int a = 2 * q, b = a + 1;
+    if (get(L_role, a) == ROLE_PREFILL || get(L_role, b) == ROLE_PREFILL || get(L_pend, a) || get(L_pend, b))
+      return;
+    const int m = load_of(b) < load_of(a) ? b : a;
+    if (get(L_job, m) == JOB_NONE) try_switch(m, t);
+    else if (own(m)) L_pend = 1;
+  }
+
+  // rebalance_pair at x's boundary (SEMANTICS §6)
+  KV_DEV void rebalance(int x, double t) {
+    const int y = x ^ 1;
+    if (get(L_role, y) != ROLE_DECODE || get(L_pend, y)) return;
+    int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
+    int64_t d = load_of(x) - load_of(y);
+    while (c >= 1 && d >= 1) {
+      // largest candidate (kv desc, rid asc) with kv <= d (kv < d when c == 1)
+      const int64_t lim = c >= 2 ? d : d - 1;
+      const int32_t nb = get(L_nb, x);
+      uint64_t best = 0;
+      int32_t bidx = -1;
+      for (int32_t j = lane; j < nb; j += 32) {
+        const int32_t rf = b_rem(x)[j];
+        if (rf & kCopy) {
+          const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
+          if (kv <= lim) {
+            const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
+            if (kk > best) { best = kk; bidx = j; }
+          }
+        }
+      }
+      const uint64_t wb = simt::warp_max(best);
+      if (wb == 0) break;
+      const int src = simt::ffs(simt::ballot(best == wb)) - 1;
+      const int32_t idx = simt::shfl(bidx, src);
+      const int64_t kv = (int64_t)(wb >> 32);
+      move_one(x, idx, t);
+      c -= 2;
+      d -= 2 * kv;
+    }
+  }
+  // move batch slot idx of x to y's incoming (zero-byte label swap)
+  KV_DEV void move_one(int x, int32_t idx, double t) {
+    const int y = x ^ 1;
+    const int32_t rid = b_rid(x)[idx];
+    const int32_t rf = b_rem(x)[idx];
+    const int32_t rem = rf & kRemMask;
+    const int64_t kv = (int64_t)b_kvb(x)[idx] - rem;
+    const double tb = b_tbt(x)[idx];
+    const bool joiner = (rf & kJoin) != 0;
+    const double fresh = joiner ? c_fresh[rid] : get(L_mirror_fin, x);
+    const double ready = fresh > t ? fresh : t;
+    const double last = joiner ? c_last[rid] : get(L_prev_end, x);
+    const int32_t dl = c_dl[rid];
+    simt::sync();
+    if (lane == 0) {
+      c_em[rid] = dl - rem;
+      c_tbt[rid] = tb;
+      c_last[rid] = last;
+      c_cpy[rid] = x;
+      c_fresh[rid] = t;
+      c_nmv[rid] += 1;
+    }
+    batch_remove(x, idx);
+    incoming_append(y, rid, ready);
+    if (own(x)) { L_skv -= kv; L_ncopy -= 1; L_copy_tok += kv; }
+    if (own(y)) { L_skv_in += kv; L_copy_tok -= kv; }
+    n_moves += 1;
+    log(KVSIM_EV_MOVE, x, rid, y, 0);
+  }
+
+  KV_DEV void acc_boundary(int x, double t) {
+    join(x, t);
+    if (get(L_pend, x)) {
+      if (own(x)) L_pend = 0;
+      if (try_switch(x, t)) return;
+    }
+    ensure_prefill(x >> 1, t);
+    if (get(L_role, x) == ROLE_PREFILL) return;
+    rebalance(x, t);
+    step_start(x, t);
+  }
+
+  KV_DEV void acc_prefill_done(int x, double t) {
+    account_job(x, t);
+    n_prefills += 1;
+    const int y = x ^ 1;
+    const int32_t k = get(L_njob, x);
+    const double jstart = get(L_job_start, x);
+    if (own(x)) L_job = JOB_NONE;
+    // pass 1: emission, completions; survivors' kv
+    int32_t completed = 0;
+    int64_t kvfree = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      bool done = false;
+      if (act) {
+        const int32_t rid = j_rid(x)[i];
+        const int32_t em = emit_prefill_token(rid, t);
+        done = em == c_dl[rid];
+        if (done) {
+          c_done[rid] = t;
+          kvfree += (int64_t)c_pl[rid] + em - 1;
+        }
+      }
+      completed += simt::popc(simt::ballot(done));
+    }
+    kvfree = simt::warp_sum(kvfree);
+    simt::sync();
+    if (own(x)) L_used -= kvfree;
+    count_tokens(k, t);
+    log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
+    // pass 2: redundant copies on y in job order while they fit
+    int64_t used_y = get(L_used, y);
+    int64_t s1c = 0;
+    int32_t ncopy = 0;
+    bool seq = false;  // once a survivor does not fit, decide one by one
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      int32_t rid = 0;
+      bool surv = false;
+      int64_t kv = 0;
+      if (act) {
+        rid = j_rid(x)[i];
+        surv = c_em[rid] != c_dl[rid];
+        if (surv) kv = (int64_t)c_pl[rid] + c_em[rid] - 1;
+      }
+      bool cp = false;
+      if (!seq) {
+        const int64_t incl = simt::warp_incl_scan(kv);
+        const bool fits = used_y + incl <= f.cap;
+        const unsigned bad = simt::ballot(surv && !fits);
+        if (!bad) {
+          cp = surv;
+          used_y += simt::shfl(incl, 31);
+        } else {
+          const int f0 = simt::ffs(bad) - 1;
+          cp = surv && lane < f0;
+          used_y += simt::shfl(incl, f0) - simt::shfl(kv, f0);
+          seq = true;
+          for (int l = f0; l < 32; ++l) {
+            const bool sl = simt::shfl((int32_t)surv, l) != 0;
+            const int64_t kl = simt::shfl(kv, l);
+            if (sl && used_y + kl <= f.cap) {
+              used_y += kl;
+              if (lane == l) cp = true;
+            }
+          }
+        }
+      } else {
+        for (int l = 0; l < 32; ++l) {
+          const bool sl = simt::shfl((int32_t)surv, l) != 0;
+          const int64_t kl = simt::shfl(kv, l);
+          if (sl && used_y + kl <= f.cap) {
+            used_y += kl;
+            if (lane == l) cp = true;
+          }
+        }
+      }
+      if (cp) c_cpy[rid] = y;
+      else if (surv) c_cpy[rid] = -1;
+      s1c += simt::warp_sum(cp ? kv : (int64_t)0);
+      ncopy += simt::popc(simt::ballot(cp));
+    }
+    simt::sync();
+    add_used(y, s1c);
+    if (own(y)) L_copy_tok += s1c;
+    if (ncopy) log(KVSIM_EV_COPY, y, ncopy, 0, s1c);
+    double fin = 0.0;
+    if (s1c > 0) fin = prefill_transfer(x, y, s1c, jstart, t);
+    // pass 3: survivors join x's batch as joiners (last token = t)
+    const int32_t nb = get(L_nb, x);
+    int32_t add = 0, addc = 0;
+    int64_t kvadd = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      int32_t rid = 0;
+      bool surv = false;
+      if (act) {
+        rid = j_rid(x)[i];
+        surv = c_em[rid] != c_dl[rid];
+      }
+      const unsigned sm = simt::ballot(surv);
+      if (surv) {
+        const int32_t em = c_em[rid], dl = c_dl[rid], pl = c_pl[rid];
+        const bool hasc = c_cpy[rid] == y;
+        if (hasc) c_fresh[rid] = fin;
+        const int32_t pos = nb + add + simt::popc(sm & simt::lanemask_lt());
+        b_rid(x)[pos] = rid;
+        b_rem(x)[pos] = (dl - em) | kJoin | (hasc ? kCopy : 0);
+        b_kvb(x)[pos] = pl + dl - 1;
+        b_tbt(x)[pos] = c_tbt[rid];
+        kvadd += (int64_t)pl + em - 1;
+      }
+      addc += simt::popc(simt::ballot(surv && c_cpy[surv ? rid : 0] == y));
+      add += simt::popc(sm);
+    }
+    kvadd = simt::warp_sum(kvadd);
+    simt::sync();
+    if (own(x)) { L_nb += add; L_skv += kvadd; L_ncopy += addc; L_njob = 0; }
+    if (head_admissible(x)) {
+      move_all_to_partner(x, t);
+      acc_start_job(x, t);
+      return;
+    }
+    if (own(x)) L_role = ROLE_DECODE;
+    log(KVSIM_EV_ROLE, x, ROLE_DECODE, 0, 0);
+    acc_boundary(x, t);
+  }
+
+  // -------------------------------------------------------------- arrival
+  KV_DEV void arrive(double t) {
+    const int64_t rid64 = next_rid;
+    const int32_t rid = (int32_t)rid64;
+    int32_t pl, dl;
+    if (tr_arr != nullptr) {
+      pl = tr_pl[rid];
+      dl = tr_dl[rid];
+    } else {
+      pl = uniform_range(draw_k(key, rid64, 0), pmin, pmax);
+      dl = uniform_range(draw_k(key, rid64, 1), dmin, dmax);
+    }
+    if (lane == 0) {
+      c_arr[rid] = t;
+      c_pl[rid] = pl;
+      c_dl[rid] = dl;
+      c_qlen[rid] = pl;
+      c_em[rid] = 0;
+      c_cpy[rid] = -1;
+      c_tbt[rid] = 0.0;
+      c_last[rid] = 0.0;
+      c_fresh[rid] = 0.0;
+      c_first[rid] = 0.0;
+      c_done[rid] = 0.0;
+      c_nmv[rid] = 0;
+      c_npre[rid] = 0;
+    }
+    simt::sync();
+    // advance the generator
+    t_prev = t;
+    next_rid += 1;
+    gen_next();
+    if (policy == KVSIM_POLICY_UNIFIED) {
+      const int64_t fr = lane < n ? f.cap - L_used - Q_tok : INT64_MIN;
+      const int64_t best = simt::warp_max(fr);
+      const int x = simt::ffs(simt::ballot(fr == best)) - 1;
+      log(KVSIM_EV_ARRIVE, x, rid, pl, 0);
+      q_push_back(x, rid, pl);
+      if (get(L_job, x) == JOB_NONE) unified_start(x, t);
+    } else if (policy == KVSIM_POLICY_SPLITWISE) {
+      log(KVSIM_EV_ARRIVE, 0, rid, pl, 0);
+      q_push_back(0, rid, pl);
+    } else {
+      const int np = n >> 1;
+      const int64_t ua = simt::shfl(L_used, (2 * lane) & 31);
+      const int64_t ub = simt::shfl(L_used, (2 * lane + 1) & 31);
+      const int64_t fr = lane < np ? (f.cap - ua) + (f.cap - ub) - Q_tok : INT64_MIN;
+      const int64_t best = simt::warp_max(fr);
+      const int q = simt::ffs(simt::ballot(fr == best)) - 1;
+      log(KVSIM_EV_ARRIVE, q, rid, pl, 0);
+      q_push_back(q, rid, pl);
+      ensure_prefill(q, t);
+    }
+  }
+
+  // ------------------------------------------------------------ main loop
+  KV_DEV void run() {
+    const double kInf = as_f64(0x7ff0000000000000ull);
+    for (;;) {
+      double ct = kInf;
+      int32_t ck = 1 << 20;
+      if (lane < n) {
+        if (L_job != JOB_NONE) {
+          ct = L_busy_until;
+          ck = (L_job == JOB_PREFILL ? 2 : 3) * 64 + lane;
+        } else if (L_role == ROLE_DECODE && L_ni > 0) {
+          ct = L_min_ready;
+          ck = 1 * 64 + lane;
+        }
+      }
+      for (int m = 16; m; m >>= 1) {
+        const double ot = simt::shfl_xor(ct, m);
+        const int32_t ok = simt::shfl_xor(ck, m);
+        if (ot < ct || (ot == ct && ok < ck)) { ct = ot; ck = ok; }
+      }
+      bool is_arrival = false;
+      if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
+      if (!is_arrival && ck == (1 << 20)) break;
+      if (++n_events > event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
+      if (is_arrival) {
+        now = t_next;
+        arrive(t_next);
+      } else {
+        const double t = ct;
+        now = t;
+        const int kind = ck >> 6, x = ck & 63;
+        if (kind == 1) {
+          log(KVSIM_EV_WAKE, x, 0, 0, 0);
+          if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(x, t);
+          else { join(x, t); step_start(x, t); }
+        } else if (kind == 2) {
+          if (policy == KVSIM_POLICY_SPLITWISE) sw_prefill_done(x, t);
+          else acc_prefill_done(x, t);
+        } else {
+          if (policy == KVSIM_POLICY_UNIFIED) {
+            unified_end(x, t);
+          } else {
+            step_end(x, t);
+            if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(x, t);
+            else { join(x, t); step_start(x, t); }
+          }
+        }
+      }
+      if (policy == KVSIM_POLICY_SPLITWISE) sw_try_start(now);
+    }
+    simt::sync();
+  }
+
+  // --------------------------------------------- per-point metrics (K4 fused)
+  // nearest-rank selection over uint64 keys stored (as doubles' bits) in arr
+  KV_DEV void radix_select2(const double* arr, int64_t nn, int64_t k1, int64_t k2, uint64_t& r1, uint64_t& r2) {
+    uint64_t pre1 = 0, pre2 = 0, mask = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int b = lane; b < 256; b += 32) { W->hist[0][b] = 0; W->hist[1][b] = 0; }
+      simt::sync();
+      for (int64_t i = lane; i < nn; i += 32) {
+        const uint64_t kk = as_u64(arr[i]);
+        const uint32_t dg = (uint32_t)((kk >> shift) & 255u);
+        if ((kk & mask) == pre1) simt::atomic_add_smem(&W->hist[0][dg], 1u);
+        if ((kk & mask) == pre2) simt::atomic_add_smem(&W->hist[1][dg], 1u);
+      }
+      simt::sync();
+      // scan histograms (uniform, all lanes)
+      int64_t acc1 = 0, acc2 = 0;
+      int b1 = -1, b2 = -1;
+      for (int b = 0; b < 256; ++b) {
+        const int64_t h1 = W->hist[0][b], h2 = W->hist[1][b];
+        if (b1 < 0 && acc1 + h1 > k1) b1 = b; else if (b1 < 0) acc1 += h1;
+        if (b2 < 0 && acc2 + h2 > k2) b2 = b; else if (b2 < 0) acc2 += h2;
+      }
+      k1 -= acc1;
+      k2 -= acc2;
+      pre1 |= (uint64_t)b1 << shift;
+      pre2 |= (uint64_t)b2 << shift;
+      mask |= (uint64_t)255u << shift;
+      simt::sync();
+    }
+    r1 = pre1;
+    r2 = pre2;
+  }
+
+  KV_DEV void finalize() {
+    kvsim_point_summary s;
+    // zero everything
+    {
+      char* z = reinterpret_cast<char*>(&s);
+      for (unsigned i = 0; i < sizeof(s); ++i) z[i] = 0;
+    }
+    const kvsim_point_desc& d = A.pts[point];
+    const double kNaN = as_f64(0x7ff8000000000000ull);
+    const double kInf = as_f64(0x7ff0000000000000ull);
+    s.status = status;
+    s.num_instances = (status == KVSIM_OK || status == KVSIM_E_EVENT_BUDGET) ? n : 0;
+    s.user_tag = d.user_tag;
+    const int64_t N = next_rid;  // requests that arrived
+    s.n_requests = status == KVSIM_OK ? N : 0;
+    if (status == KVSIM_OK || status == KVSIM_E_EVENT_BUDGET) {
+      s.n_requests = N;
+      s.n_events = n_events; s.n_steps = n_steps; s.n_prefills = n_prefills; s.n_moves = n_moves;
+      s.n_preemptions = n_preempt; s.n_evictions = n_evict;
+      s.tokens_total = tok_total; s.tokens_window = tok_window;
+      s.link_prefill_tokens = pf_tokens; s.link_mirror_tokens = mir_tokens;
+      s.makespan_s = now;
+      const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
+      double busy = 0.0;
+      for (int x = 0; x < n; ++x) busy = kadd(busy, get(L_busy_time, x));
+      s.peak_kv_tokens = peak;
+      s.busy_s_total = busy;
+      s.peak_kv_gb = kdiv(kmul((double)peak, f.kvb), 1e9);
+      s.link_prefill_gb = kdiv(kmul((double)pf_tokens, f.kvb), 1e9);
+      s.link_mirror_gb = kdiv(kmul((double)mir_tokens, f.kvb), 1e9);
+      // records (parity configs)
+      if (A.recs != nullptr) {
+        kvsim_request_record* R = A.recs + A.rec_off[point];
+        for (int64_t i = lane; i < N; i += 32) {
+          const bool dn = c_em[i] == c_dl[i];
+          kvsim_request_record r;
+          r.arrival_s = c_arr[i];
+          r.first_token_s = c_em[i] > 0 ? c_first[i] : kNaN;
+          r.completion_s = dn ? c_done[i] : kNaN;
+          r.tbt_max_s = c_tbt[i];
+          r.prompt_len = c_pl[i];
+          r.decode_len = c_dl[i];
+          r.n_moves = c_nmv[i];
+          r.n_preemptions = c_npre[i];
+          R[i] = r;
+        }
+      }
+      simt::sync();
+      // sequential (rid-order) sums, maxima; keys for selection
+      double s_ttft = 0.0, s_jct = 0.0, s_tbt = 0.0, tmax = 0.0;
+      int64_t n_tbt = 0, m = 0, completed = 0;
+      double mx_ttft = 0.0, mx_jct = 0.0;
+      for (int64_t i0 = 0; i0 < N; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const bool act = i < N;
+        double a = 0.0, b = 0.0, tb = 0.0, ts = 0.0;
+        bool inc = false, dn = false;
+        int32_t dl = 0;
+        if (act) {
+          const double arr = c_arr[i];
+          dl = c_dl[i];
+          dn = c_em[i] == dl;
+          inc = dn && arr >= warmup;
+          if (inc) {
+            a = ksub(c_first[i], arr);
+            b = ksub(c_done[i], arr);
+            ts = ksub(c_done[i], c_first[i]);
+            tb = c_tbt[i];
+          }
+        }
+        simt::sync();
+        if (act) {
+          c_first[i] = inc ? a : kInf;
+          c_done[i] = inc ? b : kInf;
+        }
+        completed += simt::popc(simt::ballot(dn));
+        const int cnt = act ? 1 : 0;
+        (void)cnt;
+        const int lim = (int)((N - i0) < 32 ? (N - i0) : 32);
+        for (int l = 0; l < lim; ++l) {
+          const bool il = simt::shfl((int32_t)inc, l) != 0;
+          const double al = simt::shfl(a, l), bl = simt::shfl(b, l), tsl = simt::shfl(ts, l);
+          const double tbl = simt::shfl(tb, l);
+          const int32_t dll = simt::shfl(dl, l);
+          if (il) {
+            m += 1;
+            s_ttft = kadd(s_ttft, al);
+            s_jct = kadd(s_jct, bl);
+            if (al > mx_ttft) mx_ttft = al;
+            if (bl > mx_jct) mx_jct = bl;
+            if (dll > 1) {
+              s_tbt = kadd(s_tbt, tsl);
+              n_tbt += dll - 1;
+              if (tbl > tmax) tmax = tbl;
+            }
+          }
+        }
+      }
+      simt::sync();
+      s.n_completed = completed;
+      s.n_measured = m;
+      if (m > 0) {
+        s.ttft_mean = kdiv(s_ttft, (double)m);
+        s.jct_mean = kdiv(s_jct, (double)m);
+        s.ttft_max = mx_ttft;
+        s.jct_max = mx_jct;
+        const int64_t k50 = (50 * m + 99) / 100 - 1, k95 = (95 * m + 99) / 100 - 1;
+        uint64_t r1, r2;
+        radix_select2(c_first, N, k50, k95, r1, r2);
+        s.ttft_p50 = as_f64(r1);
+        s.ttft_p95 = as_f64(r2);
+        radix_select2(c_done, N, k50, k95, r1, r2);
+        s.jct_p50 = as_f64(r1);
+        s.jct_p95 = as_f64(r2);
+      } else {
+        s.ttft_mean = s.jct_mean = s.ttft_p50 = s.ttft_p95 = s.ttft_max = kNaN;
+        s.jct_p50 = s.jct_p95 = s.jct_max = kNaN;
+      }
+      s.tbt_mean = n_tbt > 0 ? kdiv(s_tbt, (double)n_tbt) : kNaN;
+      s.tbt_max = n_tbt > 0 ? tmax : kNaN;
+      const double window = ksub(now, warmup);
+      if (window > 0.0) {
+        s.cost_eff = kdiv((double)tok_window, kmul(window, (double)n));
+        s.idle_frac = ksub(1.0, kdiv(busy, kmul((double)n, window)));
+      } else {
+        s.cost_eff = s.idle_frac = kNaN;
+      }
+    }
+    simt::sync();
+    if (lane == 0) {
+      A.out[point] = s;
+      if (A.ev_count != nullptr) A.ev_count[point] = ev_n;
+    }
+    simt::sync();
+  }
+};
+
+// Persistent warp loop: pull points from a global counter (LPT order is set
+// by the host), simulate, finalize.
+KV_DEV void sweep_warp(const SweepArgs& a, WarpScratch* w, int64_t slot) {
+  Sim sim(a, w, slot);
+  for (;;) {
+    unsigned long long p = 0;
+#if defined(KVSIM_EMU)
+    if (sim.lane == 0) p = std::atomic_ref<unsigned long long>(*a.next_point).fetch_add(1);
+#else
+    if (sim.lane == 0) p = atomicAdd(a.next_point, 1ull);
+#endif
+    p = simt::shfl((uint64_t)p, 0);
+    if ((int64_t)p >= a.n_pts) break;
+    const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
+    if (sim.init_point(pt)) sim.run();
+    sim.finalize();
+  }
+}
+
+}  // namespace kvsim_dev

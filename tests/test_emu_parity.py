@@ -1,0 +1,46 @@
+"""CPU CI for the kernel logic: the sm_100a simulation core
+(csrc/kvsim_sim.cuh) compiled for the host SIMT emulator must reproduce the
+independent CPU oracle bit for bit — summaries, per-request records and the
+decision/event log — on the SPEC closed form, BASELINE config 1 and the
+SPEC.md:469 randomized small-config suite (with memory-starved variants)."""
+import pytest
+
+from configs import closed_form_point, config1, config2, config3, random_small
+from harness import diff_results, run_oracle, run_points_emu
+
+EV = 1 << 16
+
+
+def check(points, ev=EV):
+    got = run_points_emu(points, ev_cap=ev, warps=4)
+    bad = []
+    for p, g in zip(points, got):
+        d = diff_results(run_oracle(p, ev_cap=ev), g)
+        if d:
+            bad.append((p.policy, p.num_instances, p.num_requests, d[:4]))
+    assert not bad, bad
+
+
+def test_closed_form_and_config1():
+    check([closed_form_point(), config1(seed=0, n=120), config1(seed=1, n=120)])
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_random_small_configs(chunk):
+    check([random_small(i) for i in range(chunk * 25, chunk * 25 + 25)])
+
+
+def test_config2_config3_small():
+    pts = [config2(pol, 6.0, n=60) for pol in ("unified", "splitwise", "accellm")]
+    pts += [config3(pol, 2.0, n=40) for pol in ("unified", "splitwise", "accellm")]
+    check(pts)
+
+
+def test_invalid_points_reported():
+    from paper_2411_05555_b200.abi import make_point
+    pts = [make_point(policy="accellm", instances=3, num_requests=5),
+           make_point(policy="accellm", instances=2, num_requests=5, device=(1e12, 10e9, 1e12, 1e9))]
+    got = run_points_emu(pts, ev_cap=0, recs=False)
+    assert got[0].status == -3 and got[1].status == -2
+    for p, g in zip(pts, got):
+        assert run_oracle(p, ev_cap=0, recs=False).status == g.status
