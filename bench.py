@@ -1,0 +1,301 @@
+"""bench.py — simulated requests/s of a kvsim sweep on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 4 — 3 policies x instance counts {4,8,12,16} x
+833 request rates linearly spaced in (0, 3*N_inst] req/s, 10k requests per
+point, mixed workload, Llama-2-70B on simulated H100 instances, seed = point
+index (9,996 points, ~1e8 simulated requests). A step = one full sweep.
+
+  value  device-resident sweep (points already in HBM), CUDA events on the
+         launch stream, max over ranks
+  e2e    the same sweep through the reference-facing C-ABI call with host
+         buffers (kvsim_gpu_run: H2D points, kernel, D2H summaries)
+  --impl reference  the CPU oracle (restated reference simulator) on all host
+         threads over a bounded sample of the same points
+
+Multi-GPU (torchrun): each rank runs its own config-4 grid with a disjoint
+seed range (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2411_05555_b200.abi import PointDesc, PointSummary, make_point  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def config4_points(seed_base=0, n_rates=833, n_req=10000, policies=("unified", "splitwise", "accellm"),
+                   instances=(4, 8, 12, 16)):
+    pts = []
+    k = 0
+    for pol in policies:
+        for ni in instances:
+            for j in range(n_rates):
+                rate = 3.0 * ni * (j + 1) / n_rates
+                pts.append(make_point(model="llama2-70b", device="h100", policy=pol, instances=ni, rate=rate,
+                                      num_requests=n_req, workload="mixed", seed=seed_base + k, user_tag=k))
+                k += 1
+    return pts
+
+
+def algorithmic_bytes(summaries):
+    # B_req = 16 (trace) + 24 (TTFT/TBT/JCT record) + 8 * S_req,
+    # S_req = decode iterations = decode_len - 1 => sum = tokens_total - n_requests
+    n = sum(s.n_requests for s in summaries)
+    tok = sum(s.tokens_total for s in summaries)
+    return 40 * n + 8 * (tok - n)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    def __init__(self, device=0):
+        self.samples = []
+        self.stop = threading.Event()
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", "-i", str(self.device),
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "--format=csv,noheader,nounits", "-lms", "200"]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for nm, v in zip(names, s[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def cpu_reference(points, budget_s, threads):
+    """Time the CPU oracle (restated reference simulator) on a bounded,
+    deterministic subsample of the points (every k-th), all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from harness import oracle  # test infrastructure: the checker / CPU baseline only
+    L = oracle()
+    # calibrate on a tiny slice, then choose a stride so the run takes ~budget_s
+    probe = points[:: max(1, len(points) // 48)][:48]
+    P = (PointDesc * len(probe))(*probe)
+    S = (PointSummary * len(probe))()
+    t0 = time.perf_counter()
+    L.kvo_run_sweep(P, len(probe), threads, S)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_pt = dt / len(probe)
+    n_take = max(threads, min(len(points), int(budget_s / per_pt)))
+    stride = max(1, len(points) // n_take)
+    sample = points[::stride]
+    P = (PointDesc * len(sample))(*sample)
+    S = (PointSummary * len(sample))()
+    t0 = time.perf_counter()
+    L.kvo_run_sweep(P, len(sample), threads, S)
+    dt = time.perf_counter() - t0
+    reqs = sum(s.n_requests for s in S)
+    return reqs / dt, len(sample), stride, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kvsim", choices=["kvsim", "reference"])
+    ap.add_argument("--rates", type=int, default=833)
+    ap.add_argument("--requests", type=int, default=10000)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_cpu = os.cpu_count() or 1
+    metric = "simulated requests/sec (sweep, 1-8 B200) vs ref CPU; HBM GB/s fraction"
+    workload = (f"BASELINE config 4: 3 policies x instances {{4,8,12,16}} x {args.rates} rates in (0,3N] req/s, "
+                f"{args.requests} requests/point, mixed, Llama-2-70B on simulated H100")
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        pts = config4_points(0, args.rates, args.requests)
+        vals = []
+        for _ in range(args.warmup):
+            cpu_reference(pts, min(3.0, args.cpu_budget / 4), n_cpu)
+        info = None
+        for _ in range(args.steps):
+            v, ns, stride, dt = cpu_reference(pts, args.cpu_budget / max(args.steps, 1), n_cpu)
+            vals.append(v)
+            info = (ns, stride, dt)
+        v = statistics.median(vals)
+        line = {"metric": metric, "value": v, "unit": "simulated requests/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": info[2] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (device-RNG-equivalent traces from the seeded generator)",
+                "impl": "reference",
+                "config": {"workload": workload, "parallelism": f"{n_cpu} host threads"},
+                "cpu_baseline": {"value": v, "unit": "simulated requests/s", "cores": n_cpu, "kind": "port",
+                                 "sample": f"every {info[1]}th point of the sweep ({info[0]} points x "
+                                           f"{args.requests} requests) per step"},
+                "e2e": {"value": v, "unit": "simulated requests/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    torch.cuda.set_device(dev)
+    import paper_2411_05555_b200 as pkg
+    sim = pkg.KvSim(dev)
+    pts = config4_points(rank * 1_000_000, args.rates, args.requests)
+    n = len(pts)
+    P = (PointDesc * n)(*pts)
+    # device-resident inputs / outputs (torch owns the memory)
+    d_pts = torch.frombuffer(bytearray(bytes(P)), dtype=torch.uint8).to(f"cuda:{dev}")
+    d_out = torch.empty(n * C.sizeof(PointSummary), dtype=torch.uint8, device=f"cuda:{dev}")
+    sim.reserve(pts)
+    stream = torch.cuda.Stream(dev)  # non-default stream: the kernels and the events share it
+
+    def step():
+        sim.run_device(d_pts.data_ptr(), n, d_out.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            for a, b in ev:
+                a.record(stream)
+                step()
+                b.record(stream)
+        torch.cuda.synchronize(dev)
+    launches = args.steps * sim.last_launches()
+    times = [a.elapsed_time(b) / 1e3 for a, b in ev]
+    t_total = sum(times)
+    if dist:
+        t = torch.tensor([t_total], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_total = float(t.item())
+    host_out = d_out.cpu().numpy().tobytes()
+    summ = (PointSummary * n).from_buffer_copy(host_out)
+    bad = sum(1 for s in summ if s.status != 0)
+    reqs = sum(s.n_requests for s in summ)
+    total_reqs = reqs * world
+    value = total_reqs * args.steps / t_total
+    kernel_s = t_total / args.steps
+    bytes_alg = algorithmic_bytes(summ)
+    peaks, src = measured_peaks()
+    achieved = bytes_alg / kernel_s / 1e9
+    events = sum(s.n_events for s in summ)
+
+    # e2e: through the reference-facing C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h2d = n * C.sizeof(PointDesc)
+        d2h = n * C.sizeof(PointSummary)
+        tt = []
+        for i in range(max(1, args.steps)):
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            s2 = sim.run(pts)
+            tt.append(time.perf_counter() - t0)
+        te = sum(tt)
+        if dist:
+            t = torch.tensor([te], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        assert all(bytes(a) == bytes(b) for a, b in zip(s2, summ)), "e2e results differ from device-resident run"
+        e2e = {"value": total_reqs * len(tt) / te, "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        v, ns, stride, dt = cpu_reference(pts, args.cpu_budget, n_cpu)
+        cpu = {"value": v, "unit": "simulated requests/s", "cores": n_cpu, "kind": "port",
+               "sample": f"every {stride}th point of this sweep ({ns} points x {args.requests} requests), "
+                         f"{dt:.1f} s on {n_cpu} host threads (CPU oracle, one point per thread)"}
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": "simulated requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: requests generated on device by the seeded counter-based RNG (SEMANTICS §2)",
+            "config": {"workload": workload, "points_per_gpu": n, "requests_per_step_per_gpu": reqs,
+                       "parallelism": f"points sharded over {world} GPU(s), warp per point",
+                       "l2": "arena working set >> 126 MB L2 and rewritten every step (no flush needed)"},
+            "gpu_launches": launches,
+            "events_per_step_per_gpu": events,
+            "failed_points": bad,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"),
+                         "unit": "GB/s", "frac": achieved / peaks.get("hbm_gbs"), "traffic": None,
+                         "peak_source": src,
+                         "algorithmic_bytes_per_launch": bytes_alg,
+                         "note": "algorithmic bytes per SURVEY §8d (40 B/request + 8 B/decode iteration); "
+                                 "the kernel is bound by per-event issue latency, not HBM"},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,7 +178,8 @@ int kvsim_gpu_run(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
                   char* err, size_t err_len);
 
 /* Device-resident variant: d_pts / d_out are device pointers, generated traces
- * only, no records; launched on `stream` (cudaStream_t) without synchronising.
+ * only, no records; launched on `stream` (a cudaStream_t; NULL selects the
+ * context's own stream) without synchronising.
  * Used by bench.py to time the kernels with inputs already in HBM. */
 int kvsim_gpu_run_device(kvsim_gpu_ctx* ctx, const kvsim_point_desc* d_pts, size_t n,
                          kvsim_point_summary* d_out, void* stream,

@@ -109,14 +109,15 @@ class KvSim:
         rc = self.lib.kvsim_gpu_run(self.h, P, n, T, nt, S, R, E, events, cnt, self.err, 512)
         self._check(rc, "kvsim_gpu_run")
         summaries = list(S)
+        self.last_event_counts = list(cnt) if events else None
         if not records and not events:
             return summaries
         recs_out, ev_out, off = [], [], 0
         for i, p in enumerate(points):
             nr = max(int(p.num_requests), 0)
-            recs_out.append(list(R)[off:off + summaries[i].n_requests] if records else None)
+            recs_out.append(R[off:off + summaries[i].n_requests] if records else None)
             off += nr
-            ev_out.append(list(E)[i * events:i * events + min(cnt[i], events)] if events else None)
+            ev_out.append(E[i * events:i * events + min(cnt[i], events)] if events else None)
         return summaries, recs_out, ev_out
 
     def reserve(self, points):

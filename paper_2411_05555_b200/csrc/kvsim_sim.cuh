@@ -105,7 +105,10 @@ struct Sim {
   // uniform counters
   int64_t n_events, n_steps, n_prefills, n_moves, n_preempt, n_evict;
   int64_t tok_total, tok_window, pf_tokens, mir_tokens, ev_n;
-  double now;
+  int64_t n_loop;  // main-loop iterations actually executed (diagnostic)
+  double now;     // time of the event being processed (event-log timestamps)
+  double t_last;  // latest event time processed (makespan)
+  bool chain_steps = true;  // exact step chaining (fast_forward); off = plain event loop
   int32_t status;
   kvsim_event_record* ev;
   int64_t ev_cap;
@@ -113,6 +116,8 @@ struct Sim {
   double L_busy_until, L_job_start, L_prev_end, L_mirror_fin, L_busy_time, L_min_ready, L_link;
   int64_t L_used, L_peak, L_skv, L_skv_in, L_job_s1, L_copy_tok;
   int32_t L_role, L_job, L_nb, L_ni, L_pend, L_njob, L_ncopy;
+  int32_t L_minrem;  // lower bound of remaining tokens over the batch
+  int64_t L_final;   // splitwise: sum of final KV (prompt+decode-1) over batch + incoming
   // lane-owned queue state (lane q <-> queue q)
   int32_t Q_head, Q_n;
   int64_t Q_tok;
@@ -251,7 +256,9 @@ struct Sim {
     else if (!f.fits) status = KVSIM_E_MODEL_FIT;
     n_events = n_steps = n_prefills = n_moves = n_preempt = n_evict = 0;
     tok_total = tok_window = pf_tokens = mir_tokens = ev_n = 0;
+    n_loop = 0;
     now = 0.0;
+    t_last = 0.0;
     ev = A.ev ? A.ev + p * A.ev_cap : nullptr;
     ev_cap = A.ev_cap;
     L_busy_until = L_job_start = L_prev_end = L_mirror_fin = L_busy_time = 0.0;
@@ -261,6 +268,8 @@ struct Sim {
     L_role = (policy == KVSIM_POLICY_SPLITWISE && lane < n_prefill) ? ROLE_PREFILL : ROLE_DECODE;
     L_job = JOB_NONE;
     L_nb = L_ni = L_pend = L_njob = L_ncopy = 0;
+    L_minrem = 0x7fffffff;
+    L_final = 0;
     Q_head = 0; Q_n = 0; Q_tok = 0;
     // splitwise directed links
     if (policy == KVSIM_POLICY_SPLITWISE)
@@ -323,7 +332,7 @@ struct Sim {
   // kv (before the step) of completed requests, the kv-after of completed
   // requests holding a copy, and the number of members holding a copy.
   struct StepOut {
-    int32_t nb_old, completed, m_copies, copy_done;
+    int32_t nb_old, completed, m_copies, copy_done, minrem;
     int64_t kv_done, copy_free;
   };
   KV_DEV StepOut step_loop(int x, double t) {
@@ -334,7 +343,7 @@ struct Sim {
     int32_t* rem_a = b_rem(x);
     int32_t* kvb_a = b_kvb(x);
     double* tbt_a = b_tbt(x);
-    int32_t wpos = 0, completed = 0, m = 0, copy_done = 0;
+    int32_t wpos = 0, completed = 0, m = 0, copy_done = 0, minrem = 0x7fffffff;
     int64_t kv_done = 0, copy_free = 0;  // per-lane partials
     for (int32_t j0 = 0; j0 < nb; j0 += 32) {
       const int32_t j = j0 + lane;
@@ -366,6 +375,7 @@ struct Sim {
       m += simt::popc(simt::ballot(act && hasc));
       simt::sync();  // all reads of this chunk precede its compaction writes
       if (surv) {
+        if (rem < minrem) minrem = rem;
         rem_a[dst] = rem | (rf & kCopy);
         if (moved) {
           rid_a[dst] = rid;
@@ -394,6 +404,7 @@ struct Sim {
     o.copy_done = copy_done;
     o.kv_done = simt::warp_sum(kv_done);
     o.copy_free = simt::warp_sum(copy_free);
+    o.minrem = simt::warp_min(minrem);
     simt::sync();
     return o;
   }
@@ -406,7 +417,7 @@ struct Sim {
     const int32_t nb = get(L_nb, x);
     int32_t* irid = i_rid(x);
     double* irdy = i_ready(x);
-    int32_t keep = 0, add = 0, ncopy = 0;
+    int32_t keep = 0, add = 0, ncopy = 0, minrem = 0x7fffffff;
     int64_t kvsum = 0;
     double mn = as_f64(0x7ff0000000000000ull);
     for (int32_t j0 = 0; j0 < ni; j0 += 32) {
@@ -434,6 +445,7 @@ struct Sim {
         b_kvb(x)[k] = pl + dl - 1;
         b_tbt(x)[k] = c_tbt[rid];
         kvsum += (int64_t)pl + em - 1;
+        if (dl - em < minrem) minrem = dl - em;
       }
       ncopy += simt::popc(simt::ballot(go && c_cpy[go ? rid : 0] >= 0));
       keep += simt::popc(sm);
@@ -441,8 +453,10 @@ struct Sim {
     }
     kvsum = simt::warp_sum(kvsum);
     mn = simt::warp_min(mn);
+    minrem = simt::warp_min(minrem);
     simt::sync();
     if (own(x)) {
+      if (minrem < L_minrem) L_minrem = minrem;
       L_nb += add;
       L_ni -= add;
       L_skv += kvsum;
@@ -570,7 +584,7 @@ struct Sim {
       c_qlen[rid] = qlen;
       c_npre[rid] += 1;
     }
-    if (own(x)) { L_used -= kv; L_skv -= kv; }
+    if (own(x)) { L_used -= kv; L_skv -= kv; L_final -= (int64_t)pl + dl - 1; }
     if (rf & kCopy) {
       const int y = x ^ 1;
       if (own(y)) { L_used -= kv; L_copy_tok -= kv; }
@@ -652,6 +666,10 @@ struct Sim {
     }
     log(KVSIM_EV_STEP_START, x, nb, 0, K);
     if (preempted && acc) ensure_prefill(x >> 1, t);
+    else if (!preempted && chain_steps) {
+      if (acc) fast_forward_pair(x);
+      else fast_forward(x, t);
+    }
   }
 
   KV_DEV void step_end(int x, double t) {
@@ -665,6 +683,8 @@ struct Sim {
       L_skv = L_skv - o.kv_done + surv;
       L_nb = surv;
       L_prev_end = t;
+      L_minrem = o.minrem;
+      L_final -= o.kv_done + o.completed;
     }
     count_tokens(o.nb_old, t);
     if (policy == KVSIM_POLICY_ACCELLM) {
@@ -681,6 +701,333 @@ struct Sim {
       }
     }
     log(KVSIM_EV_STEP_END, x, o.nb_old, o.completed, 0);
+  }
+
+
+  // ------------------------------------------------ exact step chaining
+  // Called right after x started a decode step at boundary t. If x's next
+  // step ends cannot interact with any other pending event (no completion,
+  // join, admission, policy action or memory pressure on x, and every
+  // interacting event -- the next arrival, x's pair partner (AcceLLM), the
+  // prefill instances (Splitwise) -- is later), those step-end events are
+  // processed here in one register loop plus a single pass over the batch.
+  // Events of independent instances/pairs commute with them, so every
+  // per-request timestamp, ledger value and decision is unchanged.
+  KV_DEV void fast_forward(int x, double t) {
+    (void)t;
+    const int32_t B = get(L_nb, x);
+    if (B <= 0) return;
+    int64_t kmax = (int64_t)get(L_minrem, x) - 1;
+    if (kmax < 1) return;
+    const double kInf = as_f64(0x7ff0000000000000ull);
+    const int y = x ^ 1;
+    const bool acc = policy == KVSIM_POLICY_ACCELLM;
+    double ht = has_next ? t_next : kInf;
+    int32_t hk = -1;  // arrivals precede every instance event at equal time
+    int32_t m = 0;
+    if (policy == KVSIM_POLICY_UNIFIED) {
+      if (get(Q_n, x) != 0) return;
+    } else if (policy == KVSIM_POLICY_SPLITWISE) {
+      const bool all_busy = simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
+      if (!all_busy) {
+        if (get(Q_n, 0) != 0) return;
+        if (simt::ballot(lane >= n_prefill && lane < n && L_final > f.cap) != 0) return;
+      }
+      double pt = (lane < n_prefill && L_job != JOB_NONE) ? L_busy_until : kInf;
+      int32_t pk = 2 * 64 + lane;
+      for (int mm = 16; mm; mm >>= 1) {
+        const double ot = simt::shfl_xor(pt, mm);
+        const int32_t ok = simt::shfl_xor(pk, mm);
+        if (ot < pt || (ot == pt && ok < pk)) { pt = ot; pk = ok; }
+      }
+      if (pt < ht || (pt == ht && pk < hk)) { ht = pt; hk = pk; }
+    } else {
+      if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
+      const int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
+      if (get(L_role, y) == ROLE_DECODE && c >= 1) {
+        // rebalance_pair at chained boundary i moves iff some copy-holding
+        // member has kv0 + i <= lim0 + i*B (d grows by B per step, each kv by 1)
+        const int64_t d0 = load_of(x) - load_of(y);
+        const int64_t lim0 = c >= 2 ? d0 : d0 - 1;
+        int64_t kvmin = INT64_MAX;
+        for (int32_t q = lane; q < B; q += 32) {
+          const int32_t rf = b_rem(x)[q];
+          if (rf & kCopy) {
+            const int64_t kv = (int64_t)b_kvb(x)[q] - (rf & kRemMask);
+            if (kv < kvmin) kvmin = kv;
+          }
+        }
+        kvmin = simt::warp_min(kvmin);
+        if (kvmin != INT64_MAX) {
+          if (kvmin <= lim0) return;
+          if (B >= 2) {
+            const int64_t istar = (kvmin - lim0 + (B - 2)) / (B - 1);  // first boundary with a move
+            if (istar - 1 < kmax) kmax = istar - 1;
+          }
+        }
+      }
+      const int32_t jy = get(L_job, y);
+      double yt = kInf;
+      int32_t yk = 0;
+      if (jy != JOB_NONE) { yt = get(L_busy_until, y); yk = (jy == JOB_PREFILL ? 2 : 3) * 64 + y; }
+      else if (get(L_role, y) == ROLE_DECODE && get(L_ni, y) > 0) { yt = get(L_min_ready, y); yk = 64 + y; }
+      if (yt < ht || (yt == ht && yk < hk)) { ht = yt; hk = yk; }
+      m = get(L_ncopy, x);
+      if (m > 0) {
+        const int64_t roomy = (f.cap - get(L_used, y)) / m;
+        if (roomy < kmax) kmax = roomy;
+      }
+    }
+    {
+      const int64_t roomx = (f.cap - get(L_used, x)) / B;
+      if (roomx < kmax) kmax = roomx;
+      const int64_t ev_room = event_budget - n_events;
+      if (ev_room < kmax) kmax = ev_room;
+    }
+    if (kmax < 1) return;
+    const double mr = get(L_ni, x) > 0 ? get(L_min_ready, x) : kInf;
+    const int32_t key = 3 * 64 + x;
+    double e = get(L_busy_until, x);
+    const double e1 = e;
+    double js = get(L_job_start, x);
+    double busy = get(L_busy_time, x);
+    double link = acc ? get(L_link, x) : 0.0;
+    double mfin = acc ? get(L_mirror_fin, x) : 0.0;
+    const double pe_old = get(L_prev_end, x);
+    int64_t K = get(L_skv, x);
+    double prev = js, G = 0.0;
+    int64_t j = 0, tw = 0;
+    const double mbytes = kmul((double)m, f.kvb);
+    const double now0 = now;
+    while (j < kmax) {
+      if (!(e < ht || (e == ht && key < hk))) break;
+      if (e >= mr) break;
+      // virtual step-end event at e ...
+      now = e;
+      if (js >= warmup) busy = kadd(busy, ksub(e, js));
+      if (e >= warmup) tw += B;
+      if (j >= 1) {
+        const double g = ksub(e, prev);
+        if (g > G) G = g;
+      }
+      if (m > 0) {
+        const double st = e > link ? e : link;
+        link = kadd(st, transfer_latency(f, mbytes));
+        mfin = link;
+        log(KVSIM_EV_TRANSFER, x, y, 1, m);
+      }
+      log(KVSIM_EV_STEP_END, x, B, 0, 0);
+      // ... and the next step started at its boundary
+      K += B;
+      log(KVSIM_EV_STEP_START, x, B, 0, K);
+      prev = e;
+      js = e;
+      e = kadd(e, decode_latency(f, B, K));
+      ++j;
+    }
+    now = now0;
+    if (j == 0) return;
+    n_steps += j;
+    n_events += j;
+    tok_total += j * B;
+    tok_window += tw;
+    mir_tokens += j * m;
+    if (prev > t_last) t_last = prev;
+    if (own(x)) {
+      L_busy_time = busy;
+      L_job_start = js;
+      L_busy_until = e;
+      L_prev_end = prev;
+      L_skv = K;
+      L_minrem -= (int32_t)j;
+      L_used += j * B;
+      if (L_used > L_peak) L_peak = L_used;
+      if (acc) { L_link = link; L_mirror_fin = mfin; }
+    }
+    if (acc && m > 0 && own(y)) {
+      L_used += j * m;
+      L_copy_tok += j * m;
+      if (L_used > L_peak) L_peak = L_used;
+    }
+    // one pass over the batch: j tokens each, TBT max over the chained gaps
+    int32_t* rem_a = b_rem(x);
+    double* tbt_a = b_tbt(x);
+    for (int32_t q = lane; q < B; q += 32) {
+      const int32_t rf = rem_a[q];
+      double tb = tbt_a[q];
+      const double last = (rf & kJoin) ? c_last[b_rid(x)[q]] : pe_old;
+      double g1 = ksub(e1, last);
+      if (G > g1) g1 = G;
+      rem_a[q] = ((rf & kRemMask) - (int32_t)j) | (rf & kCopy);
+      if (g1 > tb) tbt_a[q] = g1;
+    }
+    simt::sync();
+  }
+
+  // AcceLLM pair chaining: co-advance the step ends of both pair members in
+  // their merged (time, id) order while no boundary could act (completion,
+  // join, memory shortfall, rebalance move, switch) and before the next
+  // arrival. Other pairs only interact through arrivals.
+  struct Chain {
+    double e, js, busy, link, mfin, prev, G, e1, pe_old, mr;
+    int64_t K, used, tw, lim_kv, i;
+    int32_t B, m, minrem, z;
+  };
+  KV_DEV void chain_init(Chain& c, int z) {
+    c.z = z;
+    c.B = get(L_nb, z);
+    c.e = get(L_busy_until, z);
+    c.e1 = c.e;
+    c.js = get(L_job_start, z);
+    c.busy = get(L_busy_time, z);
+    c.link = get(L_link, z);
+    c.mfin = get(L_mirror_fin, z);
+    c.pe_old = get(L_prev_end, z);
+    c.prev = c.js;
+    c.G = 0.0;
+    c.K = get(L_skv, z);
+    c.used = get(L_used, z);
+    c.tw = 0;
+    c.i = 0;
+    c.m = get(L_ncopy, z);
+    c.minrem = get(L_minrem, z);
+    c.mr = get(L_ni, z) > 0 ? get(L_min_ready, z) : as_f64(0x7ff0000000000000ull);
+    // smallest kv among copy-holding members (rebalance candidates)
+    int64_t kvmin = INT64_MAX;
+    for (int32_t q = lane; q < c.B; q += 32) {
+      const int32_t rf = b_rem(z)[q];
+      if (rf & kCopy) {
+        const int64_t kv = (int64_t)b_kvb(z)[q] - (rf & kRemMask);
+        if (kv < kvmin) kvmin = kv;
+      }
+    }
+    c.lim_kv = simt::warp_min(kvmin);
+  }
+  KV_DEV void chain_commit(Chain& c, int64_t used_partner_add) {
+    const int z = c.z;
+    if (c.i > 0) {
+      n_steps += c.i;
+      n_events += c.i;
+      tok_total += c.i * c.B;
+      tok_window += c.tw;
+      mir_tokens += c.i * c.m;
+      if (c.prev > t_last) t_last = c.prev;
+      if (own(z)) {
+        L_busy_time = c.busy;
+        L_job_start = c.js;
+        L_busy_until = c.e;
+        L_prev_end = c.prev;
+        L_skv = c.K;
+        L_minrem -= (int32_t)c.i;
+        L_link = c.link;
+        L_mirror_fin = c.mfin;
+      }
+      int32_t* rem_a = b_rem(z);
+      double* tbt_a = b_tbt(z);
+      for (int32_t q = lane; q < c.B; q += 32) {
+        const int32_t rf = rem_a[q];
+        const double tb = tbt_a[q];
+        const double last = (rf & kJoin) ? c_last[b_rid(z)[q]] : c.pe_old;
+        double g1 = ksub(c.e1, last);
+        if (c.G > g1) g1 = c.G;
+        rem_a[q] = ((rf & kRemMask) - (int32_t)c.i) | (rf & kCopy);
+        if (g1 > tb) tbt_a[q] = g1;
+      }
+      simt::sync();
+    }
+    if (own(z)) {
+      L_used = c.used;
+      if (L_used > L_peak) L_peak = L_used;
+      L_copy_tok += used_partner_add;
+    }
+  }
+  KV_DEV void fast_forward_pair(int x) {
+    const int y = x ^ 1;
+    if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
+    if (get(L_nb, x) <= 0 || get(L_minrem, x) < 2) return;
+    const double kInf = as_f64(0x7ff0000000000000ull);
+    double ht = has_next ? t_next : kInf;
+    int32_t hk = -1;
+    const int32_t jy = get(L_job, y);
+    const bool ystep = jy == JOB_STEP;
+    if (!ystep) {
+      double yt = kInf;
+      int32_t yk = 0;
+      if (jy == JOB_PREFILL) { yt = get(L_busy_until, y); yk = 2 * 64 + y; }
+      else if (get(L_role, y) == ROLE_DECODE && get(L_ni, y) > 0) { yt = get(L_min_ready, y); yk = 64 + y; }
+      if (yt < ht || (yt == ht && yk < hk)) { ht = yt; hk = yk; }
+    }
+    const bool rb_ok = get(L_role, y) == ROLE_DECODE;  // rebalances possible in this pair
+    const int64_t cx = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
+    Chain a, b;
+    chain_init(a, x);
+    if (ystep) chain_init(b, y);
+    else {
+      b.z = y; b.B = 0; b.i = 0; b.e = kInf; b.m = 0; b.used = get(L_used, y); b.K = get(L_skv, y);
+      b.lim_kv = INT64_MAX; b.minrem = 0; b.mr = kInf;
+    }
+    const int64_t loadx0 = load_of(x), loady0 = load_of(y);
+    int64_t copy_add_x = 0, copy_add_y = 0;  // mirror reservations landing on x / y
+    const double now0 = now;
+    int64_t budget_left = event_budget - n_events;
+    for (;;) {
+      // next chained event: the earlier step end, ties to the lower id
+      const bool pickA = !(b.e < a.e || (b.e == a.e && y < x));
+      Chain& c = pickA ? a : b;
+      Chain& o = pickA ? b : a;
+      const int z = c.z;
+      if (c.B <= 0) break;
+      if (!(c.e < ht || (c.e == ht && 3 * 64 + z < hk))) break;
+      if (c.i + 1 >= c.minrem) break;      // a member completes at this step end
+      if (c.e >= c.mr) break;              // a join at this boundary
+      if (budget_left <= 0) break;
+      // rebalance at z's boundary after this step end
+      if (rb_ok) {
+        const int64_t cz = pickA ? cx : -cx;
+        if (cz >= 1 && c.lim_kv != INT64_MAX) {
+          const int64_t lz = (pickA ? loadx0 : loady0) + (c.i + 1) * c.B;
+          const int64_t lw = (pickA ? loady0 : loadx0) + o.i * o.B;
+          const int64_t dz = lz - lw;
+          const int64_t lim = cz >= 2 ? dz : dz - 1;
+          if (c.lim_kv + c.i + 1 <= lim) break;
+        }
+      }
+      // memory for z's next step start: B on z, m mirror lines on the partner
+      if (c.used + c.B > f.cap || o.used + c.m > f.cap) break;
+      // ---- commit the virtual step end of z at c.e and its next step start
+      now = c.e;
+      if (c.js >= warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
+      if (c.e >= warmup) c.tw += c.B;
+      if (c.i >= 1) {
+        const double g = ksub(c.e, c.prev);
+        if (g > c.G) c.G = g;
+      }
+      if (c.m > 0) {
+        const double st = c.e > c.link ? c.e : c.link;
+        c.link = kadd(st, transfer_latency(f, kmul((double)c.m, f.kvb)));
+        c.mfin = c.link;
+        log(KVSIM_EV_TRANSFER, z, z ^ 1, 1, c.m);
+      }
+      log(KVSIM_EV_STEP_END, z, c.B, 0, 0);
+      c.K += c.B;
+      c.used += c.B;
+      o.used += c.m;
+      if (pickA) copy_add_y += c.m; else copy_add_x += c.m;
+      log(KVSIM_EV_STEP_START, z, c.B, 0, c.K);
+      c.prev = c.e;
+      c.js = c.e;
+      c.e = kadd(c.e, decode_latency(f, c.B, c.K));
+      c.i += 1;
+      budget_left -= 1;
+    }
+    now = now0;
+    chain_commit(a, copy_add_x);
+    if (ystep) chain_commit(b, copy_add_y);
+    else if (own(y)) {
+      L_used = b.used;
+      if (L_used > L_peak) L_peak = L_used;
+      L_copy_tok += copy_add_y;
+    }
   }
 
   // ------------------------------------------------------------- unified
@@ -733,6 +1080,7 @@ struct Sim {
       L_job_s1 = s1;
     }
     log(KVSIM_EV_STEP_START, x, nb, k, K);
+    if (k == 0 && chain_steps) fast_forward(x, t);
   }
 
   KV_DEV void unified_end(int x, double t) {
@@ -745,7 +1093,7 @@ struct Sim {
     count_tokens(o.nb_old, t);
     // co-batched prefills emit and join (non-joiners: their last token is t)
     const int32_t k = get(L_njob, x);
-    int32_t completed = o.completed, add = 0;
+    int32_t completed = o.completed, add = 0, minrem = o.minrem;
     int64_t kvadd = 0, kvfree = 0;
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -768,12 +1116,14 @@ struct Sim {
         b_kvb(x)[pos] = pl + dl - 1;
         b_tbt(x)[pos] = c_tbt[rid];
         kvadd += (int64_t)pl + em - 1;
+        if (dl - em < minrem) minrem = dl - em;
       }
       add += simt::popc(jm);
       completed += simt::popc(simt::ballot(done));
     }
     kvadd = simt::warp_sum(kvadd);
     kvfree = simt::warp_sum(kvfree);
+    minrem = simt::warp_min(minrem);
     simt::sync();
     count_tokens(k, t);
     if (k > 0) n_prefills += 1;
@@ -784,6 +1134,7 @@ struct Sim {
       L_nb = nb + add;
       L_prev_end = t;
       L_njob = 0;
+      L_minrem = minrem;
     }
     log(KVSIM_EV_STEP_END, x, o.nb_old, completed, 0);
     unified_start(x, t);
@@ -890,7 +1241,7 @@ struct Sim {
       }
     }
     simt::sync();
-    if (lane < kMaxInst) W->cnt[lane] = 0;
+    if (lane < kMaxInst) { W->cnt[lane] = 0; W->acc_b[lane] = 0; }
     simt::sync();
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -904,8 +1255,11 @@ struct Sim {
         i_rid(d)[pos] = rid;
         i_ready(d)[pos] = fin_d;
         c_cpy[rid] = -1;
+        simt::atomic_add_smem(&W->acc_b[d], (int64_t)c_pl[rid] + c_dl[rid] - 1);
       }
     }
+    simt::sync();
+    if (lane >= n_prefill && lane < n) L_final += W->acc_b[lane];
     simt::sync();
   }
 
@@ -1269,7 +1623,7 @@ struct Sim {
     if (s1c > 0) fin = prefill_transfer(x, y, s1c, jstart, t);
     // pass 3: survivors join x's batch as joiners (last token = t)
     const int32_t nb = get(L_nb, x);
-    int32_t add = 0, addc = 0;
+    int32_t add = 0, addc = 0, minrem = 0x7fffffff;
     int64_t kvadd = 0;
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -1291,13 +1645,21 @@ struct Sim {
         b_kvb(x)[pos] = pl + dl - 1;
         b_tbt(x)[pos] = c_tbt[rid];
         kvadd += (int64_t)pl + em - 1;
+        if (dl - em < minrem) minrem = dl - em;
       }
       addc += simt::popc(simt::ballot(surv && c_cpy[surv ? rid : 0] == y));
       add += simt::popc(sm);
     }
     kvadd = simt::warp_sum(kvadd);
+    minrem = simt::warp_min(minrem);
     simt::sync();
-    if (own(x)) { L_nb += add; L_skv += kvadd; L_ncopy += addc; L_njob = 0; }
+    if (own(x)) {
+      L_nb += add;
+      L_skv += kvadd;
+      L_ncopy += addc;
+      L_njob = 0;
+      if (minrem < L_minrem) L_minrem = minrem;
+    }
     if (head_admissible(x)) {
       move_all_to_partner(x, t);
       acc_start_job(x, t);
@@ -1387,12 +1749,15 @@ struct Sim {
       if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
       if (!is_arrival && ck == (1 << 20)) break;
       if (++n_events > event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
+      ++n_loop;
       if (is_arrival) {
         now = t_next;
+        if (now > t_last) t_last = now;
         arrive(t_next);
       } else {
         const double t = ct;
         now = t;
+        if (now > t_last) t_last = now;
         const int kind = ck >> 6, x = ck & 63;
         if (kind == 1) {
           log(KVSIM_EV_WAKE, x, 0, 0, 0);
@@ -1470,7 +1835,8 @@ struct Sim {
       s.n_preemptions = n_preempt; s.n_evictions = n_evict;
       s.tokens_total = tok_total; s.tokens_window = tok_window;
       s.link_prefill_tokens = pf_tokens; s.link_mirror_tokens = mir_tokens;
-      s.makespan_s = now;
+      s.makespan_s = t_last;
+      s.reserved[0] = n_loop;
       const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
       double busy = 0.0;
       for (int x = 0; x < n; ++x) busy = kadd(busy, get(L_busy_time, x));
@@ -1569,7 +1935,7 @@ struct Sim {
       }
       s.tbt_mean = n_tbt > 0 ? kdiv(s_tbt, (double)n_tbt) : kNaN;
       s.tbt_max = n_tbt > 0 ? tmax : kNaN;
-      const double window = ksub(now, warmup);
+      const double window = ksub(t_last, warmup);
       if (window > 0.0) {
         s.cost_eff = kdiv((double)tok_window, kmul(window, (double)n));
         s.idle_frac = ksub(1.0, kdiv(busy, kmul((double)n, window)));

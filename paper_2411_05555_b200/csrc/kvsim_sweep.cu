@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -28,7 +29,10 @@ constexpr int kWarpsPerBlock = 4;
 }
 
 // ------------------------------------------------------------------ kernels
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) kvsim_sweep_kernel(SweepArgs a) {
+// MINB = minimum resident blocks per SM requested from ptxas (register cap
+// 65536 / (128 * MINB)); selected at context open (KVSIM_MINB, default below).
+template <int MINB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   const int w = threadIdx.x >> 5;
@@ -125,9 +129,22 @@ struct kvsim_gpu_ctx {
   SweepArgs reserved_args{};
   bool reserved = false;
   int64_t last_launches = 0;
+  void (*kernel)(SweepArgs) = nullptr;
+  int minb = 2;
 };
 
 namespace {
+
+using SweepFn = void (*)(SweepArgs);
+constexpr int kDefaultMinBlocks = 2;
+SweepFn sweep_variant(int minb) {
+  switch (minb) {
+    case 1: return kvsim_sweep_kernel<1>;
+    case 3: return kvsim_sweep_kernel<3>;
+    case 4: return kvsim_sweep_kernel<4>;
+    default: return kvsim_sweep_kernel<2>;
+  }
+}
 
 int set_err(char* err, size_t len, int code, const std::string& msg) {
   if (err && len) {
@@ -168,7 +185,7 @@ int prepare_arena(kvsim_gpu_ctx* c, const kvsim_host::ArenaGeom& g, size_t n_pts
 int launch_sweep(kvsim_gpu_ctx* c, SweepArgs& a, cudaStream_t s, char* err, size_t err_len) {
   const int blocks = (a.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
   KV_CUDA(cudaMemsetAsync(a.next_point, 0, sizeof(unsigned long long), s));
-  kvsim_sweep_kernel<<<blocks, kWarpsPerBlock * 32, smem_bytes(), s>>>(a);
+  c->kernel<<<blocks, kWarpsPerBlock * 32, smem_bytes(), s>>>(a);
   KV_CUDA(cudaGetLastError());
   c->last_launches = 1;
   return KVSIM_OK;
@@ -238,9 +255,12 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   auto* c = new kvsim_gpu_ctx();
   c->device = device;
   c->sms = prop.multiProcessorCount;
-  KV_CUDA(cudaFuncSetAttribute(kvsim_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+  c->minb = kDefaultMinBlocks;
+  if (const char* e = std::getenv("KVSIM_MINB")) c->minb = std::atoi(e);
+  c->kernel = sweep_variant(c->minb);
+  KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
   int bps = 1;
-  KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kvsim_sweep_kernel, kWarpsPerBlock * 32, smem_bytes()));
+  KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
   c->blocks_per_sm = bps > 0 ? bps : 1;
   KV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   *out = c;

@@ -76,11 +76,13 @@ def emu():
 
 
 class Result:
-    def __init__(self, summary, recs, events, status=0):
+    def __init__(self, summary, recs, events, status=0, ev_total=None):
         self.summary = summary
         self.recs = recs
         self.events = events
         self.status = status
+        # total events produced (may exceed the captured log)
+        self.ev_total = ev_total if ev_total is not None else (len(events) if events is not None else None)
 
 
 def run_oracle(p: PointDesc, trace: TraceView | None = None, ev_cap: int = 0, recs: bool = True) -> Result:
@@ -93,7 +95,7 @@ def run_oracle(p: PointDesc, trace: TraceView | None = None, ev_cap: int = 0, re
     st = L.kvo_run_point(C.byref(p), C.byref(trace) if trace is not None else None, C.byref(s), R, E, ev_cap,
                          C.byref(cnt))
     n = s.n_requests
-    return Result(s, list(R)[:n] if recs else None, list(E)[:min(cnt.value, ev_cap)] if ev_cap else None, st)
+    return Result(s, R[:n] if recs else None, E[:min(cnt.value, ev_cap)] if ev_cap else None, st, cnt.value)
 
 
 def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warps: int = 2):
@@ -116,10 +118,10 @@ def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warp
     for i, p in enumerate(points):
         s = S[i]
         nr = max(int(p.num_requests), 0)
-        rr = list(R)[off:off + s.n_requests] if recs else None
+        rr = R[off:off + s.n_requests] if recs else None
         off += nr
-        ee = list(E)[i * ev_cap:i * ev_cap + min(cnt[i], ev_cap)] if ev_cap else None
-        out.append(Result(s, rr, ee, s.status))
+        ee = E[i * ev_cap:i * ev_cap + min(cnt[i], ev_cap)] if ev_cap else None
+        out.append(Result(s, rr, ee, s.status, cnt[i]))
     return out
 
 
@@ -164,6 +166,11 @@ def diff_results(a: Result, b: Result, *, events: bool = True) -> list[str]:
             if len(errs) > 20:
                 break
     if events and a.events is not None and b.events is not None:
+        if a.ev_total != b.ev_total:
+            errs.append(f"event totals: {a.ev_total} != {b.ev_total}")
+        if len(a.events) < a.ev_total or len(b.events) < b.ev_total:
+            errs.append(f"event log truncated ({len(a.events)}/{a.ev_total}); raise ev_cap")
+            return errs
         ka = sorted(ev_key(e) for e in a.events)
         kb = sorted(ev_key(e) for e in b.events)
         if ka != kb:

@@ -1,0 +1,146 @@
+"""GPU parity: the sm_100a kernels, called through the C-ABI, against the CPU
+oracle on the same seeded inputs. Scheduling decisions, per-request
+timestamps, event logs and per-point summaries must be bit-identical
+(SEMANTICS.md contract; north-star tolerance 1e-9 is met with 0)."""
+import ctypes as C
+import math
+import random
+
+import pytest
+
+from configs import closed_form_point, config1, config2, config3, random_small
+from harness import Result, diff_results, oracle, run_oracle
+from paper_2411_05555_b200.abi import MODELS, make_point
+
+pytestmark = pytest.mark.gpu
+EV = 1 << 16
+
+
+@pytest.fixture(scope="module")
+def sim():
+    import paper_2411_05555_b200 as pkg
+    s = pkg.KvSim(0)
+    yield s
+    s.close()
+
+
+def check(sim, points, ev=EV, records=True):
+    summ, recs, evs = sim.run(points, records=records, events=ev)
+    cnts = sim.last_event_counts
+    bad = []
+    for i, p in enumerate(points):
+        ref = run_oracle(p, ev_cap=ev, recs=records)
+        d = diff_results(ref, Result(summ[i], recs[i], evs[i], ev_total=cnts[i]))
+        if d:
+            bad.append((i, p.policy, p.num_requests, d[:4]))
+    assert not bad, bad
+    return summ
+
+
+def test_closed_form(sim):
+    s = check(sim, [closed_form_point()])
+    assert s[0].n_completed == 1 and s[0].tokens_total == 10
+
+
+def test_config1_all_seeds(sim):
+    # BASELINE config 1 at full size: 1000 requests, seeds 0-9, records + decision logs
+    check(sim, [config1(seed=s, n=1000) for s in range(10)], ev=1 << 19)
+
+
+def test_config2_three_policies(sim):
+    pts = [config2(pol, rate, seed=s, n=2000) for pol in ("accellm", "splitwise", "unified")
+           for rate in (6.0, 12.0) for s in (0, 1)]
+    check(sim, pts, ev=1 << 20)
+
+
+def test_config3_three_policies(sim):
+    pts = [config3(pol, rate, seed=0, n=1500) for pol in ("accellm", "splitwise", "unified") for rate in (1.0, 3.0)]
+    check(sim, pts, ev=1 << 20)
+
+
+def test_random_small_configs(sim):
+    check(sim, [random_small(i) for i in range(200)])
+
+
+def test_random_medium_configs(sim):
+    check(sim, [random_small(1000 + i, max_req=400) for i in range(60)], ev=1 << 17)
+
+
+def test_sweep_summaries_sample(sim):
+    # a slice of BASELINE config 4 (rate x instances x policy), summaries only
+    pts = []
+    for pol in ("unified", "splitwise", "accellm"):
+        for ni in (4, 8, 12, 16):
+            for k in (1, 200, 500, 832):
+                rate = 3.0 * ni * (k + 1) / 833
+                pts.append(make_point(policy=pol, instances=ni, rate=rate, num_requests=1500, seed=len(pts)))
+    summ = sim.run(pts)
+    for p, s in zip(pts, summ):
+        ref = run_oracle(p, ev_cap=0, recs=False)
+        assert not diff_results(ref, Result(s, None, None), events=False), (p.policy, p.num_instances, p.rate)
+
+
+def test_shard_invariance(sim):
+    # results must not depend on how points are split across launches / GPUs
+    pts = [random_small(500 + i, max_req=200) for i in range(40)]
+    whole = sim.run(pts)
+    parts = sim.run(pts[::2]) + sim.run(pts[1::2])
+    shard = {}
+    for i, s in zip(list(range(0, 40, 2)) + list(range(1, 40, 2)), parts):
+        shard[i] = s
+    for i in range(40):
+        assert bytes(whole[i]) == bytes(shard[i])
+
+
+def test_perf_batch_bitwise(sim):
+    L = oracle()
+    r = random.Random(5)
+    pts = [make_point(model=r.choice(list(MODELS)), device=r.choice(["h100", "910b2"]),
+                      eff=(r.uniform(0.1, 1), r.uniform(0.1, 1), r.uniform(0.1, 1)),
+                      link=r.choice(["striped", "single"]), num_devices=r.choice([1, 2, 4, 8]))
+           for _ in range(16)]
+    pidx, ops, s1, s2 = [], [], [], []
+    for _ in range(4000):
+        i = r.randrange(16)
+        op = r.randrange(4)
+        if op == 0:
+            lens = [r.randint(1, 8000) for _ in range(r.randint(1, 20))]
+            a, b = sum(lens), sum(x * x for x in lens)
+        elif op == 1:
+            bsz = r.randint(1, 2000)
+            a, b = bsz, bsz * r.randint(1, 4000)
+        else:
+            a, b = r.randint(0, 1 << 40), 0
+        pidx.append(i); ops.append(op); s1.append(a); s2.append(b)
+    got = sim.perf_batch(pts, pidx, ops, s1, s2)
+    for j in range(len(pidx)):
+        p = pts[pidx[j]]
+        if ops[j] == 0:
+            want = L.kvo_prefill_latency(C.byref(p), s1[j], s2[j])
+        elif ops[j] == 1:
+            want = L.kvo_decode_step_latency(C.byref(p), s1[j], s2[j])
+        elif ops[j] == 2:
+            want = L.kvo_transfer_latency(C.byref(p), float(s1[j]))
+        else:
+            cap = C.c_int64()
+            st = L.kvo_kv_capacity_tokens(C.byref(p), C.byref(cap))
+            want = cap.value if st == 0 else -1
+            got_i = C.c_int64.from_buffer(C.c_double(got[j])).value
+            assert got_i == want
+            continue
+        assert got[j] == want or (math.isnan(got[j]) and math.isnan(want)), (ops[j], got[j], want)
+
+
+def test_trace_generator_bitwise(sim):
+    L = oracle()
+    for i, (proc, rate, n) in enumerate([("poisson", 2.0, 5000), ("poisson", 37.5, 3000), ("fixed", 3.0, 1000),
+                                         ("poisson", 0.25, 2000)]):
+        p = make_point(arrival=proc, rate=rate, num_requests=n, seed=11 + i, workload="mixed",
+                       duration_s=900.0 if i == 3 else math.inf)
+        arr, pl, dl = sim.gen_trace(p)
+        a = (C.c_double * n)()
+        b = (C.c_int32 * n)()
+        c = (C.c_int32 * n)()
+        k = L.kvo_gen_trace(C.byref(p), a, b, c, n)
+        assert len(arr) == k
+        assert list(a)[:k] == arr and list(b)[:k] == pl and list(c)[:k] == dl
