@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -97,13 +98,21 @@ inline size_t carve(Args& a, char* base, const ArenaGeom& g, int32_t slots) {
 inline std::vector<int64_t> lpt_order(const kvsim_point_desc* pts, size_t n) {
   std::vector<int64_t> ord(n);
   std::vector<double> cost(n);
+  // Points are grouped by policy (co-resident warps then execute the same
+  // policy-specialised code: the kernel is instruction-fetch bound otherwise),
+  // longest first within a policy. KVSIM_ORDER=lpt disables the grouping.
+  const char* mode = std::getenv("KVSIM_ORDER");
+  const bool by_policy = !(mode && mode[0] == 'l');
   for (size_t i = 0; i < n; ++i) {
     const kvsim_point_desc& p = pts[i];
     const double dbar = 0.5 * ((double)p.decode_min + (double)p.decode_max);
     cost[i] = (double)p.num_requests * dbar * (1.0 + 1.0 / (0.25 + (p.rate > 0 ? p.rate : 0)));
     ord[i] = (int64_t)i;
   }
-  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+    if (by_policy && pts[a].policy != pts[b].policy) return pts[a].policy < pts[b].policy;
+    return cost[a] > cost[b];
+  });
   return ord;
 }
 

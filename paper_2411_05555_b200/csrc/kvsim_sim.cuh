@@ -31,7 +31,22 @@ enum { JOB_NONE = 0, JOB_PREFILL = 1, JOB_STEP = 2 };
 
 // Per-warp shared scratch (atomics and radix histograms only; all simulation
 // state lives in registers or the HBM arena).
+struct PointConst {
+  Perf f;
+  int64_t budget, n_limit, event_budget;
+  double warmup, duration, rate;
+  uint64_t key;
+  const double* tr_arr;
+  const int32_t *tr_pl, *tr_dl;
+  int32_t pmin, pmax, dmin, dmax, fixed_arrivals;
+};
+struct Counters {
+  int64_t n_steps, n_prefills, n_moves, n_preempt, n_evict;
+  int64_t tok_total, tok_window, pf_tokens, mir_tokens, n_loop;
+};
 struct WarpScratch {
+  PointConst pc;  // written by lane 0 at point start, read (broadcast) by all
+  Counters ct;    // updated by lane 0 only
   int64_t acc_a[kMaxInst];
   int64_t acc_b[kMaxInst];
   int32_t cnt[kMaxInst];
@@ -73,45 +88,29 @@ struct SweepArgs {
   unsigned long long* next_point;
 };
 
+#define PC (W->pc)
+// One specialisation per policy: every `policy == ...` test folds at compile
+// time, so a warp only ever executes (and caches) its own policy's code.
+template <int POL>
 struct Sim {
-  const SweepArgs& A;
-  WarpScratch* W;
+  const SweepArgs* A;  // kernel parameters (param space; __grid_constant__)
+  WarpScratch* W;      // per-warp shared scratch: point constants, counters
   int lane;
+  int32_t slot;
   int64_t point;
-  // arena (slot-local)
-  double *c_arr, *c_last, *c_tbt, *c_fresh, *c_first, *c_done;
-  int32_t *c_pl, *c_dl, *c_qlen, *c_em, *c_cpy, *c_nmv, *c_npre;
-  int32_t* q_rid;
-  int32_t *b_rid_, *b_rem_, *b_kvb_;
-  double* b_tbt_;
-  int32_t* i_rid_;
-  double* i_ready_;
-  int32_t *j_rid_, *j_dst_;
-  double* link_;
-  int64_t Ncap, Bcap, Jcap;
-  // point constants
-  Perf f;
-  int32_t policy, n, n_prefill, fixed_arrivals;
-  int32_t pmin, pmax, dmin, dmax;
-  int64_t budget, n_limit, event_budget;
-  double warmup, duration, rate;
-  uint64_t key;
-  const double* tr_arr;
-  const int32_t *tr_pl, *tr_dl;
+  static constexpr int32_t policy = POL;
+  int32_t n, n_prefill;
   // arrival generator
   double t_next, t_prev;
   int64_t next_rid;
   bool has_next;
-  // uniform counters
-  int64_t n_events, n_steps, n_prefills, n_moves, n_preempt, n_evict;
-  int64_t tok_total, tok_window, pf_tokens, mir_tokens, ev_n;
-  int64_t n_loop;  // main-loop iterations actually executed (diagnostic)
+  // uniform counters that steer control flow
+  int64_t n_events, ev_n;
   double now;     // time of the event being processed (event-log timestamps)
   double t_last;  // latest event time processed (makespan)
   bool chain_steps = true;  // exact step chaining (fast_forward); off = plain event loop
+  bool logging = false;     // event log requested (parity runs)
   int32_t status;
-  kvsim_event_record* ev;
-  int64_t ev_cap;
   // lane-owned instance state (lane x <-> instance x)
   double L_busy_until, L_job_start, L_prev_end, L_mirror_fin, L_busy_time, L_min_ready, L_link;
   int64_t L_used, L_peak, L_skv, L_skv_in, L_job_s1, L_copy_tok;
@@ -122,35 +121,38 @@ struct Sim {
   int32_t Q_head, Q_n;
   int64_t Q_tok;
 
-  KV_DEV Sim(const SweepArgs& a, WarpScratch* w, int64_t slot) : A(a), W(w) {
-    lane = simt::lane_id();
-    Ncap = a.Ncap;
-    Bcap = a.Bcap;
-    Jcap = a.Jcap;
-    const int64_t cs = slot * Ncap;
-    c_arr = a.c_arr + cs; c_last = a.c_last + cs; c_tbt = a.c_tbt + cs; c_fresh = a.c_fresh + cs;
-    c_first = a.c_first + cs; c_done = a.c_done + cs;
-    c_pl = a.c_pl + cs; c_dl = a.c_dl + cs; c_qlen = a.c_qlen + cs; c_em = a.c_em + cs;
-    c_cpy = a.c_cpy + cs; c_nmv = a.c_nmv + cs; c_npre = a.c_npre + cs;
-    q_rid = a.q_rid + slot * (int64_t)a.Imax * Ncap;
-    const int64_t bs = slot * (int64_t)a.Imax * Bcap;
-    b_rid_ = a.b_rid + bs; b_rem_ = a.b_rem + bs; b_kvb_ = a.b_kvb + bs; b_tbt_ = a.b_tbt + bs;
-    i_rid_ = a.i_rid + bs; i_ready_ = a.i_ready + bs;
-    const int64_t js = slot * (int64_t)a.Imax * Jcap;
-    j_rid_ = a.j_rid + js; j_dst_ = a.j_dst + js;
-    link_ = a.link + slot * (int64_t)a.Imax * a.Imax;
-  }
+  KV_DEV Sim(const SweepArgs* a, WarpScratch* w, int32_t s) : A(a), W(w), slot(s) { lane = simt::lane_id(); }
+
+  // ------------------------------------------------------------ arena views
+  KV_DEV int64_t cs() const { return (int64_t)slot * A->Ncap; }
+  KV_DEV double* c_arr() const { return A->c_arr + cs(); }
+  KV_DEV double* c_last() const { return A->c_last + cs(); }
+  KV_DEV double* c_tbt() const { return A->c_tbt + cs(); }
+  KV_DEV double* c_fresh() const { return A->c_fresh + cs(); }
+  KV_DEV double* c_first() const { return A->c_first + cs(); }
+  KV_DEV double* c_done() const { return A->c_done + cs(); }
+  KV_DEV int32_t* c_pl() const { return A->c_pl + cs(); }
+  KV_DEV int32_t* c_dl() const { return A->c_dl + cs(); }
+  KV_DEV int32_t* c_qlen() const { return A->c_qlen + cs(); }
+  KV_DEV int32_t* c_em() const { return A->c_em + cs(); }
+  KV_DEV int32_t* c_cpy() const { return A->c_cpy + cs(); }
+  KV_DEV int32_t* c_nmv() const { return A->c_nmv + cs(); }
+  KV_DEV int32_t* c_npre() const { return A->c_npre + cs(); }
+  KV_DEV int64_t bofs(int x) const { return ((int64_t)slot * A->Imax + x) * A->Bcap; }
+  KV_DEV int64_t jofs(int x) const { return ((int64_t)slot * A->Imax + x) * A->Jcap; }
 
   // ------------------------------------------------------------ accessors
-  KV_DEV int32_t* b_rid(int x) { return b_rid_ + (int64_t)x * Bcap; }
-  KV_DEV int32_t* b_rem(int x) { return b_rem_ + (int64_t)x * Bcap; }
-  KV_DEV int32_t* b_kvb(int x) { return b_kvb_ + (int64_t)x * Bcap; }
-  KV_DEV double* b_tbt(int x) { return b_tbt_ + (int64_t)x * Bcap; }
-  KV_DEV int32_t* i_rid(int x) { return i_rid_ + (int64_t)x * Bcap; }
-  KV_DEV double* i_ready(int x) { return i_ready_ + (int64_t)x * Bcap; }
-  KV_DEV int32_t* j_rid(int x) { return j_rid_ + (int64_t)x * Jcap; }
-  KV_DEV int32_t* j_dst(int x) { return j_dst_ + (int64_t)x * Jcap; }
-  KV_DEV int32_t* ring(int q) { return q_rid + (int64_t)q * Ncap; }
+  KV_DEV int32_t* b_rid(int x) { return A->b_rid + bofs(x); }
+  KV_DEV int32_t* b_rem(int x) { return A->b_rem + bofs(x); }
+  KV_DEV int32_t* b_kvb(int x) { return A->b_kvb + bofs(x); }
+  KV_DEV double* b_tbt(int x) { return A->b_tbt + bofs(x); }
+  KV_DEV int32_t* i_rid(int x) { return A->i_rid + bofs(x); }
+  KV_DEV double* i_ready(int x) { return A->i_ready + bofs(x); }
+  KV_DEV int32_t* j_rid(int x) { return A->j_rid + jofs(x); }
+  KV_DEV int32_t* j_dst(int x) { return A->j_dst + jofs(x); }
+  KV_DEV int32_t* ring(int q) { return A->q_rid + ((int64_t)slot * A->Imax + q) * A->Ncap; }
+  KV_DEV double* link_() { return A->link + (int64_t)slot * A->Imax * A->Imax; }
+  KV_DEV kvsim_event_record* evlog() const { return A->ev ? A->ev + point * A->ev_cap : nullptr; }
 
   template <class T>
   KV_DEV T get(T v, int x) { return simt::shfl(v, x); }
@@ -166,22 +168,24 @@ struct Sim {
   }
 
   KV_DEV void log(int kind, int inst, int a, int b, int64_t c) {
-    if (ev != nullptr && lane == 0 && ev_n < ev_cap) {
+    if (!logging) return;
+    if (lane == 0 && ev_n < A->ev_cap) {
       kvsim_event_record r;
       r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
-      ev[ev_n] = r;
+      evlog()[ev_n] = r;
     }
     ev_n += 1;
   }
   // lane-parallel logging: lanes with `p` log one record each (moves)
   KV_DEV void log_lanes(bool p, int kind, int inst, int a, int b, int64_t c) {
+    if (!logging) return;
     unsigned m = simt::ballot(p);
-    if (ev != nullptr && p) {
+    if (p) {
       int64_t k = ev_n + simt::popc(m & simt::lanemask_lt());
-      if (k < ev_cap) {
+      if (k < A->ev_cap) {
         kvsim_event_record r;
         r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
-        ev[k] = r;
+        evlog()[k] = r;
       }
     }
     ev_n += simt::popc(m);
@@ -191,27 +195,27 @@ struct Sim {
   KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q), c = get(Q_n, q);
     int64_t idx = (int64_t)h + c;
-    if (idx >= Ncap) idx -= Ncap;
+    if (idx >= A->Ncap) idx -= A->Ncap;
     if (lane == 0) ring(q)[idx] = rid;
     simt::sync();
     if (own(q)) { Q_n += 1; Q_tok += len; }
   }
   KV_DEV void q_push_front(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q);
-    int32_t nh = h == 0 ? (int32_t)(Ncap - 1) : h - 1;
+    int32_t nh = h == 0 ? (int32_t)(A->Ncap - 1) : h - 1;
     if (lane == 0) ring(q)[nh] = rid;
     simt::sync();
     if (own(q)) { Q_head = nh; Q_n += 1; Q_tok += len; }
   }
   KV_DEV int32_t q_at(int q, int32_t h, int64_t k) {
     int64_t idx = (int64_t)h + k;
-    if (idx >= Ncap) idx -= Ncap;
+    if (idx >= A->Ncap) idx -= A->Ncap;
     return ring(q)[idx];
   }
   KV_DEV void q_pop(int q, int32_t k, int64_t tokens) {
     if (own(q)) {
       int64_t nh = (int64_t)Q_head + k;
-      if (nh >= Ncap) nh -= Ncap;
+      if (nh >= A->Ncap) nh -= A->Ncap;
       Q_head = (int32_t)nh;
       Q_n -= k;
       Q_tok -= tokens;
@@ -221,46 +225,49 @@ struct Sim {
   // ------------------------------------------------------------ point init
   KV_DEV bool init_point(int64_t p) {
     point = p;
-    const kvsim_point_desc& d = A.pts[p];
-    f = make_perf(d);
-    policy = d.policy;
+    const kvsim_point_desc& d = A->pts[p];
+    PointConst pc;
+    pc.f = make_perf(d);
     n = d.num_instances;
     n_prefill = 0;
     if (policy == KVSIM_POLICY_SPLITWISE)
       n_prefill = d.num_prefill_instances > 0 ? d.num_prefill_instances : (n + 2) / 4;
-    budget = d.prefill_token_budget > 0 ? d.prefill_token_budget : 8192;
-    fixed_arrivals = d.arrival_process == KVSIM_ARRIVAL_FIXED;
-    pmin = d.prompt_min; pmax = d.prompt_max; dmin = d.decode_min; dmax = d.decode_max;
-    warmup = d.warmup_s;
-    duration = d.duration_s;
-    rate = d.rate;
-    key = stream_key(d.seed);
+    pc.budget = d.prefill_token_budget > 0 ? d.prefill_token_budget : 8192;
+    pc.fixed_arrivals = d.arrival_process == KVSIM_ARRIVAL_FIXED;
+    pc.pmin = d.prompt_min; pc.pmax = d.prompt_max; pc.dmin = d.decode_min; pc.dmax = d.decode_max;
+    pc.warmup = d.warmup_s;
+    pc.duration = d.duration_s;
+    pc.rate = d.rate;
+    pc.key = stream_key(d.seed);
     status = KVSIM_OK;
-    int64_t nreq = d.num_requests < Ncap ? d.num_requests : Ncap;
-    int32_t evd = dmax;
+    const int64_t nreq = d.num_requests < A->Ncap ? d.num_requests : A->Ncap;
+    int32_t evd = pc.dmax;
     if (d.trace_index >= 0) {
-      const int64_t off = A.tr_off[d.trace_index];
-      tr_arr = A.tr_arr + off; tr_pl = A.tr_pl + off; tr_dl = A.tr_dl + off;
-      int64_t tn = A.tr_n[d.trace_index];
-      n_limit = tn < nreq ? tn : nreq;
-      evd = A.tr_dmax[d.trace_index];
+      const int64_t off = A->tr_off[d.trace_index];
+      pc.tr_arr = A->tr_arr + off; pc.tr_pl = A->tr_pl + off; pc.tr_dl = A->tr_dl + off;
+      const int64_t tn = A->tr_n[d.trace_index];
+      pc.n_limit = tn < nreq ? tn : nreq;
+      evd = A->tr_dmax[d.trace_index];
     } else {
-      tr_arr = nullptr; tr_pl = nullptr; tr_dl = nullptr;
-      n_limit = rate > 0.0 ? nreq : 0;
+      pc.tr_arr = nullptr; pc.tr_pl = nullptr; pc.tr_dl = nullptr;
+      pc.n_limit = pc.rate > 0.0 ? nreq : 0;
     }
-    event_budget = 4 * n_limit * ((int64_t)(evd > 1 ? evd : 1) + 2) + 4096;
+    pc.event_budget = 4 * pc.n_limit * ((int64_t)(evd > 1 ? evd : 1) + 2) + 4096;
     // validity (perfmodel validate())
-    if (n < 1 || n > kMaxInst || n > A.Imax || policy < 0 || policy > 2) status = KVSIM_E_INVALID;
+    if (n < 1 || n > kMaxInst || n > A->Imax || d.policy != POL) status = KVSIM_E_INVALID;
     else if (policy == KVSIM_POLICY_ACCELLM && (n & 1)) status = KVSIM_E_ODD_INSTANCES;
     else if (policy == KVSIM_POLICY_SPLITWISE && (n < 2 || n_prefill >= n)) status = KVSIM_E_INVALID;
-    else if (!f.fits) status = KVSIM_E_MODEL_FIT;
-    n_events = n_steps = n_prefills = n_moves = n_preempt = n_evict = 0;
-    tok_total = tok_window = pf_tokens = mir_tokens = ev_n = 0;
-    n_loop = 0;
+    else if (!pc.f.fits) status = KVSIM_E_MODEL_FIT;
+    simt::sync();  // previous point's readers are done with the scratch
+    if (lane == 0) {
+      W->pc = pc;
+      W->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    }
+    simt::sync();
+    n_events = ev_n = 0;
+    logging = A->ev != nullptr;
     now = 0.0;
     t_last = 0.0;
-    ev = A.ev ? A.ev + p * A.ev_cap : nullptr;
-    ev_cap = A.ev_cap;
     L_busy_until = L_job_start = L_prev_end = L_mirror_fin = L_busy_time = 0.0;
     L_min_ready = as_f64(0x7ff0000000000000ull);
     L_link = 0.0;
@@ -273,7 +280,7 @@ struct Sim {
     Q_head = 0; Q_n = 0; Q_tok = 0;
     // splitwise directed links
     if (policy == KVSIM_POLICY_SPLITWISE)
-      for (int i = lane; i < n * n; i += 32) link_[i] = 0.0;
+      for (int i = lane; i < n * n; i += 32) link_()[i] = 0.0;
     next_rid = 0;
     t_prev = 0.0;
     has_next = false;
@@ -283,19 +290,19 @@ struct Sim {
   }
 
   // arrival generator (SEMANTICS §2); uniform across lanes
-  KV_DEV void gen_next() {
+  KV_DEV_NOINLINE void gen_next() {
     has_next = false;
-    if (next_rid >= n_limit) return;
+    if (next_rid >= PC.n_limit) return;
     double t;
-    if (tr_arr != nullptr) {
-      t = tr_arr[next_rid];
-    } else if (fixed_arrivals) {
-      t = kdiv((double)next_rid, rate);
-      if (!(t < duration)) return;
+    if (PC.tr_arr != nullptr) {
+      t = PC.tr_arr[next_rid];
+    } else if (PC.fixed_arrivals) {
+      t = kdiv((double)next_rid, PC.rate);
+      if (!(t < PC.duration)) return;
     } else {
-      const double g = poisson_gap(key, next_rid, rate);
+      const double g = poisson_gap(PC.key, next_rid, PC.rate);
       t = next_rid == 0 ? g : kadd(t_prev, g);
-      if (!(t < duration)) return;
+      if (!(t < PC.duration)) return;
     }
     t_next = t;
     has_next = true;
@@ -305,25 +312,25 @@ struct Sim {
   // token emission for a request leaving a prefill (first or recompute token)
   // by this lane; returns emitted count after.
   KV_DEV int32_t emit_prefill_token(int32_t rid, double t) {
-    int32_t em = c_em[rid];
+    int32_t em = c_em()[rid];
     if (em == 0) {
-      c_first[rid] = t;
+      c_first()[rid] = t;
     } else {
-      double gap = ksub(t, c_last[rid]);
-      if (gap > c_tbt[rid]) c_tbt[rid] = gap;
+      double gap = ksub(t, c_last()[rid]);
+      if (gap > c_tbt()[rid]) c_tbt()[rid] = gap;
     }
-    c_last[rid] = t;
+    c_last()[rid] = t;
     em += 1;
-    c_em[rid] = em;
+    c_em()[rid] = em;
     return em;
   }
   KV_DEV void count_tokens(int64_t k, double t) {
-    tok_total += k;
-    if (t >= warmup) tok_window += k;
+    if (lane == 0) W->ct.tok_total += k;
+    if (t >= PC.warmup) if (lane == 0) W->ct.tok_window += k;
   }
   KV_DEV void account_job(int x, double t) {
     double js = get(L_job_start, x);
-    if (own(x) && js >= warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
+    if (own(x) && js >= PC.warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
   }
 
   // ------------------------------------------------------- hot decode loop
@@ -335,7 +342,7 @@ struct Sim {
     int32_t nb_old, completed, m_copies, copy_done, minrem;
     int64_t kv_done, copy_free;
   };
-  KV_DEV StepOut step_loop(int x, double t) {
+  KV_DEV_NOINLINE StepOut step_loop(int x, double t) {
     StepOut o;
     const int32_t nb = get(L_nb, x);
     const double prev = get(L_prev_end, x);
@@ -366,7 +373,7 @@ struct Sim {
       double gap = 0.0;
       bool upd = false;
       if (act) {
-        const double last = joiner ? c_last[rid] : prev;
+        const double last = joiner ? c_last()[rid] : prev;
         gap = ksub(t, last);
         upd = gap > tb;
         if (upd) tb = gap;
@@ -386,9 +393,9 @@ struct Sim {
         }
       }
       if (done) {
-        c_done[rid] = t;
-        c_tbt[rid] = tb;
-        c_em[rid] = c_dl[rid];
+        c_done()[rid] = t;
+        c_tbt()[rid] = tb;
+        c_em()[rid] = c_dl()[rid];
         const int64_t kvbef = (int64_t)kvb - 1;  // kv before the step: kvb - (rem+1), rem == 0
         kv_done += kvbef;
         if (hasc) copy_free += kvbef + 1;
@@ -410,7 +417,7 @@ struct Sim {
   }
 
   // -------------------------------------------------------------- joins
-  KV_DEV void join(int x, double t) {
+  KV_DEV_NOINLINE void join(int x, double t) {
     const int32_t ni = get(L_ni, x);
     if (ni == 0) return;
     if (get(L_min_ready, x) > t) return;
@@ -438,16 +445,16 @@ struct Sim {
       }
       if (go) {
         const int32_t k = nb + add + simt::popc(gm & simt::lanemask_lt());
-        const int32_t em = c_em[rid], dl = c_dl[rid], pl = c_pl[rid];
-        const bool hasc = c_cpy[rid] >= 0;
+        const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
+        const bool hasc = c_cpy()[rid] >= 0;
         b_rid(x)[k] = rid;
         b_rem(x)[k] = (dl - em) | kJoin | (hasc ? kCopy : 0);
         b_kvb(x)[k] = pl + dl - 1;
-        b_tbt(x)[k] = c_tbt[rid];
+        b_tbt(x)[k] = c_tbt()[rid];
         kvsum += (int64_t)pl + em - 1;
         if (dl - em < minrem) minrem = dl - em;
       }
-      ncopy += simt::popc(simt::ballot(go && c_cpy[go ? rid : 0] >= 0));
+      ncopy += simt::popc(simt::ballot(go && c_cpy()[go ? rid : 0] >= 0));
       keep += simt::popc(sm);
       add += simt::popc(gm);
     }
@@ -507,7 +514,7 @@ struct Sim {
     int64_t kv;
   };
   // largest redundant copy held on instance x (max kv, ties lowest rid)
-  KV_DEV Found largest_copy_on(int x) {
+  KV_DEV_NOINLINE Found largest_copy_on(int x) {
     const int y = x ^ 1;
     uint64_t best = 0;
     int32_t bidx = -1, bwhere = 0;
@@ -522,8 +529,8 @@ struct Sim {
     }
     for (int32_t j = lane; j < ni; j += 32) {
       const int32_t rid = i_rid(y)[j];
-      if (c_cpy[rid] == x) {
-        const int64_t kv = (int64_t)c_pl[rid] + c_em[rid] - 1;
+      if (c_cpy()[rid] == x) {
+        const int64_t kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
         const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - rid);
         if (k > best) { best = k; bidx = j; bwhere = 2; }
       }
@@ -540,7 +547,7 @@ struct Sim {
     r.kv = (int64_t)(wbest >> 32);
     return r;
   }
-  KV_DEV void evict(int x, const Found& v) {
+  KV_DEV_NOINLINE void evict(int x, const Found& v) {
     const int y = x ^ 1;
     int64_t held = v.kv;
     if (v.where == 1) {
@@ -548,16 +555,16 @@ struct Sim {
       if (lane == 0) b_rem(y)[v.idx] &= ~kCopy;
       if (own(y)) L_ncopy -= 1;
     } else {
-      if (lane == 0) c_cpy[v.rid] = -1;
+      if (lane == 0) c_cpy()[v.rid] = -1;
     }
     simt::sync();
     if (own(x)) { L_used -= held; L_copy_tok -= held; }
-    n_evict += 1;
+    if (lane == 0) W->ct.n_evict += 1;
     log(KVSIM_EV_EVICT, x, v.rid, 0, 0);
   }
 
   // ------------------------------------------------------ preemption (P9)
-  KV_DEV void preempt_newest(int x) {
+  KV_DEV_NOINLINE void preempt_newest(int x) {
     const int32_t nb = get(L_nb, x);
     int32_t best = -1, bidx = -1;
     for (int32_t j = lane; j < nb; j += 32) {
@@ -570,19 +577,19 @@ struct Sim {
     const int32_t rf = b_rem(x)[idx];
     const int32_t rem = rf & kRemMask;
     const int64_t kv = (int64_t)b_kvb(x)[idx] - rem;
-    const int32_t dl = c_dl[rid], pl = c_pl[rid];
+    const int32_t dl = c_dl()[rid], pl = c_pl()[rid];
     const int32_t em = dl - rem;
     const double tb = b_tbt(x)[idx];
-    const double last = (rf & kJoin) ? c_last[rid] : get(L_prev_end, x);
+    const double last = (rf & kJoin) ? c_last()[rid] : get(L_prev_end, x);
     const int32_t qlen = pl + em;
     simt::sync();
     if (lane == 0) {
-      c_em[rid] = em;
-      c_tbt[rid] = tb;
-      c_last[rid] = last;
-      c_cpy[rid] = -1;
-      c_qlen[rid] = qlen;
-      c_npre[rid] += 1;
+      c_em()[rid] = em;
+      c_tbt()[rid] = tb;
+      c_last()[rid] = last;
+      c_cpy()[rid] = -1;
+      c_qlen()[rid] = qlen;
+      c_npre()[rid] += 1;
     }
     if (own(x)) { L_used -= kv; L_skv -= kv; L_final -= (int64_t)pl + dl - 1; }
     if (rf & kCopy) {
@@ -591,7 +598,7 @@ struct Sim {
       if (own(x)) L_ncopy -= 1;
     }
     batch_remove(x, idx);
-    n_preempt += 1;
+    if (lane == 0) W->ct.n_preempt += 1;
     log(KVSIM_EV_PREEMPT, x, rid, qlen, 0);
     q_push_front(queue_of(x), rid, qlen);
   }
@@ -599,37 +606,37 @@ struct Sim {
   // ------------------------------------------------------------ link FIFO
   KV_DEV double link_get(int s, int d) {
     if (policy == KVSIM_POLICY_ACCELLM) return get(L_link, s);  // only (s, s^1)
-    return link_[s * n + d];
+    return link_()[s * n + d];
   }
   KV_DEV void link_set(int s, int d, double v) {
     if (policy == KVSIM_POLICY_ACCELLM) {
       if (own(s)) L_link = v;
     } else {
       simt::sync();  // every lane has read the old value
-      if (lane == 0) link_[s * n + d] = v;
+      if (lane == 0) link_()[s * n + d] = v;
       simt::sync();
     }
   }
-  KV_DEV double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
+  KV_DEV_NOINLINE double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
     const double busy = link_get(s, d);
-    const double tail = kadd(t_done, transfer_latency(f, kmul((double)s1, f.kvb_layer)));
+    const double tail = kadd(t_done, transfer_latency(PC.f, kmul((double)s1, PC.f.kvb_layer)));
     const double start = t_start > busy ? t_start : busy;
-    const double full = kadd(start, transfer_latency(f, kmul((double)s1, f.kvb)));
+    const double full = kadd(start, transfer_latency(PC.f, kmul((double)s1, PC.f.kvb)));
     const double fin = tail > full ? tail : full;
     link_set(s, d, fin);
-    pf_tokens += s1;
+    if (lane == 0) W->ct.pf_tokens += s1;
     log(KVSIM_EV_TRANSFER, s, d, 0, s1);
     return fin;
   }
 
   // ------------------------------------------- decode step (splitwise/accellm)
-  KV_DEV void step_start(int x, double t) {
+  KV_DEV_NOINLINE void step_start(int x, double t) {
     int32_t nb = get(L_nb, x);
     if (nb == 0) return;
     const bool acc = policy == KVSIM_POLICY_ACCELLM;
     bool preempted = false;
     for (;;) {
-      if (get(L_used, x) + nb <= f.cap) break;
+      if (get(L_used, x) + nb <= PC.f.cap) break;
       if (acc) {
         Found v = largest_copy_on(x);
         if (v.where) { evict(x, v); continue; }
@@ -647,7 +654,7 @@ struct Sim {
       const int y = x ^ 1;
       for (;;) {
         const int32_t m = get(L_ncopy, x);
-        if (get(L_used, y) + m <= f.cap) {
+        if (get(L_used, y) + m <= PC.f.cap) {
           add_used(y, m);
           if (own(y)) L_copy_tok += m;
           break;
@@ -658,7 +665,7 @@ struct Sim {
     }
     const int64_t K = get(L_skv, x);
     add_used(x, nb);
-    const double lat = decode_latency(f, nb, K);
+    const double lat = decode_latency(PC.f, nb, K);
     if (own(x)) {
       L_job = JOB_STEP;
       L_job_start = t;
@@ -672,9 +679,9 @@ struct Sim {
     }
   }
 
-  KV_DEV void step_end(int x, double t) {
+  KV_DEV_NOINLINE void step_end(int x, double t) {
     account_job(x, t);
-    n_steps += 1;
+    if (lane == 0) W->ct.n_steps += 1;
     const StepOut o = step_loop(x, t);
     const int32_t surv = o.nb_old - o.completed;
     if (own(x)) {
@@ -694,9 +701,9 @@ struct Sim {
       if (o.m_copies > 0) {
         const double busy = get(L_link, x);
         const double start = t > busy ? t : busy;
-        const double fin = kadd(start, transfer_latency(f, kmul((double)o.m_copies, f.kvb)));
+        const double fin = kadd(start, transfer_latency(PC.f, kmul((double)o.m_copies, PC.f.kvb)));
         if (own(x)) { L_link = fin; L_mirror_fin = fin; }
-        mir_tokens += o.m_copies;
+        if (lane == 0) W->ct.mir_tokens += o.m_copies;
         log(KVSIM_EV_TRANSFER, x, y, 1, o.m_copies);
       }
     }
@@ -713,7 +720,7 @@ struct Sim {
   // processed here in one register loop plus a single pass over the batch.
   // Events of independent instances/pairs commute with them, so every
   // per-request timestamp, ledger value and decision is unchanged.
-  KV_DEV void fast_forward(int x, double t) {
+  KV_DEV_NOINLINE void fast_forward(int x, double t) {
     (void)t;
     const int32_t B = get(L_nb, x);
     if (B <= 0) return;
@@ -731,7 +738,7 @@ struct Sim {
       const bool all_busy = simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
       if (!all_busy) {
         if (get(Q_n, 0) != 0) return;
-        if (simt::ballot(lane >= n_prefill && lane < n && L_final > f.cap) != 0) return;
+        if (simt::ballot(lane >= n_prefill && lane < n && L_final > PC.f.cap) != 0) return;
       }
       double pt = (lane < n_prefill && L_job != JOB_NONE) ? L_busy_until : kInf;
       int32_t pk = 2 * 64 + lane;
@@ -774,19 +781,19 @@ struct Sim {
       if (yt < ht || (yt == ht && yk < hk)) { ht = yt; hk = yk; }
       m = get(L_ncopy, x);
       if (m > 0) {
-        const int64_t roomy = (f.cap - get(L_used, y)) / m;
+        const int64_t roomy = (PC.f.cap - get(L_used, y)) / m;
         if (roomy < kmax) kmax = roomy;
       }
     }
     {
-      const int64_t roomx = (f.cap - get(L_used, x)) / B;
+      const int64_t roomx = (PC.f.cap - get(L_used, x)) / B;
       if (roomx < kmax) kmax = roomx;
-      const int64_t ev_room = event_budget - n_events;
+      const int64_t ev_room = PC.event_budget - n_events;
       if (ev_room < kmax) kmax = ev_room;
     }
     if (kmax < 1) return;
     const double mr = get(L_ni, x) > 0 ? get(L_min_ready, x) : kInf;
-    const int32_t key = 3 * 64 + x;
+    const int32_t xkey = 3 * 64 + x;
     double e = get(L_busy_until, x);
     const double e1 = e;
     double js = get(L_job_start, x);
@@ -797,22 +804,24 @@ struct Sim {
     int64_t K = get(L_skv, x);
     double prev = js, G = 0.0;
     int64_t j = 0, tw = 0;
-    const double mbytes = kmul((double)m, f.kvb);
+    const double mlat = transfer_latency(PC.f, kmul((double)m, PC.f.kvb));
+    const double comp = kdiv(kmul(PC.f.two_p, (double)B), PC.f.pf_den);  // decode compute floor
+    const double kvb = PC.f.kvb, Wb = PC.f.W, mden = PC.f.mem_den;
     const double now0 = now;
     while (j < kmax) {
-      if (!(e < ht || (e == ht && key < hk))) break;
+      if (!(e < ht || (e == ht && xkey < hk))) break;
       if (e >= mr) break;
       // virtual step-end event at e ...
       now = e;
-      if (js >= warmup) busy = kadd(busy, ksub(e, js));
-      if (e >= warmup) tw += B;
+      if (js >= PC.warmup) busy = kadd(busy, ksub(e, js));
+      if (e >= PC.warmup) tw += B;
       if (j >= 1) {
         const double g = ksub(e, prev);
         if (g > G) G = g;
       }
       if (m > 0) {
         const double st = e > link ? e : link;
-        link = kadd(st, transfer_latency(f, mbytes));
+        link = kadd(st, mlat);
         mfin = link;
         log(KVSIM_EV_TRANSFER, x, y, 1, m);
       }
@@ -822,16 +831,16 @@ struct Sim {
       log(KVSIM_EV_STEP_START, x, B, 0, K);
       prev = e;
       js = e;
-      e = kadd(e, decode_latency(f, B, K));
+      e = kadd(e, kvsim_math::kmax(kdiv(kadd(Wb, kmul((double)K, kvb)), mden), comp));
       ++j;
     }
     now = now0;
     if (j == 0) return;
-    n_steps += j;
+    if (lane == 0) W->ct.n_steps += j;
     n_events += j;
-    tok_total += j * B;
-    tok_window += tw;
-    mir_tokens += j * m;
+    if (lane == 0) W->ct.tok_total += j * B;
+    if (lane == 0) W->ct.tok_window += tw;
+    if (lane == 0) W->ct.mir_tokens += j * m;
     if (prev > t_last) t_last = prev;
     if (own(x)) {
       L_busy_time = busy;
@@ -855,7 +864,7 @@ struct Sim {
     for (int32_t q = lane; q < B; q += 32) {
       const int32_t rf = rem_a[q];
       double tb = tbt_a[q];
-      const double last = (rf & kJoin) ? c_last[b_rid(x)[q]] : pe_old;
+      const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe_old;
       double g1 = ksub(e1, last);
       if (G > g1) g1 = G;
       rem_a[q] = ((rf & kRemMask) - (int32_t)j) | (rf & kCopy);
@@ -869,11 +878,11 @@ struct Sim {
   // join, memory shortfall, rebalance move, switch) and before the next
   // arrival. Other pairs only interact through arrivals.
   struct Chain {
-    double e, js, busy, link, mfin, prev, G, e1, pe_old, mr;
+    double e, js, busy, link, mfin, prev, G, e1, pe_old, mr, comp, mlat;
     int64_t K, used, tw, lim_kv, i;
     int32_t B, m, minrem, z;
   };
-  KV_DEV void chain_init(Chain& c, int z) {
+  KV_DEV_NOINLINE void chain_init(Chain& c, int z) {
     c.z = z;
     c.B = get(L_nb, z);
     c.e = get(L_busy_until, z);
@@ -902,15 +911,17 @@ struct Sim {
       }
     }
     c.lim_kv = simt::warp_min(kvmin);
+    c.comp = kdiv(kmul(PC.f.two_p, (double)c.B), PC.f.pf_den);
+    c.mlat = transfer_latency(PC.f, kmul((double)c.m, PC.f.kvb));
   }
-  KV_DEV void chain_commit(Chain& c, int64_t used_partner_add) {
+  KV_DEV_NOINLINE void chain_commit(Chain& c, int64_t used_partner_add) {
     const int z = c.z;
     if (c.i > 0) {
-      n_steps += c.i;
+      if (lane == 0) W->ct.n_steps += c.i;
       n_events += c.i;
-      tok_total += c.i * c.B;
-      tok_window += c.tw;
-      mir_tokens += c.i * c.m;
+      if (lane == 0) W->ct.tok_total += c.i * c.B;
+      if (lane == 0) W->ct.tok_window += c.tw;
+      if (lane == 0) W->ct.mir_tokens += c.i * c.m;
       if (c.prev > t_last) t_last = c.prev;
       if (own(z)) {
         L_busy_time = c.busy;
@@ -927,7 +938,7 @@ struct Sim {
       for (int32_t q = lane; q < c.B; q += 32) {
         const int32_t rf = rem_a[q];
         const double tb = tbt_a[q];
-        const double last = (rf & kJoin) ? c_last[b_rid(z)[q]] : c.pe_old;
+        const double last = (rf & kJoin) ? c_last()[b_rid(z)[q]] : c.pe_old;
         double g1 = ksub(c.e1, last);
         if (c.G > g1) g1 = c.G;
         rem_a[q] = ((rf & kRemMask) - (int32_t)c.i) | (rf & kCopy);
@@ -941,7 +952,7 @@ struct Sim {
       L_copy_tok += used_partner_add;
     }
   }
-  KV_DEV void fast_forward_pair(int x) {
+  KV_DEV_NOINLINE void fast_forward_pair(int x) {
     const int y = x ^ 1;
     if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
     if (get(L_nb, x) <= 0 || get(L_minrem, x) < 2) return;
@@ -969,7 +980,7 @@ struct Sim {
     const int64_t loadx0 = load_of(x), loady0 = load_of(y);
     int64_t copy_add_x = 0, copy_add_y = 0;  // mirror reservations landing on x / y
     const double now0 = now;
-    int64_t budget_left = event_budget - n_events;
+    int64_t budget_left = PC.event_budget - n_events;
     for (;;) {
       // next chained event: the earlier step end, ties to the lower id
       const bool pickA = !(b.e < a.e || (b.e == a.e && y < x));
@@ -993,18 +1004,18 @@ struct Sim {
         }
       }
       // memory for z's next step start: B on z, m mirror lines on the partner
-      if (c.used + c.B > f.cap || o.used + c.m > f.cap) break;
+      if (c.used + c.B > PC.f.cap || o.used + c.m > PC.f.cap) break;
       // ---- commit the virtual step end of z at c.e and its next step start
       now = c.e;
-      if (c.js >= warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
-      if (c.e >= warmup) c.tw += c.B;
+      if (c.js >= PC.warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
+      if (c.e >= PC.warmup) c.tw += c.B;
       if (c.i >= 1) {
         const double g = ksub(c.e, c.prev);
         if (g > c.G) c.G = g;
       }
       if (c.m > 0) {
         const double st = c.e > c.link ? c.e : c.link;
-        c.link = kadd(st, transfer_latency(f, kmul((double)c.m, f.kvb)));
+        c.link = kadd(st, c.mlat);
         c.mfin = c.link;
         log(KVSIM_EV_TRANSFER, z, z ^ 1, 1, c.m);
       }
@@ -1016,7 +1027,7 @@ struct Sim {
       log(KVSIM_EV_STEP_START, z, c.B, 0, c.K);
       c.prev = c.e;
       c.js = c.e;
-      c.e = kadd(c.e, decode_latency(f, c.B, c.K));
+      c.e = kadd(c.e, kvsim_math::kmax(kdiv(kadd(PC.f.W, kmul((double)c.K, PC.f.kvb)), PC.f.mem_den), c.comp));
       c.i += 1;
       budget_left -= 1;
     }
@@ -1031,15 +1042,15 @@ struct Sim {
   }
 
   // ------------------------------------------------------------- unified
-  KV_DEV void unified_start(int x, double t) {
+  KV_DEV_NOINLINE void unified_start(int x, double t) {
     int32_t nb = get(L_nb, x);
-    while (get(L_used, x) + nb > f.cap) {
+    while (get(L_used, x) + nb > PC.f.cap) {
       preempt_newest(x);
       nb -= 1;
     }
     add_used(x, nb);
     const int64_t K = get(L_skv, x);
-    // FCFS admission under budget and memory (prefix-closed tests)
+    // FCFS admission under PC.budget and memory (prefix-closed tests)
     const int32_t h = get(Q_head, x), qn = get(Q_n, x);
     int64_t used = get(L_used, x);
     int32_t k = 0;
@@ -1049,10 +1060,10 @@ struct Sim {
       const bool valid = i < qn;
       int32_t rid = 0;
       int64_t len = 0;
-      if (valid) { rid = q_at(x, h, i); len = c_qlen[rid]; }
+      if (valid) { rid = q_at(x, h, i); len = c_qlen()[rid]; }
       const int64_t incl = simt::warp_incl_scan(len);
-      const bool okb = (k == 0 && lane == 0) || s1 + incl <= budget;
-      const bool okm = used + incl <= f.cap;
+      const bool okb = (k == 0 && lane == 0) || s1 + incl <= PC.budget;
+      const bool okm = used + incl <= PC.f.cap;
       const unsigned fail = simt::ballot(valid && !(okb && okm));
       const int32_t nvalid = simt::popc(simt::ballot(valid));
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
@@ -1071,7 +1082,7 @@ struct Sim {
       add_used(x, s1);
     }
     if (nb == 0 && k == 0) return;
-    const double lat = kadd(k ? prefill_latency(f, s1, s2) : 0.0, nb ? decode_latency(f, nb, K) : 0.0);
+    const double lat = kadd(k ? prefill_latency(PC.f, s1, s2) : 0.0, nb ? decode_latency(PC.f, nb, K) : 0.0);
     if (own(x)) {
       L_job = JOB_STEP;
       L_job_start = t;
@@ -1083,9 +1094,9 @@ struct Sim {
     if (k == 0 && chain_steps) fast_forward(x, t);
   }
 
-  KV_DEV void unified_end(int x, double t) {
+  KV_DEV_NOINLINE void unified_end(int x, double t) {
     account_job(x, t);
-    n_steps += 1;
+    if (lane == 0) W->ct.n_steps += 1;
     const StepOut o = step_loop(x, t);
     int32_t nb = o.nb_old - o.completed;
     int64_t skv = get(L_skv, x) - o.kv_done + nb;
@@ -1102,19 +1113,19 @@ struct Sim {
       if (act) {
         rid = j_rid(x)[i];
         em = emit_prefill_token(rid, t);
-        dl = c_dl[rid];
-        pl = c_pl[rid];
+        dl = c_dl()[rid];
+        pl = c_pl()[rid];
       }
       const bool done = act && em == dl;
       const bool join = act && !done;
-      if (done) { c_done[rid] = t; kvfree += (int64_t)pl + em - 1; }
+      if (done) { c_done()[rid] = t; kvfree += (int64_t)pl + em - 1; }
       const unsigned jm = simt::ballot(join);
       if (join) {
         const int32_t pos = nb + add + simt::popc(jm & simt::lanemask_lt());
         b_rid(x)[pos] = rid;
         b_rem(x)[pos] = dl - em;
         b_kvb(x)[pos] = pl + dl - 1;
-        b_tbt(x)[pos] = c_tbt[rid];
+        b_tbt(x)[pos] = c_tbt()[rid];
         kvadd += (int64_t)pl + em - 1;
         if (dl - em < minrem) minrem = dl - em;
       }
@@ -1126,7 +1137,7 @@ struct Sim {
     minrem = simt::warp_min(minrem);
     simt::sync();
     count_tokens(k, t);
-    if (k > 0) n_prefills += 1;
+    if (k > 0) if (lane == 0) W->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
       L_used -= freed + kvfree;
@@ -1141,7 +1152,7 @@ struct Sim {
   }
 
   // ------------------------------------------------------------ splitwise
-  KV_DEV void sw_try_start(double t) {
+  KV_DEV_NOINLINE void sw_try_start(double t) {
     for (int p = 0; p < n_prefill; ++p) {
       if (get(L_job, p) != JOB_NONE) continue;
       int32_t qn = get(Q_n, 0);
@@ -1155,14 +1166,14 @@ struct Sim {
         const int32_t i = k + lane;
         const bool valid = i < qn;
         int32_t crid = 0, clen = 0;
-        if (valid) { crid = q_at(0, h, i); clen = c_qlen[crid]; }
+        if (valid) { crid = q_at(0, h, i); clen = c_qlen()[crid]; }
         const int32_t nvalid = simt::popc(simt::ballot(valid));
         for (int32_t c = 0; c < nvalid; ++c) {
           const int32_t rid = simt::shfl(crid, c);
           const int64_t len = simt::shfl(clen, c);
-          if (k > 0 && s1 + len > budget) { stop = true; break; }
+          if (k > 0 && s1 + len > PC.budget) { stop = true; break; }
           // destination: decode instance with most free tokens, ties lowest id
-          int64_t fr = (lane >= n_prefill && lane < n) ? f.cap - L_used : INT64_MIN;
+          int64_t fr = (lane >= n_prefill && lane < n) ? PC.f.cap - L_used : INT64_MIN;
           const int64_t best = simt::warp_max(fr);
           const int d = simt::ffs(simt::ballot(fr == best)) - 1;
           if (best < len) { stop = true; break; }
@@ -1177,7 +1188,7 @@ struct Sim {
       if (k == 0) continue;
       q_pop(0, k, s1);
       add_used(p, s1);
-      const double lat = prefill_latency(f, s1, s2);
+      const double lat = prefill_latency(PC.f, s1, s2);
       if (own(p)) {
         L_job = JOB_PREFILL;
         L_job_start = t;
@@ -1189,9 +1200,9 @@ struct Sim {
     }
   }
 
-  KV_DEV void sw_prefill_done(int p, double t) {
+  KV_DEV_NOINLINE void sw_prefill_done(int p, double t) {
     account_job(p, t);
-    n_prefills += 1;
+    if (lane == 0) W->ct.n_prefills += 1;
     const int32_t k = get(L_njob, p);
     const int64_t s1 = get(L_job_s1, p);
     const double jstart = get(L_job_start, p);
@@ -1207,11 +1218,11 @@ struct Sim {
         const int32_t rid = j_rid(p)[i];
         const int32_t d = j_dst(p)[i];
         const int32_t em = emit_prefill_token(rid, t);
-        const int32_t dl = c_dl[rid];
-        const int64_t kv = (int64_t)c_pl[rid] + em - 1;
+        const int32_t dl = c_dl()[rid];
+        const int64_t kv = (int64_t)c_pl()[rid] + em - 1;
         done = em == dl;
         if (done) {
-          c_done[rid] = t;
+          c_done()[rid] = t;
           simt::atomic_add_smem(&W->acc_b[d], kv);
         } else {
           simt::atomic_add_smem(&W->acc_a[d], kv);
@@ -1250,12 +1261,12 @@ struct Sim {
       if (act) { rid = j_rid(p)[i]; d = j_dst(p)[i]; }
       const double fin_d = simt::shfl(fin_mine, d);
       const int32_t base_d = simt::shfl(base_mine, d);
-      if (act && c_em[rid] != c_dl[rid]) {
+      if (act && c_em()[rid] != c_dl()[rid]) {
         const int32_t pos = base_d + simt::atomic_add_smem(&W->cnt[d], 1);
         i_rid(d)[pos] = rid;
         i_ready(d)[pos] = fin_d;
-        c_cpy[rid] = -1;
-        simt::atomic_add_smem(&W->acc_b[d], (int64_t)c_pl[rid] + c_dl[rid] - 1);
+        c_cpy()[rid] = -1;
+        simt::atomic_add_smem(&W->acc_b[d], (int64_t)c_pl()[rid] + c_dl()[rid] - 1);
       }
     }
     simt::sync();
@@ -1269,11 +1280,11 @@ struct Sim {
     const int q = x >> 1;
     if (get(Q_n, q) == 0) return false;
     const int32_t rid = q_at(q, get(Q_head, q), 0);
-    const int64_t len = c_qlen[rid];
-    return get(L_used, x) - get(L_copy_tok, x) + len <= f.cap;
+    const int64_t len = c_qlen()[rid];
+    return get(L_used, x) - get(L_copy_tok, x) + len <= PC.f.cap;
   }
   // move every request whose primary is x and that holds a copy on x^1
-  KV_DEV void move_all_to_partner(int x, double t) {
+  KV_DEV_NOINLINE void move_all_to_partner(int x, double t) {
     const int y = x ^ 1;
     const double mfin = get(L_mirror_fin, x);
     const double pend = get(L_prev_end, x);
@@ -1300,15 +1311,15 @@ struct Sim {
       if (mv) {
         const int32_t rem = rf & kRemMask;
         const bool joiner = (rf & kJoin) != 0;
-        const double fresh = joiner ? c_fresh[rid] : mfin;
+        const double fresh = joiner ? c_fresh()[rid] : mfin;
         const double ready = fresh > t ? fresh : t;
-        const int32_t dl = c_dl[rid];
-        c_em[rid] = dl - rem;
-        c_tbt[rid] = tb;
-        if (!joiner) c_last[rid] = pend;
-        c_cpy[rid] = x;
-        c_fresh[rid] = t;
-        c_nmv[rid] += 1;
+        const int32_t dl = c_dl()[rid];
+        c_em()[rid] = dl - rem;
+        c_tbt()[rid] = tb;
+        if (!joiner) c_last()[rid] = pend;
+        c_cpy()[rid] = x;
+        c_fresh()[rid] = t;
+        c_nmv()[rid] += 1;
         const int32_t pos = ni_y + moved + simt::popc(mm & simt::lanemask_lt());
         i_rid(y)[pos] = rid;
         i_ready(y)[pos] = ready;
@@ -1331,7 +1342,7 @@ struct Sim {
       int32_t rid = 0;
       double rd = 0.0;
       if (act) { rid = i_rid(x)[j]; rd = i_ready(x)[j]; }
-      const bool mv = act && c_cpy[act ? rid : 0] == y;
+      const bool mv = act && c_cpy()[act ? rid : 0] == y;
       const bool st = act && !mv;
       const unsigned mm = simt::ballot(mv), sm = simt::ballot(st);
       simt::sync();
@@ -1341,15 +1352,15 @@ struct Sim {
         i_ready(x)[k] = rd;
       }
       if (mv) {
-        const double fresh = c_fresh[rid];
+        const double fresh = c_fresh()[rid];
         const double ready = fresh > t ? fresh : t;
-        c_cpy[rid] = x;
-        c_fresh[rid] = t;
-        c_nmv[rid] += 1;
+        c_cpy()[rid] = x;
+        c_fresh()[rid] = t;
+        c_nmv()[rid] += 1;
         const int32_t pos = ni_y + moved + simt::popc(mm & simt::lanemask_lt());
         i_rid(y)[pos] = rid;
         i_ready(y)[pos] = ready;
-        kv_moved += (int64_t)c_pl[rid] + c_em[rid] - 1;
+        kv_moved += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
         if (ready < mn) mn = ready;
       }
       log_lanes(mv, KVSIM_EV_MOVE, x, rid, y, 0);
@@ -1367,7 +1378,7 @@ struct Sim {
     mx = simt::warp_min(mx);
     simt::sync();
     const int64_t kv_all = kv_b + kv_i;
-    n_moves += moved;
+    if (lane == 0) W->ct.n_moves += moved;
     if (own(x)) {
       L_nb = keep;
       L_ni = ikeep;
@@ -1385,7 +1396,7 @@ struct Sim {
     }
   }
 
-  KV_DEV void acc_start_job(int x, double t) {
+  KV_DEV_NOINLINE void acc_start_job(int x, double t) {
     const int q = x >> 1;
     const int32_t h = get(Q_head, q);
     int32_t k = 0;
@@ -1397,11 +1408,11 @@ struct Sim {
       const bool valid = i < qn;
       int32_t rid = 0;
       int64_t len = 0;
-      if (valid) { rid = q_at(q, h, i); len = c_qlen[rid]; }
+      if (valid) { rid = q_at(q, h, i); len = c_qlen()[rid]; }
       const int64_t incl = simt::warp_incl_scan(len);
       const int64_t used = get(L_used, x);
-      const bool okb = (k == 0 && lane == 0) || s1 + incl <= budget;
-      const bool okm = used + incl <= f.cap;
+      const bool okb = (k == 0 && lane == 0) || s1 + incl <= PC.budget;
+      const bool okm = used + incl <= PC.f.cap;
       const unsigned fail = simt::ballot(valid && !(okb && okm));
       const int32_t nvalid = simt::popc(simt::ballot(valid));
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
@@ -1418,16 +1429,16 @@ struct Sim {
       const int64_t lenf = simt::shfl(len, f0);
       if (!fb) break;
       // memory: evict copies held on x, largest first
-      while (get(L_used, x) + lenf > f.cap) {
+      while (get(L_used, x) + lenf > PC.f.cap) {
         Found v = largest_copy_on(x);
         if (!v.where) break;
         evict(x, v);
       }
-      if (get(L_used, x) + lenf > f.cap) break;
+      if (get(L_used, x) + lenf > PC.f.cap) break;
     }
     simt::sync();
     q_pop(q, k, s1);
-    const double lat = prefill_latency(f, s1, s2);
+    const double lat = prefill_latency(PC.f, s1, s2);
     if (own(x)) {
       L_job = JOB_PREFILL;
       L_job_start = t;
@@ -1438,7 +1449,7 @@ struct Sim {
     log(KVSIM_EV_PREFILL_START, x, k, k ? j_rid(x)[0] : -1, s1);
   }
 
-  KV_DEV bool try_switch(int x, double t) {
+  KV_DEV_NOINLINE bool try_switch(int x, double t) {
     if (!head_admissible(x)) return false;
     if (own(x)) L_pend = 0;
     move_all_to_partner(x, t);
@@ -1448,7 +1459,7 @@ struct Sim {
     return true;
   }
 
-  KV_DEV void ensure_prefill(int q, double t) {
+  KV_DEV_NOINLINE void ensure_prefill(int q, double t) {
     if (get(Q_n, q) == 0) return;
     const int a = 2 * q, b = a + 1;
     if (get(L_role, a) == ROLE_PREFILL || get(L_role, b) == ROLE_PREFILL || get(L_pend, a) || get(L_pend, b))
@@ -1459,7 +1470,7 @@ struct Sim {
   }
 
   // rebalance_pair at x's boundary (SEMANTICS §6)
-  KV_DEV void rebalance(int x, double t) {
+  KV_DEV_NOINLINE void rebalance(int x, double t) {
     const int y = x ^ 1;
     if (get(L_role, y) != ROLE_DECODE || get(L_pend, y)) return;
     int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
@@ -1491,7 +1502,7 @@ struct Sim {
     }
   }
   // move batch slot idx of x to y's incoming (zero-byte label swap)
-  KV_DEV void move_one(int x, int32_t idx, double t) {
+  KV_DEV_NOINLINE void move_one(int x, int32_t idx, double t) {
     const int y = x ^ 1;
     const int32_t rid = b_rid(x)[idx];
     const int32_t rf = b_rem(x)[idx];
@@ -1499,28 +1510,28 @@ struct Sim {
     const int64_t kv = (int64_t)b_kvb(x)[idx] - rem;
     const double tb = b_tbt(x)[idx];
     const bool joiner = (rf & kJoin) != 0;
-    const double fresh = joiner ? c_fresh[rid] : get(L_mirror_fin, x);
+    const double fresh = joiner ? c_fresh()[rid] : get(L_mirror_fin, x);
     const double ready = fresh > t ? fresh : t;
-    const double last = joiner ? c_last[rid] : get(L_prev_end, x);
-    const int32_t dl = c_dl[rid];
+    const double last = joiner ? c_last()[rid] : get(L_prev_end, x);
+    const int32_t dl = c_dl()[rid];
     simt::sync();
     if (lane == 0) {
-      c_em[rid] = dl - rem;
-      c_tbt[rid] = tb;
-      c_last[rid] = last;
-      c_cpy[rid] = x;
-      c_fresh[rid] = t;
-      c_nmv[rid] += 1;
+      c_em()[rid] = dl - rem;
+      c_tbt()[rid] = tb;
+      c_last()[rid] = last;
+      c_cpy()[rid] = x;
+      c_fresh()[rid] = t;
+      c_nmv()[rid] += 1;
     }
     batch_remove(x, idx);
     incoming_append(y, rid, ready);
     if (own(x)) { L_skv -= kv; L_ncopy -= 1; L_copy_tok += kv; }
     if (own(y)) { L_skv_in += kv; L_copy_tok -= kv; }
-    n_moves += 1;
+    if (lane == 0) W->ct.n_moves += 1;
     log(KVSIM_EV_MOVE, x, rid, y, 0);
   }
 
-  KV_DEV void acc_boundary(int x, double t) {
+  KV_DEV_NOINLINE void acc_boundary(int x, double t) {
     join(x, t);
     if (get(L_pend, x)) {
       if (own(x)) L_pend = 0;
@@ -1532,9 +1543,9 @@ struct Sim {
     step_start(x, t);
   }
 
-  KV_DEV void acc_prefill_done(int x, double t) {
+  KV_DEV_NOINLINE void acc_prefill_done(int x, double t) {
     account_job(x, t);
-    n_prefills += 1;
+    if (lane == 0) W->ct.n_prefills += 1;
     const int y = x ^ 1;
     const int32_t k = get(L_njob, x);
     const double jstart = get(L_job_start, x);
@@ -1549,10 +1560,10 @@ struct Sim {
       if (act) {
         const int32_t rid = j_rid(x)[i];
         const int32_t em = emit_prefill_token(rid, t);
-        done = em == c_dl[rid];
+        done = em == c_dl()[rid];
         if (done) {
-          c_done[rid] = t;
-          kvfree += (int64_t)c_pl[rid] + em - 1;
+          c_done()[rid] = t;
+          kvfree += (int64_t)c_pl()[rid] + em - 1;
         }
       }
       completed += simt::popc(simt::ballot(done));
@@ -1575,13 +1586,13 @@ struct Sim {
       int64_t kv = 0;
       if (act) {
         rid = j_rid(x)[i];
-        surv = c_em[rid] != c_dl[rid];
-        if (surv) kv = (int64_t)c_pl[rid] + c_em[rid] - 1;
+        surv = c_em()[rid] != c_dl()[rid];
+        if (surv) kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
       }
       bool cp = false;
       if (!seq) {
         const int64_t incl = simt::warp_incl_scan(kv);
-        const bool fits = used_y + incl <= f.cap;
+        const bool fits = used_y + incl <= PC.f.cap;
         const unsigned bad = simt::ballot(surv && !fits);
         if (!bad) {
           cp = surv;
@@ -1594,7 +1605,7 @@ struct Sim {
           for (int l = f0; l < 32; ++l) {
             const bool sl = simt::shfl((int32_t)surv, l) != 0;
             const int64_t kl = simt::shfl(kv, l);
-            if (sl && used_y + kl <= f.cap) {
+            if (sl && used_y + kl <= PC.f.cap) {
               used_y += kl;
               if (lane == l) cp = true;
             }
@@ -1604,14 +1615,14 @@ struct Sim {
         for (int l = 0; l < 32; ++l) {
           const bool sl = simt::shfl((int32_t)surv, l) != 0;
           const int64_t kl = simt::shfl(kv, l);
-          if (sl && used_y + kl <= f.cap) {
+          if (sl && used_y + kl <= PC.f.cap) {
             used_y += kl;
             if (lane == l) cp = true;
           }
         }
       }
-      if (cp) c_cpy[rid] = y;
-      else if (surv) c_cpy[rid] = -1;
+      if (cp) c_cpy()[rid] = y;
+      else if (surv) c_cpy()[rid] = -1;
       s1c += simt::warp_sum(cp ? kv : (int64_t)0);
       ncopy += simt::popc(simt::ballot(cp));
     }
@@ -1632,22 +1643,22 @@ struct Sim {
       bool surv = false;
       if (act) {
         rid = j_rid(x)[i];
-        surv = c_em[rid] != c_dl[rid];
+        surv = c_em()[rid] != c_dl()[rid];
       }
       const unsigned sm = simt::ballot(surv);
       if (surv) {
-        const int32_t em = c_em[rid], dl = c_dl[rid], pl = c_pl[rid];
-        const bool hasc = c_cpy[rid] == y;
-        if (hasc) c_fresh[rid] = fin;
+        const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
+        const bool hasc = c_cpy()[rid] == y;
+        if (hasc) c_fresh()[rid] = fin;
         const int32_t pos = nb + add + simt::popc(sm & simt::lanemask_lt());
         b_rid(x)[pos] = rid;
         b_rem(x)[pos] = (dl - em) | kJoin | (hasc ? kCopy : 0);
         b_kvb(x)[pos] = pl + dl - 1;
-        b_tbt(x)[pos] = c_tbt[rid];
+        b_tbt(x)[pos] = c_tbt()[rid];
         kvadd += (int64_t)pl + em - 1;
         if (dl - em < minrem) minrem = dl - em;
       }
-      addc += simt::popc(simt::ballot(surv && c_cpy[surv ? rid : 0] == y));
+      addc += simt::popc(simt::ballot(surv && c_cpy()[surv ? rid : 0] == y));
       add += simt::popc(sm);
     }
     kvadd = simt::warp_sum(kvadd);
@@ -1671,31 +1682,31 @@ struct Sim {
   }
 
   // -------------------------------------------------------------- arrival
-  KV_DEV void arrive(double t) {
+  KV_DEV_NOINLINE void arrive(double t) {
     const int64_t rid64 = next_rid;
     const int32_t rid = (int32_t)rid64;
     int32_t pl, dl;
-    if (tr_arr != nullptr) {
-      pl = tr_pl[rid];
-      dl = tr_dl[rid];
+    if (PC.tr_arr != nullptr) {
+      pl = PC.tr_pl[rid];
+      dl = PC.tr_dl[rid];
     } else {
-      pl = uniform_range(draw_k(key, rid64, 0), pmin, pmax);
-      dl = uniform_range(draw_k(key, rid64, 1), dmin, dmax);
+      pl = uniform_range(draw_k(PC.key, rid64, 0), PC.pmin, PC.pmax);
+      dl = uniform_range(draw_k(PC.key, rid64, 1), PC.dmin, PC.dmax);
     }
     if (lane == 0) {
-      c_arr[rid] = t;
-      c_pl[rid] = pl;
-      c_dl[rid] = dl;
-      c_qlen[rid] = pl;
-      c_em[rid] = 0;
-      c_cpy[rid] = -1;
-      c_tbt[rid] = 0.0;
-      c_last[rid] = 0.0;
-      c_fresh[rid] = 0.0;
-      c_first[rid] = 0.0;
-      c_done[rid] = 0.0;
-      c_nmv[rid] = 0;
-      c_npre[rid] = 0;
+      c_arr()[rid] = t;
+      c_pl()[rid] = pl;
+      c_dl()[rid] = dl;
+      c_qlen()[rid] = pl;
+      c_em()[rid] = 0;
+      c_cpy()[rid] = -1;
+      c_tbt()[rid] = 0.0;
+      c_last()[rid] = 0.0;
+      c_fresh()[rid] = 0.0;
+      c_first()[rid] = 0.0;
+      c_done()[rid] = 0.0;
+      c_nmv()[rid] = 0;
+      c_npre()[rid] = 0;
     }
     simt::sync();
     // advance the generator
@@ -1703,7 +1714,7 @@ struct Sim {
     next_rid += 1;
     gen_next();
     if (policy == KVSIM_POLICY_UNIFIED) {
-      const int64_t fr = lane < n ? f.cap - L_used - Q_tok : INT64_MIN;
+      const int64_t fr = lane < n ? PC.f.cap - L_used - Q_tok : INT64_MIN;
       const int64_t best = simt::warp_max(fr);
       const int x = simt::ffs(simt::ballot(fr == best)) - 1;
       log(KVSIM_EV_ARRIVE, x, rid, pl, 0);
@@ -1716,7 +1727,7 @@ struct Sim {
       const int np = n >> 1;
       const int64_t ua = simt::shfl(L_used, (2 * lane) & 31);
       const int64_t ub = simt::shfl(L_used, (2 * lane + 1) & 31);
-      const int64_t fr = lane < np ? (f.cap - ua) + (f.cap - ub) - Q_tok : INT64_MIN;
+      const int64_t fr = lane < np ? (PC.f.cap - ua) + (PC.f.cap - ub) - Q_tok : INT64_MIN;
       const int64_t best = simt::warp_max(fr);
       const int q = simt::ffs(simt::ballot(fr == best)) - 1;
       log(KVSIM_EV_ARRIVE, q, rid, pl, 0);
@@ -1748,8 +1759,8 @@ struct Sim {
       bool is_arrival = false;
       if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
       if (!is_arrival && ck == (1 << 20)) break;
-      if (++n_events > event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
-      ++n_loop;
+      if (++n_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
+      if (lane == 0) W->ct.n_loop += 1;
       if (is_arrival) {
         now = t_next;
         if (now > t_last) t_last = now;
@@ -1783,7 +1794,7 @@ struct Sim {
 
   // --------------------------------------------- per-point metrics (K4 fused)
   // nearest-rank selection over uint64 keys stored (as doubles' bits) in arr
-  KV_DEV void radix_select2(const double* arr, int64_t nn, int64_t k1, int64_t k2, uint64_t& r1, uint64_t& r2) {
+  KV_DEV_NOINLINE void radix_select2(const double* arr, int64_t nn, int64_t k1, int64_t k2, uint64_t& r1, uint64_t& r2) {
     uint64_t pre1 = 0, pre2 = 0, mask = 0;
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int b = lane; b < 256; b += 32) { W->hist[0][b] = 0; W->hist[1][b] = 0; }
@@ -1814,14 +1825,14 @@ struct Sim {
     r2 = pre2;
   }
 
-  KV_DEV void finalize() {
+  KV_DEV_NOINLINE void finalize() {
     kvsim_point_summary s;
     // zero everything
     {
       char* z = reinterpret_cast<char*>(&s);
       for (unsigned i = 0; i < sizeof(s); ++i) z[i] = 0;
     }
-    const kvsim_point_desc& d = A.pts[point];
+    const kvsim_point_desc& d = A->pts[point];
     const double kNaN = as_f64(0x7ff8000000000000ull);
     const double kInf = as_f64(0x7ff0000000000000ull);
     s.status = status;
@@ -1831,34 +1842,35 @@ struct Sim {
     s.n_requests = status == KVSIM_OK ? N : 0;
     if (status == KVSIM_OK || status == KVSIM_E_EVENT_BUDGET) {
       s.n_requests = N;
-      s.n_events = n_events; s.n_steps = n_steps; s.n_prefills = n_prefills; s.n_moves = n_moves;
-      s.n_preemptions = n_preempt; s.n_evictions = n_evict;
-      s.tokens_total = tok_total; s.tokens_window = tok_window;
-      s.link_prefill_tokens = pf_tokens; s.link_mirror_tokens = mir_tokens;
+      const Counters ct = W->ct;
+      s.n_events = n_events; s.n_steps = ct.n_steps; s.n_prefills = ct.n_prefills; s.n_moves = ct.n_moves;
+      s.n_preemptions = ct.n_preempt; s.n_evictions = ct.n_evict;
+      s.tokens_total = ct.tok_total; s.tokens_window = ct.tok_window;
+      s.link_prefill_tokens = ct.pf_tokens; s.link_mirror_tokens = ct.mir_tokens;
       s.makespan_s = t_last;
-      s.reserved[0] = n_loop;
+      s.reserved[0] = ct.n_loop;
       const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
       double busy = 0.0;
       for (int x = 0; x < n; ++x) busy = kadd(busy, get(L_busy_time, x));
       s.peak_kv_tokens = peak;
       s.busy_s_total = busy;
-      s.peak_kv_gb = kdiv(kmul((double)peak, f.kvb), 1e9);
-      s.link_prefill_gb = kdiv(kmul((double)pf_tokens, f.kvb), 1e9);
-      s.link_mirror_gb = kdiv(kmul((double)mir_tokens, f.kvb), 1e9);
+      s.peak_kv_gb = kdiv(kmul((double)peak, PC.f.kvb), 1e9);
+      s.link_prefill_gb = kdiv(kmul((double)ct.pf_tokens, PC.f.kvb), 1e9);
+      s.link_mirror_gb = kdiv(kmul((double)ct.mir_tokens, PC.f.kvb), 1e9);
       // records (parity configs)
-      if (A.recs != nullptr) {
-        kvsim_request_record* R = A.recs + A.rec_off[point];
+      if (A->recs != nullptr) {
+        kvsim_request_record* R = A->recs + A->rec_off[point];
         for (int64_t i = lane; i < N; i += 32) {
-          const bool dn = c_em[i] == c_dl[i];
+          const bool dn = c_em()[i] == c_dl()[i];
           kvsim_request_record r;
-          r.arrival_s = c_arr[i];
-          r.first_token_s = c_em[i] > 0 ? c_first[i] : kNaN;
-          r.completion_s = dn ? c_done[i] : kNaN;
-          r.tbt_max_s = c_tbt[i];
-          r.prompt_len = c_pl[i];
-          r.decode_len = c_dl[i];
-          r.n_moves = c_nmv[i];
-          r.n_preemptions = c_npre[i];
+          r.arrival_s = c_arr()[i];
+          r.first_token_s = c_em()[i] > 0 ? c_first()[i] : kNaN;
+          r.completion_s = dn ? c_done()[i] : kNaN;
+          r.tbt_max_s = c_tbt()[i];
+          r.prompt_len = c_pl()[i];
+          r.decode_len = c_dl()[i];
+          r.n_moves = c_nmv()[i];
+          r.n_preemptions = c_npre()[i];
           R[i] = r;
         }
       }
@@ -1874,21 +1886,21 @@ struct Sim {
         bool inc = false, dn = false;
         int32_t dl = 0;
         if (act) {
-          const double arr = c_arr[i];
-          dl = c_dl[i];
-          dn = c_em[i] == dl;
-          inc = dn && arr >= warmup;
+          const double arr = c_arr()[i];
+          dl = c_dl()[i];
+          dn = c_em()[i] == dl;
+          inc = dn && arr >= PC.warmup;
           if (inc) {
-            a = ksub(c_first[i], arr);
-            b = ksub(c_done[i], arr);
-            ts = ksub(c_done[i], c_first[i]);
-            tb = c_tbt[i];
+            a = ksub(c_first()[i], arr);
+            b = ksub(c_done()[i], arr);
+            ts = ksub(c_done()[i], c_first()[i]);
+            tb = c_tbt()[i];
           }
         }
         simt::sync();
         if (act) {
-          c_first[i] = inc ? a : kInf;
-          c_done[i] = inc ? b : kInf;
+          c_first()[i] = inc ? a : kInf;
+          c_done()[i] = inc ? b : kInf;
         }
         completed += simt::popc(simt::ballot(dn));
         const int cnt = act ? 1 : 0;
@@ -1923,10 +1935,10 @@ struct Sim {
         s.jct_max = mx_jct;
         const int64_t k50 = (50 * m + 99) / 100 - 1, k95 = (95 * m + 99) / 100 - 1;
         uint64_t r1, r2;
-        radix_select2(c_first, N, k50, k95, r1, r2);
+        radix_select2(c_first(), N, k50, k95, r1, r2);
         s.ttft_p50 = as_f64(r1);
         s.ttft_p95 = as_f64(r2);
-        radix_select2(c_done, N, k50, k95, r1, r2);
+        radix_select2(c_done(), N, k50, k95, r1, r2);
         s.jct_p50 = as_f64(r1);
         s.jct_p95 = as_f64(r2);
       } else {
@@ -1935,9 +1947,9 @@ struct Sim {
       }
       s.tbt_mean = n_tbt > 0 ? kdiv(s_tbt, (double)n_tbt) : kNaN;
       s.tbt_max = n_tbt > 0 ? tmax : kNaN;
-      const double window = ksub(t_last, warmup);
+      const double window = ksub(t_last, PC.warmup);
       if (window > 0.0) {
-        s.cost_eff = kdiv((double)tok_window, kmul(window, (double)n));
+        s.cost_eff = kdiv((double)ct.tok_window, kmul(window, (double)n));
         s.idle_frac = ksub(1.0, kdiv(busy, kmul((double)n, window)));
       } else {
         s.cost_eff = s.idle_frac = kNaN;
@@ -1945,29 +1957,40 @@ struct Sim {
     }
     simt::sync();
     if (lane == 0) {
-      A.out[point] = s;
-      if (A.ev_count != nullptr) A.ev_count[point] = ev_n;
+      A->out[point] = s;
+      if (A->ev_count != nullptr) A->ev_count[point] = ev_n;
     }
     simt::sync();
   }
 };
 
-// Persistent warp loop: pull points from a global counter (LPT order is set
-// by the host), simulate, finalize.
-KV_DEV void sweep_warp(const SweepArgs& a, WarpScratch* w, int64_t slot) {
-  Sim sim(a, w, slot);
+// One point, simulated by the policy-specialised core.
+template <int P>
+KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot, int64_t pt) {
+  Sim<P> sim(ap, w, slot);
+  if (sim.init_point(pt)) sim.run();
+  sim.finalize();
+}
+
+// Persistent warp loop: pull points from a global counter (policy-major LPT
+// order set by the host), simulate, finalize.
+KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
+  const SweepArgs& a = *ap;
+  const int lane = simt::lane_id();
   for (;;) {
     unsigned long long p = 0;
 #if defined(KVSIM_EMU)
-    if (sim.lane == 0) p = std::atomic_ref<unsigned long long>(*a.next_point).fetch_add(1);
+    if (lane == 0) p = std::atomic_ref<unsigned long long>(*a.next_point).fetch_add(1);
 #else
-    if (sim.lane == 0) p = atomicAdd(a.next_point, 1ull);
+    if (lane == 0) p = atomicAdd(a.next_point, 1ull);
 #endif
     p = simt::shfl((uint64_t)p, 0);
     if ((int64_t)p >= a.n_pts) break;
     const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
-    if (sim.init_point(pt)) sim.run();
-    sim.finalize();
+    const int32_t pol = a.pts[pt].policy;
+    if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE>(ap, w, slot, pt);
+    else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM>(ap, w, slot, pt);
+    else run_point<KVSIM_POLICY_UNIFIED>(ap, w, slot, pt);
   }
 }
 

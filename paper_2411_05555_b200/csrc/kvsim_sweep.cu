@@ -32,13 +32,13 @@ constexpr int kWarpsPerBlock = 4;
 // MINB = minimum resident blocks per SM requested from ptxas (register cap
 // 65536 / (128 * MINB)); selected at context open (KVSIM_MINB, default below).
 template <int MINB>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(const __grid_constant__ SweepArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
   const int w = threadIdx.x >> 5;
   const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= a.slots) return;
-  kvsim_dev::sweep_warp(a, &scratch[w], slot);
+  kvsim_dev::sweep_warp(&a, &scratch[w], (int32_t)slot);
 }
 
 __global__ void kvsim_perf_kernel(const kvsim_point_desc* pts, const int32_t* pidx, const int32_t* op,

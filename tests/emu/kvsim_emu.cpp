@@ -75,7 +75,7 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
     th.emplace_back([&, w]() {
       simt::run_warp([](void* p, int) {
         Job* j = (Job*)p;
-        sweep_warp(*j->a, j->s, j->slot);
+        sweep_warp(j->a, j->s, (int32_t)j->slot);
       }, &jobs[w]);
     });
   for (auto& t : th) t.join();

@@ -63,7 +63,7 @@ def test_random_small_configs(sim):
 
 
 def test_random_medium_configs(sim):
-    check(sim, [random_small(1000 + i, max_req=400) for i in range(60)], ev=1 << 17)
+    check(sim, [random_small(1000 + i, max_req=400) for i in range(60)], ev=1 << 19)
 
 
 def test_sweep_summaries_sample(sim):

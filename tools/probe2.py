@@ -8,7 +8,7 @@ nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
 pts = config4_points(0, rates, nreq)
 sim = pkg.KvSim(0)
 sim.run(pts[:16])
-for rep in range(2):
+for rep in range(1):
     t0 = time.time(); s = sim.run(pts); dt = time.time() - t0
 reqs = sum(x.n_requests for x in s); ev = sum(x.n_events for x in s); loops = sum(x.reserved[0] for x in s)
 bad = sum(x.status != 0 for x in s)
