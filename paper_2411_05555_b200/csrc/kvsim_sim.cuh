@@ -91,7 +91,7 @@ struct SweepArgs {
 #define PC (W->pc)
 // One specialisation per policy: every `policy == ...` test folds at compile
 // time, so a warp only ever executes (and caches) its own policy's code.
-template <int POL>
+template <int POL, bool LOG>
 struct Sim {
   const SweepArgs* A;  // kernel parameters (param space; __grid_constant__)
   WarpScratch* W;      // per-warp shared scratch: point constants, counters
@@ -109,7 +109,7 @@ struct Sim {
   double now;     // time of the event being processed (event-log timestamps)
   double t_last;  // latest event time processed (makespan)
   bool chain_steps = true;  // exact step chaining (fast_forward); off = plain event loop
-  bool logging = false;     // event log requested (parity runs)
+  static constexpr bool logging = LOG;  // event log compiled in (parity runs) or out (sweeps)
   int32_t status;
   // lane-owned instance state (lane x <-> instance x)
   double L_busy_until, L_job_start, L_prev_end, L_mirror_fin, L_busy_time, L_min_ready, L_link;
@@ -168,7 +168,7 @@ struct Sim {
   }
 
   KV_DEV void log(int kind, int inst, int a, int b, int64_t c) {
-    if (!logging) return;
+    if constexpr (!LOG) return;
     if (lane == 0 && ev_n < A->ev_cap) {
       kvsim_event_record r;
       r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
@@ -178,7 +178,7 @@ struct Sim {
   }
   // lane-parallel logging: lanes with `p` log one record each (moves)
   KV_DEV void log_lanes(bool p, int kind, int inst, int a, int b, int64_t c) {
-    if (!logging) return;
+    if constexpr (!LOG) return;
     unsigned m = simt::ballot(p);
     if (p) {
       int64_t k = ev_n + simt::popc(m & simt::lanemask_lt());
@@ -265,7 +265,6 @@ struct Sim {
     }
     simt::sync();
     n_events = ev_n = 0;
-    logging = A->ev != nullptr;
     now = 0.0;
     t_last = 0.0;
     L_busy_until = L_job_start = L_prev_end = L_mirror_fin = L_busy_time = 0.0;
@@ -812,7 +811,7 @@ struct Sim {
       if (!(e < ht || (e == ht && xkey < hk))) break;
       if (e >= mr) break;
       // virtual step-end event at e ...
-      now = e;
+      if constexpr (LOG) now = e;
       if (js >= PC.warmup) busy = kadd(busy, ksub(e, js));
       if (e >= PC.warmup) tw += B;
       if (j >= 1) {
@@ -882,7 +881,7 @@ struct Sim {
     int64_t K, used, tw, lim_kv, i;
     int32_t B, m, minrem, z;
   };
-  KV_DEV_NOINLINE void chain_init(Chain& c, int z) {
+  KV_DEV void chain_init(Chain& c, int z, bool need_kvmin) {
     c.z = z;
     c.B = get(L_nb, z);
     c.e = get(L_busy_until, z);
@@ -901,20 +900,24 @@ struct Sim {
     c.m = get(L_ncopy, z);
     c.minrem = get(L_minrem, z);
     c.mr = get(L_ni, z) > 0 ? get(L_min_ready, z) : as_f64(0x7ff0000000000000ull);
-    // smallest kv among copy-holding members (rebalance candidates)
+    // smallest kv among copy-holding members (rebalance candidates); only
+    // needed when z holds more requests than its partner
     int64_t kvmin = INT64_MAX;
-    for (int32_t q = lane; q < c.B; q += 32) {
-      const int32_t rf = b_rem(z)[q];
-      if (rf & kCopy) {
-        const int64_t kv = (int64_t)b_kvb(z)[q] - (rf & kRemMask);
-        if (kv < kvmin) kvmin = kv;
+    if (need_kvmin) {
+      for (int32_t q = lane; q < c.B; q += 32) {
+        const int32_t rf = b_rem(z)[q];
+        if (rf & kCopy) {
+          const int64_t kv = (int64_t)b_kvb(z)[q] - (rf & kRemMask);
+          if (kv < kvmin) kvmin = kv;
+        }
       }
+      kvmin = simt::warp_min(kvmin);
     }
-    c.lim_kv = simt::warp_min(kvmin);
+    c.lim_kv = kvmin;
     c.comp = kdiv(kmul(PC.f.two_p, (double)c.B), PC.f.pf_den);
     c.mlat = transfer_latency(PC.f, kmul((double)c.m, PC.f.kvb));
   }
-  KV_DEV_NOINLINE void chain_commit(Chain& c, int64_t used_partner_add) {
+  KV_DEV void chain_commit(Chain& c, int64_t used_partner_add) {
     const int z = c.z;
     if (c.i > 0) {
       if (lane == 0) W->ct.n_steps += c.i;
@@ -952,6 +955,59 @@ struct Sim {
       L_copy_tok += used_partner_add;
     }
   }
+  struct ChainEnv {
+    double ht, warmup, W, kvb, mden;
+    int64_t loadx0, loady0, cx, cap, copy_add_x, copy_add_y, budget_left;
+    int32_t hk;
+    bool rb_ok;
+  };
+  // one chained step end of member c (o = its partner); false = stop chaining
+  KV_DEV bool chain_step(Chain& c, Chain& o, bool isA, ChainEnv& v) {
+    const int z = c.z;
+    if (c.B <= 0) return false;
+    if (!(c.e < v.ht || (c.e == v.ht && 3 * 64 + z < v.hk))) return false;
+    if (c.i + 1 >= c.minrem) return false;  // a member completes at this step end
+    if (c.e >= c.mr) return false;          // a join at this boundary
+    if (v.budget_left <= 0) return false;
+    if (v.rb_ok) {                           // rebalance at z's boundary after this step end
+      const int64_t cz = isA ? v.cx : -v.cx;
+      if (cz >= 1 && c.lim_kv != INT64_MAX) {
+        const int64_t lz = (isA ? v.loadx0 : v.loady0) + (c.i + 1) * c.B;
+        const int64_t lw = (isA ? v.loady0 : v.loadx0) + o.i * o.B;
+        const int64_t dz = lz - lw;
+        const int64_t lim = cz >= 2 ? dz : dz - 1;
+        if (c.lim_kv + c.i + 1 <= lim) return false;
+      }
+    }
+    // memory for z's next step start: B on z, m mirror lines on the partner
+    if (c.used + c.B > v.cap || o.used + c.m > v.cap) return false;
+    // ---- the virtual step end of z at c.e and its next step start
+    if constexpr (LOG) now = c.e;
+    if (c.js >= v.warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
+    if (c.e >= v.warmup) c.tw += c.B;
+    if (c.i >= 1) {
+      const double g = ksub(c.e, c.prev);
+      if (g > c.G) c.G = g;
+    }
+    if (c.m > 0) {
+      const double st = c.e > c.link ? c.e : c.link;
+      c.link = kadd(st, c.mlat);
+      c.mfin = c.link;
+      log(KVSIM_EV_TRANSFER, z, z ^ 1, 1, c.m);
+    }
+    log(KVSIM_EV_STEP_END, z, c.B, 0, 0);
+    c.K += c.B;
+    c.used += c.B;
+    o.used += c.m;
+    if (isA) v.copy_add_y += c.m; else v.copy_add_x += c.m;
+    log(KVSIM_EV_STEP_START, z, c.B, 0, c.K);
+    c.prev = c.e;
+    c.js = c.e;
+    c.e = kadd(c.e, kvsim_math::kmax(kdiv(kadd(v.W, kmul((double)c.K, v.kvb)), v.mden), c.comp));
+    c.i += 1;
+    v.budget_left -= 1;
+    return true;
+  }
   KV_DEV_NOINLINE void fast_forward_pair(int x) {
     const int y = x ^ 1;
     if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
@@ -971,66 +1027,28 @@ struct Sim {
     const bool rb_ok = get(L_role, y) == ROLE_DECODE;  // rebalances possible in this pair
     const int64_t cx = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
     Chain a, b;
-    chain_init(a, x);
-    if (ystep) chain_init(b, y);
+    chain_init(a, x, rb_ok && cx >= 1);
+    if (ystep) chain_init(b, y, rb_ok && -cx >= 1);
     else {
       b.z = y; b.B = 0; b.i = 0; b.e = kInf; b.m = 0; b.used = get(L_used, y); b.K = get(L_skv, y);
       b.lim_kv = INT64_MAX; b.minrem = 0; b.mr = kInf;
     }
-    const int64_t loadx0 = load_of(x), loady0 = load_of(y);
-    int64_t copy_add_x = 0, copy_add_y = 0;  // mirror reservations landing on x / y
+    ChainEnv env;
+    env.ht = ht; env.hk = hk; env.rb_ok = rb_ok;
+    env.loadx0 = load_of(x); env.loady0 = load_of(y);
+    env.cx = cx;
+    env.cap = PC.f.cap; env.warmup = PC.warmup;
+    env.W = PC.f.W; env.kvb = PC.f.kvb; env.mden = PC.f.mem_den;
+    env.copy_add_x = 0; env.copy_add_y = 0;
+    env.budget_left = PC.event_budget - n_events;
     const double now0 = now;
-    int64_t budget_left = PC.event_budget - n_events;
     for (;;) {
       // next chained event: the earlier step end, ties to the lower id
       const bool pickA = !(b.e < a.e || (b.e == a.e && y < x));
-      Chain& c = pickA ? a : b;
-      Chain& o = pickA ? b : a;
-      const int z = c.z;
-      if (c.B <= 0) break;
-      if (!(c.e < ht || (c.e == ht && 3 * 64 + z < hk))) break;
-      if (c.i + 1 >= c.minrem) break;      // a member completes at this step end
-      if (c.e >= c.mr) break;              // a join at this boundary
-      if (budget_left <= 0) break;
-      // rebalance at z's boundary after this step end
-      if (rb_ok) {
-        const int64_t cz = pickA ? cx : -cx;
-        if (cz >= 1 && c.lim_kv != INT64_MAX) {
-          const int64_t lz = (pickA ? loadx0 : loady0) + (c.i + 1) * c.B;
-          const int64_t lw = (pickA ? loady0 : loadx0) + o.i * o.B;
-          const int64_t dz = lz - lw;
-          const int64_t lim = cz >= 2 ? dz : dz - 1;
-          if (c.lim_kv + c.i + 1 <= lim) break;
-        }
-      }
-      // memory for z's next step start: B on z, m mirror lines on the partner
-      if (c.used + c.B > PC.f.cap || o.used + c.m > PC.f.cap) break;
-      // ---- commit the virtual step end of z at c.e and its next step start
-      now = c.e;
-      if (c.js >= PC.warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
-      if (c.e >= PC.warmup) c.tw += c.B;
-      if (c.i >= 1) {
-        const double g = ksub(c.e, c.prev);
-        if (g > c.G) c.G = g;
-      }
-      if (c.m > 0) {
-        const double st = c.e > c.link ? c.e : c.link;
-        c.link = kadd(st, c.mlat);
-        c.mfin = c.link;
-        log(KVSIM_EV_TRANSFER, z, z ^ 1, 1, c.m);
-      }
-      log(KVSIM_EV_STEP_END, z, c.B, 0, 0);
-      c.K += c.B;
-      c.used += c.B;
-      o.used += c.m;
-      if (pickA) copy_add_y += c.m; else copy_add_x += c.m;
-      log(KVSIM_EV_STEP_START, z, c.B, 0, c.K);
-      c.prev = c.e;
-      c.js = c.e;
-      c.e = kadd(c.e, kvsim_math::kmax(kdiv(kadd(PC.f.W, kmul((double)c.K, PC.f.kvb)), PC.f.mem_den), c.comp));
-      c.i += 1;
-      budget_left -= 1;
+      const bool ok = pickA ? chain_step(a, b, true, env) : chain_step(b, a, false, env);
+      if (!ok) break;
     }
+    const int64_t copy_add_x = env.copy_add_x, copy_add_y = env.copy_add_y;
     now = now0;
     chain_commit(a, copy_add_x);
     if (ystep) chain_commit(b, copy_add_y);
@@ -1965,9 +1983,9 @@ struct Sim {
 };
 
 // One point, simulated by the policy-specialised core.
-template <int P>
+template <int P, bool LOG>
 KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot, int64_t pt) {
-  Sim<P> sim(ap, w, slot);
+  Sim<P, LOG> sim(ap, w, slot);
   if (sim.init_point(pt)) sim.run();
   sim.finalize();
 }
@@ -1988,9 +2006,15 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
     if ((int64_t)p >= a.n_pts) break;
     const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
     const int32_t pol = a.pts[pt].policy;
-    if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE>(ap, w, slot, pt);
-    else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM>(ap, w, slot, pt);
-    else run_point<KVSIM_POLICY_UNIFIED>(ap, w, slot, pt);
+    if (a.ev != nullptr) {
+      if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE, true>(ap, w, slot, pt);
+      else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, true>(ap, w, slot, pt);
+      else run_point<KVSIM_POLICY_UNIFIED, true>(ap, w, slot, pt);
+    } else {
+      if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE, false>(ap, w, slot, pt);
+      else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, false>(ap, w, slot, pt);
+      else run_point<KVSIM_POLICY_UNIFIED, false>(ap, w, slot, pt);
+    }
   }
 }
 

@@ -142,6 +142,8 @@ SweepFn sweep_variant(int minb) {
     case 1: return kvsim_sweep_kernel<1>;
     case 3: return kvsim_sweep_kernel<3>;
     case 4: return kvsim_sweep_kernel<4>;
+    case 6: return kvsim_sweep_kernel<6>;
+    case 8: return kvsim_sweep_kernel<8>;
     default: return kvsim_sweep_kernel<2>;
   }
 }
