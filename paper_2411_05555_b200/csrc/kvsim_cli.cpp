@@ -1,0 +1,811 @@
+// kvsim_cli.cpp — the C++ host entry point (`kvsim`), the drop-in for the
+// reference CLI specified in reference SPEC.md:400-455 (tools/ in
+// proj/CMakeLists.txt:19, absent in the reference). It parses the JSON
+// ExperimentConfig (unknown keys rejected, every default echoed,
+// SPEC.md:405-407,444), expands the point grid, and calls ONLY the C-ABI
+// (include/kvsim_gpu.h) to simulate; outputs are the SPEC files:
+//
+//   kvsim run             report.json, summary.csv, meta.json [, events.jsonl]
+//   kvsim sweep           summary.csv, sweep_long.csv, report.json, meta.json
+//   kvsim curves          curves.csv          (perfmodel throughput_curves)
+//   kvsim gen-trace       trace.csv           (#kvsim-trace v1, device RNG)
+//   kvsim validate-config resolved config on stdout
+//
+// Flags: --config PATH --seed N --out DIR --emit-events --gpus N; env
+// KVSIM_LOG=0..3. Errors exit nonzero with a machine-readable
+// {"error": ...} line on stderr.
+#include <algorithm>
+#include <atomic>
+#include <cerrno>
+#include <cstdarg>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <sys/stat.h>
+#include <thread>
+#include <vector>
+
+#include "json_lite.hpp"
+#include "kvsim/perfmodel.hpp"
+#include "kvsim_gpu.h"
+
+namespace {
+
+constexpr const char* kToolVersion = "kvsim-b200 1.0";
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+int g_log = 1;
+void logf(int lvl, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+void logf(int lvl, const char* fmt, ...) {
+  if (lvl > g_log) return;
+  va_list ap;
+  va_start(ap, fmt);
+  std::fprintf(stderr, "[kvsim] ");
+  std::vfprintf(stderr, fmt, ap);
+  std::fprintf(stderr, "\n");
+  va_end(ap);
+}
+
+std::string read_file(const std::string& p) {
+  std::ifstream f(p, std::ios::binary);
+  if (!f) throw ConfigError("cannot open " + p);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+void write_file(const std::string& p, const std::string& s) {
+  // atomic per file: write then rename
+  const std::string tmp = p + ".tmp";
+  std::ofstream f(tmp, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot write " + p);
+  f << s;
+  f.close();
+  if (std::rename(tmp.c_str(), p.c_str()) != 0) throw std::runtime_error("cannot rename " + tmp);
+}
+void mkdirs(const std::string& d) {
+  std::string cur;
+  for (size_t i = 0; i <= d.size(); ++i) {
+    if (i == d.size() || d[i] == '/') {
+      if (!cur.empty()) mkdir(cur.c_str(), 0755);
+    }
+    if (i < d.size()) cur += d[i];
+  }
+}
+std::string num(double d) {
+  if (std::isnan(d)) return "nan";
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", d);
+  return b;
+}
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) { h ^= c; h *= 1099511628211ull; }
+  return h;
+}
+
+// ------------------------------------------------------------------ config
+const char* const kKeys[] = {"model", "device", "num_devices", "memory_reserve_fraction", "instances", "policy",
+                             "policies", "num_prefill_instances", "prefill_token_budget", "workload",
+                             "arrival_process", "rate", "rates", "duration_s", "num_requests", "warmup_s", "seed",
+                             "seeds", "efficiency", "link_aggregation", "trace", "sweep_instances",
+                             "sweep_devices", "curves", "emit_records", "splitwise_cobatch", "degraded_mode",
+                             "inter_pair_leveling", "output"};
+
+struct Resolved {
+  jl::Value cfg;  // resolved config (defaults filled)
+};
+
+double req_num(const jl::Value& v, const char* what) {
+  if (!v.is_num()) throw ConfigError(std::string(what) + " must be a number");
+  return v.num;
+}
+int64_t req_int(const jl::Value& v, const char* what) {
+  double d = req_num(v, what);
+  if (d != std::floor(d)) throw ConfigError(std::string(what) + " must be an integer");
+  return (int64_t)d;
+}
+
+jl::Value model_obj(const jl::Value* v) {
+  jl::Value m = jl::Value::object();
+  std::string name = "llama2-70b";
+  if (v && v->is_str()) name = v->str;
+  if (v && v->is_obj()) {
+    const char* keys[] = {"name", "param_count", "num_layers", "hidden_dim", "num_kv_heads", "head_dim",
+                          "bytes_per_value"};
+    for (auto& kv : v->obj)
+      if (std::find_if(std::begin(keys), std::end(keys), [&](const char* k) { return kv.first == k; }) ==
+          std::end(keys))
+        throw ConfigError("unknown model key: " + kv.first);
+    for (int i = 1; i < 7; ++i)
+      if (!v->find(keys[i])) throw ConfigError(std::string("model.") + keys[i] + " required");
+    m.set("name", jl::Value::string(v->find("name") && v->find("name")->is_str() ? v->find("name")->str : "custom"));
+    for (int i = 1; i < 7; ++i) m.set(keys[i], jl::Value::number(req_num(*v->find(keys[i]), keys[i])));
+    return m;
+  }
+  double P, L, H, KV, HD, B;
+  if (name == "llama2-70b") { P = 70e9; L = 80; H = 8192; KV = 8; HD = 128; B = 2; }
+  else if (name == "llama2-7b") { P = 7e9; L = 32; H = 4096; KV = 32; HD = 128; B = 2; }
+  else throw ConfigError("unknown model preset: " + name);
+  m.set("name", jl::Value::string(name));
+  m.set("param_count", jl::Value::number(P));
+  m.set("num_layers", jl::Value::number(L));
+  m.set("hidden_dim", jl::Value::number(H));
+  m.set("num_kv_heads", jl::Value::number(KV));
+  m.set("head_dim", jl::Value::number(HD));
+  m.set("bytes_per_value", jl::Value::number(B));
+  return m;
+}
+jl::Value device_obj(const jl::Value& v) {
+  jl::Value d = jl::Value::object();
+  if (v.is_obj()) {
+    const char* keys[] = {"name", "peak_flops", "hbm_capacity", "hbm_bandwidth", "link_bandwidth"};
+    for (auto& kv : v.obj)
+      if (std::find_if(std::begin(keys), std::end(keys), [&](const char* k) { return kv.first == k; }) ==
+          std::end(keys))
+        throw ConfigError("unknown device key: " + kv.first);
+    d.set("name", jl::Value::string(v.find("name") && v.find("name")->is_str() ? v.find("name")->str : "custom"));
+    for (int i = 1; i < 5; ++i) {
+      if (!v.find(keys[i])) throw ConfigError(std::string("device.") + keys[i] + " required");
+      d.set(keys[i], jl::Value::number(req_num(*v.find(keys[i]), keys[i])));
+    }
+    return d;
+  }
+  if (!v.is_str()) throw ConfigError("device must be a preset name or an object");
+  kvsim::DeviceSpec s;
+  if (v.str == "h100" || v.str == "H100") s = kvsim::device_preset_h100();
+  else if (v.str == "910b2" || v.str == "910B2") s = kvsim::device_preset_910b2();
+  else throw ConfigError("unknown device preset: " + v.str);
+  d.set("name", jl::Value::string(s.name));
+  d.set("peak_flops", jl::Value::number(s.peak_flops));
+  d.set("hbm_capacity", jl::Value::number(s.hbm_capacity));
+  d.set("hbm_bandwidth", jl::Value::number(s.hbm_bandwidth));
+  d.set("link_bandwidth", jl::Value::number(s.link_bandwidth));
+  return d;
+}
+jl::Value workload_obj(const jl::Value* v) {
+  // SPEC.md:144 presets; conversation/coding/fixed are builder presets (SEMANTICS §2)
+  jl::Value w = jl::Value::object();
+  int64_t p0 = 20, p1 = 1000, d0 = 20, d1 = 1000;
+  std::string name = "mixed";
+  if (v && v->is_str()) {
+    name = v->str;
+    if (name == "light") { p0 = 20; p1 = 500; d0 = 20; d1 = 500; }
+    else if (name == "mixed") {}
+    else if (name == "heavy") { p0 = 500; p1 = 1000; d0 = 500; d1 = 1000; }
+    else if (name == "conversation") { p0 = 50; p1 = 1500; d0 = 50; d1 = 600; }
+    else if (name == "coding") { p0 = 1000; p1 = 8000; d0 = 10; d1 = 200; }
+    else throw ConfigError("unknown workload preset: " + name);
+  } else if (v && v->is_obj()) {
+    for (auto& kv : v->obj)
+      if (kv.first != "name" && kv.first != "prompt_range" && kv.first != "decode_range" &&
+          kv.first != "distribution")
+        throw ConfigError("unknown workload key: " + kv.first);
+    auto rng = [&](const char* k, int64_t& a, int64_t& b) {
+      const jl::Value* r = v->find(k);
+      if (!r || !r->is_arr() || r->arr.size() != 2) throw ConfigError(std::string("workload.") + k + " must be [min,max]");
+      a = req_int(r->arr[0], k);
+      b = req_int(r->arr[1], k);
+    };
+    rng("prompt_range", p0, p1);
+    rng("decode_range", d0, d1);
+    if (const jl::Value* ds = v->find("distribution"))
+      if (!ds->is_str() || ds->str != "uniform") throw ConfigError("workload.distribution: only \"uniform\"");
+    name = v->find("name") && v->find("name")->is_str() ? v->find("name")->str : "custom";
+  }
+  if (p0 < 1 || p1 < p0 || d0 < 1 || d1 < d0) throw ConfigError("workload ranges must satisfy 1 <= min <= max");
+  w.set("name", jl::Value::string(name));
+  jl::Value pr = jl::Value::array();
+  pr.push(jl::Value::number((double)p0));
+  pr.push(jl::Value::number((double)p1));
+  jl::Value dr = jl::Value::array();
+  dr.push(jl::Value::number((double)d0));
+  dr.push(jl::Value::number((double)d1));
+  w.set("prompt_range", pr);
+  w.set("decode_range", dr);
+  w.set("distribution", jl::Value::string("uniform"));
+  return w;
+}
+
+jl::Value num_list(const jl::Value* v, const char* what) {
+  jl::Value a = jl::Value::array();
+  if (!v) return a;
+  if (v->is_num()) { a.push(*v); return a; }
+  if (!v->is_arr()) throw ConfigError(std::string(what) + " must be a number or a list");
+  for (auto& e : v->arr) a.push(jl::Value::number(req_num(e, what)));
+  return a;
+}
+jl::Value str_list(const jl::Value* v, const char* what) {
+  jl::Value a = jl::Value::array();
+  if (!v) return a;
+  if (v->is_str()) { a.push(*v); return a; }
+  if (!v->is_arr()) throw ConfigError(std::string(what) + " must be a string or a list");
+  for (auto& e : v->arr) {
+    if (!e.is_str()) throw ConfigError(std::string(what) + " entries must be strings");
+    a.push(e);
+  }
+  return a;
+}
+
+std::string norm_policy(const std::string& p) {
+  if (p == "accellm") return "accellm";
+  if (p == "splitwise" || p == "splitwise_static") return "splitwise_static";
+  if (p == "unified" || p == "vllm") return "unified";
+  throw ConfigError("unknown policy: " + p);
+}
+
+jl::Value resolve(const jl::Value& in, const std::string& cmd) {
+  if (!in.is_obj()) throw ConfigError("config must be a JSON object");
+  for (auto& kv : in.obj)
+    if (std::find_if(std::begin(kKeys), std::end(kKeys), [&](const char* k) { return kv.first == k; }) ==
+        std::end(kKeys))
+      throw ConfigError("unknown config key: " + kv.first);
+  for (const char* k : {"splitwise_cobatch", "degraded_mode", "inter_pair_leveling"})
+    if (const jl::Value* v = in.find(k))
+      if (!(v->kind == jl::Value::Bool && !v->b))
+        throw ConfigError(std::string(k) + " is not modelled in this version (must be false)");
+  jl::Value c = jl::Value::object();
+  c.set("model", model_obj(in.find("model")));
+  c.set("device", device_obj(in.find("device") ? *in.find("device") : jl::Value::string("h100")));
+  c.set("num_devices", jl::Value::number(in.find("num_devices") ? (double)req_int(*in.find("num_devices"), "num_devices") : 4));
+  c.set("memory_reserve_fraction",
+        jl::Value::number(in.find("memory_reserve_fraction") ? req_num(*in.find("memory_reserve_fraction"), "memory_reserve_fraction") : 0.10));
+  c.set("instances", jl::Value::number(in.find("instances") ? (double)req_int(*in.find("instances"), "instances") : 8));
+  jl::Value pols = str_list(in.find("policies"), "policies");
+  if (in.find("policy")) {
+    jl::Value one = str_list(in.find("policy"), "policy");
+    for (auto& e : one.arr) pols.push(e);
+  }
+  if (pols.arr.empty()) pols.push(jl::Value::string("accellm"));
+  for (auto& e : pols.arr) e.str = norm_policy(e.str);
+  c.set("policies", pols);
+  c.set("num_prefill_instances",
+        jl::Value::number(in.find("num_prefill_instances") ? (double)req_int(*in.find("num_prefill_instances"), "num_prefill_instances") : 0));
+  c.set("prefill_token_budget",
+        jl::Value::number(in.find("prefill_token_budget") ? (double)req_int(*in.find("prefill_token_budget"), "prefill_token_budget") : 8192));
+  c.set("workload", workload_obj(in.find("workload")));
+  std::string proc = in.find("arrival_process") && in.find("arrival_process")->is_str() ? in.find("arrival_process")->str : "poisson";
+  if (proc != "poisson" && proc != "fixed-interval" && proc != "fixed") throw ConfigError("arrival_process: poisson | fixed-interval");
+  c.set("arrival_process", jl::Value::string(proc == "poisson" ? "poisson" : "fixed-interval"));
+  jl::Value rates = num_list(in.find("rates"), "rates");
+  for (auto& e : num_list(in.find("rate"), "rate").arr) rates.push(e);
+  if (rates.arr.empty()) {
+    if (cmd == "sweep") throw ConfigError("empty rate list");
+    if (!in.find("trace")) rates.push(jl::Value::number(4.0));
+  }
+  for (auto& e : rates.arr)
+    if (!(e.num >= 0)) throw ConfigError("rates must be >= 0");
+  c.set("rates", rates);
+  const bool has_n = in.find("num_requests") != nullptr, has_d = in.find("duration_s") != nullptr;
+  double dur = has_d ? req_num(*in.find("duration_s"), "duration_s") : (has_n ? INFINITY : 300.0);
+  if (!(dur > 0)) throw ConfigError("duration_s must be > 0");
+  c.set("duration_s", std::isinf(dur) ? jl::Value::string("inf") : jl::Value::number(dur));
+  c.set("num_requests", jl::Value::number(has_n ? (double)req_int(*in.find("num_requests"), "num_requests") : 0));
+  c.set("warmup_s", jl::Value::number(in.find("warmup_s") ? req_num(*in.find("warmup_s"), "warmup_s") : (has_n && !has_d ? 0.0 : 30.0)));
+  jl::Value seeds = num_list(in.find("seeds"), "seeds");
+  for (auto& e : num_list(in.find("seed"), "seed").arr) seeds.push(e);
+  if (seeds.arr.empty()) seeds.push(jl::Value::number(0));
+  c.set("seeds", seeds);
+  jl::Value eff = jl::Value::object();
+  double ce = 0.5, me = 0.8, le = 0.8;
+  if (const jl::Value* e = in.find("efficiency")) {
+    if (!e->is_obj()) throw ConfigError("efficiency must be an object");
+    for (auto& kv : e->obj) {
+      if (kv.first == "compute_eff") ce = req_num(kv.second, "compute_eff");
+      else if (kv.first == "mem_bw_eff") me = req_num(kv.second, "mem_bw_eff");
+      else if (kv.first == "link_eff") le = req_num(kv.second, "link_eff");
+      else throw ConfigError("unknown efficiency key: " + kv.first);
+    }
+  }
+  eff.set("compute_eff", jl::Value::number(ce));
+  eff.set("mem_bw_eff", jl::Value::number(me));
+  eff.set("link_eff", jl::Value::number(le));
+  c.set("efficiency", eff);
+  std::string la = in.find("link_aggregation") && in.find("link_aggregation")->is_str() ? in.find("link_aggregation")->str : "striped";
+  if (la != "striped" && la != "single-link" && la != "single") throw ConfigError("link_aggregation: striped | single-link");
+  c.set("link_aggregation", jl::Value::string(la == "striped" ? "striped" : "single-link"));
+  if (const jl::Value* t = in.find("trace")) {
+    if (!t->is_str()) throw ConfigError("trace must be a path");
+    c.set("trace", *t);
+  }
+  jl::Value si = num_list(in.find("sweep_instances"), "sweep_instances");
+  if (si.arr.empty()) si.push(c.find("instances")->num == c.find("instances")->num ? *c.find("instances") : jl::Value());
+  c.set("sweep_instances", si);
+  jl::Value sd = jl::Value::array();
+  if (const jl::Value* v = in.find("sweep_devices")) {
+    if (!v->is_arr()) throw ConfigError("sweep_devices must be a list");
+    for (auto& e : v->arr) sd.push(device_obj(e));
+  } else {
+    sd.push(*c.find("device"));
+  }
+  c.set("sweep_devices", sd);
+  if (const jl::Value* cv = in.find("curves")) c.set("curves", *cv);
+  c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
+                                               ? in.find("emit_records")->b
+                                               : cmd == "run"));
+  return c;
+}
+
+// ------------------------------------------------------------------ traces
+struct Trace {
+  std::vector<double> arr;
+  std::vector<int32_t> pl, dl;
+};
+Trace load_trace(const std::string& path) {
+  // header `#kvsim-trace v1`, rows id,arrival_s,prompt_len,decode_len
+  std::ifstream f(path);
+  if (!f) throw ConfigError("cannot open trace " + path);
+  std::string line;
+  size_t ln = 0;
+  Trace t;
+  if (!std::getline(f, line) || line.rfind("#kvsim-trace v1", 0) != 0)
+    throw ConfigError(path + ":1: missing '#kvsim-trace v1' header");
+  ln = 1;
+  double prev = -INFINITY;
+  while (std::getline(f, line)) {
+    ++ln;
+    if (!line.empty() && line.back() == '\r') line.pop_back();
+    if (line.empty() || line[0] == '#') continue;
+    if (line.rfind("id,", 0) == 0) continue;  // optional column header
+    long long id;
+    double a;
+    long long p, d;
+    char tail;
+    if (std::sscanf(line.c_str(), "%lld,%lf,%lld,%lld%c", &id, &a, &p, &d, &tail) != 4)
+      throw ConfigError(path + ":" + std::to_string(ln) + ": parse error");
+    if ((size_t)id != t.arr.size()) throw ConfigError(path + ":" + std::to_string(ln) + ": ids must be 0..n-1 in order");
+    if (a < prev) throw ConfigError(path + ":" + std::to_string(ln) + ": arrival_s decreases");
+    if (p < 1 || d < 1 || p > (1 << 30) || d > (1 << 28))
+      throw ConfigError(path + ":" + std::to_string(ln) + ": lengths out of range");
+    prev = a;
+    t.arr.push_back(a);
+    t.pl.push_back((int32_t)p);
+    t.dl.push_back((int32_t)d);
+  }
+  return t;
+}
+std::string trace_csv(const Trace& t) {
+  std::string o = "#kvsim-trace v1\nid,arrival_s,prompt_len,decode_len\n";
+  for (size_t i = 0; i < t.arr.size(); ++i)
+    o += std::to_string(i) + "," + num(t.arr[i]) + "," + std::to_string(t.pl[i]) + "," + std::to_string(t.dl[i]) + "\n";
+  return o;
+}
+
+// ------------------------------------------------------------------ points
+struct PointMeta {
+  std::string policy, device;
+  double rate;
+  int instances;
+  uint64_t seed;
+};
+
+kvsim_point_desc base_point(const jl::Value& c, const jl::Value& dev) {
+  kvsim_point_desc p;
+  kvsim_point_defaults(&p);
+  const jl::Value& m = *c.find("model");
+  p.param_count = m.find("param_count")->num;
+  p.num_layers = (int32_t)m.find("num_layers")->num;
+  p.hidden_dim = (int32_t)m.find("hidden_dim")->num;
+  p.num_kv_heads = (int32_t)m.find("num_kv_heads")->num;
+  p.head_dim = (int32_t)m.find("head_dim")->num;
+  p.bytes_per_value = (int32_t)m.find("bytes_per_value")->num;
+  p.peak_flops = dev.find("peak_flops")->num;
+  p.hbm_capacity = dev.find("hbm_capacity")->num;
+  p.hbm_bandwidth = dev.find("hbm_bandwidth")->num;
+  p.link_bandwidth = dev.find("link_bandwidth")->num;
+  p.num_devices = (int32_t)c.find("num_devices")->num;
+  p.tensor_parallel = p.num_devices;
+  p.memory_reserve_fraction = c.find("memory_reserve_fraction")->num;
+  const jl::Value& e = *c.find("efficiency");
+  p.compute_eff = e.find("compute_eff")->num;
+  p.mem_bw_eff = e.find("mem_bw_eff")->num;
+  p.link_eff = e.find("link_eff")->num;
+  p.link_mode = c.find("link_aggregation")->str == "striped" ? KVSIM_LINK_STRIPED : KVSIM_LINK_SINGLE;
+  p.num_prefill_instances = (int32_t)c.find("num_prefill_instances")->num;
+  p.prefill_token_budget = (int32_t)c.find("prefill_token_budget")->num;
+  const jl::Value& w = *c.find("workload");
+  p.prompt_min = (int32_t)w.find("prompt_range")->arr[0].num;
+  p.prompt_max = (int32_t)w.find("prompt_range")->arr[1].num;
+  p.decode_min = (int32_t)w.find("decode_range")->arr[0].num;
+  p.decode_max = (int32_t)w.find("decode_range")->arr[1].num;
+  p.arrival_process = c.find("arrival_process")->str == "poisson" ? KVSIM_ARRIVAL_POISSON : KVSIM_ARRIVAL_FIXED;
+  const jl::Value& d = *c.find("duration_s");
+  p.duration_s = d.is_str() ? INFINITY : d.num;
+  p.warmup_s = c.find("warmup_s")->num;
+  return p;
+}
+
+int policy_code(const std::string& s) {
+  return s == "accellm" ? KVSIM_POLICY_ACCELLM : s == "splitwise_static" ? KVSIM_POLICY_SPLITWISE : KVSIM_POLICY_UNIFIED;
+}
+
+int64_t derive_requests(double rate, double duration) {
+  // cap for duration-bound generation: lambda*D + 20 sqrt(lambda*D) + 1000
+  const double m = rate * duration;
+  return (int64_t)std::ceil(m + 20.0 * std::sqrt(m) + 1000.0);
+}
+
+void expand(const jl::Value& c, const Trace* trace, std::vector<kvsim_point_desc>& pts, std::vector<PointMeta>& meta) {
+  const int64_t nreq = (int64_t)c.find("num_requests")->num;
+  const jl::Value& d = *c.find("duration_s");
+  const double dur = d.is_str() ? INFINITY : d.num;
+  std::vector<double> rates;
+  for (auto& r : c.find("rates")->arr) rates.push_back(r.num);
+  if (trace) rates = {0.0};
+  for (auto& dev : c.find("sweep_devices")->arr)
+    for (auto& ni : c.find("sweep_instances")->arr)
+      for (auto& pol : c.find("policies")->arr)
+        for (double rate : rates)
+          for (auto& sd : c.find("seeds")->arr) {
+            kvsim_point_desc p = base_point(c, dev);
+            p.policy = policy_code(pol.str);
+            p.num_instances = (int32_t)ni.num;
+            p.rate = rate;
+            p.seed = (uint64_t)sd.num;
+            if (trace) {
+              p.trace_index = 0;
+              p.num_requests = (int64_t)trace->arr.size();
+            } else {
+              p.num_requests = nreq > 0 ? nreq : derive_requests(rate, std::isinf(dur) ? 300.0 : dur);
+            }
+            p.user_tag = pts.size();
+            pts.push_back(p);
+            meta.push_back(PointMeta{pol.str, dev.find("name")->str, rate, p.num_instances, p.seed});
+          }
+}
+
+// ------------------------------------------------------------------ running
+struct RunOut {
+  std::vector<kvsim_point_summary> sum;
+  std::vector<kvsim_request_record> recs;
+  std::vector<int64_t> rec_off;
+  std::vector<kvsim_event_record> ev;
+  std::vector<int64_t> ev_cnt;
+  size_t ev_cap = 0;
+};
+
+// One host thread per GPU pulling chunks of points from a shared counter;
+// results land at their point index, so the merge is deterministic and
+// independent of the GPU count.
+void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, int gpus, bool records, size_t ev_cap,
+                RunOut& out) {
+  const size_t n = pts.size();
+  out.sum.assign(n, kvsim_point_summary{});
+  out.rec_off.assign(n + 1, 0);
+  for (size_t i = 0; i < n; ++i) out.rec_off[i + 1] = out.rec_off[i] + pts[i].num_requests;
+  if (records) out.recs.assign((size_t)out.rec_off[n], kvsim_request_record{});
+  out.ev_cap = ev_cap;
+  if (ev_cap) {
+    out.ev.assign(n * ev_cap, kvsim_event_record{});
+    out.ev_cnt.assign(n, 0);
+  }
+  kvsim_trace_view tv{};
+  if (trace) tv = kvsim_trace_view{trace->arr.data(), trace->pl.data(), trace->dl.data(), (int64_t)trace->arr.size()};
+  const int ndev = kvsim_gpu_device_count();
+  if (ndev <= 0) throw std::runtime_error("no CUDA device available (kvsim has no CPU fallback)");
+  if (gpus <= 0 || gpus > ndev) gpus = ndev < 1 ? 1 : (gpus <= 0 ? 1 : ndev);
+  const size_t chunk = std::max<size_t>(1, std::min<size_t>(65536, (n + 4 * gpus - 1) / (4 * gpus)));
+  std::atomic<size_t> next{0};
+  std::vector<std::string> errors(gpus);
+  std::vector<std::thread> th;
+  for (int g = 0; g < gpus; ++g)
+    th.emplace_back([&, g]() {
+      char err[512] = {0};
+      kvsim_gpu_ctx* ctx = nullptr;
+      if (kvsim_gpu_open(g, &ctx, err, sizeof err) != 0) { errors[g] = err; return; }
+      for (;;) {
+        const size_t a = next.fetch_add(chunk);
+        if (a >= n) break;
+        const size_t b = std::min(n, a + chunk);
+        // records of a chunk are contiguous: rec_off[a..b)
+        int rc = kvsim_gpu_run(ctx, pts.data() + a, b - a, trace ? &tv : nullptr, trace ? 1 : 0, out.sum.data() + a,
+                               records ? out.recs.data() + out.rec_off[a] : nullptr,
+                               ev_cap ? out.ev.data() + a * ev_cap : nullptr, ev_cap,
+                               ev_cap ? out.ev_cnt.data() + a : nullptr, err, sizeof err);
+        if (rc != 0) { errors[g] = err; break; }
+      }
+      kvsim_gpu_close(ctx);
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errors)
+    if (!e.empty()) throw std::runtime_error(e);
+}
+
+// ------------------------------------------------------------------ outputs
+const char* kSummaryCols = "policy,rate,ttft_mean,ttft_p95,tbt_mean,tbt_max,jct_mean,jct_p95,cost_eff,idle_frac,peak_kv_gb,link_prefill_gb,link_mirror_gb";
+
+std::string summary_row(const PointMeta& m, const kvsim_point_summary& s) {
+  return m.policy + "," + num(m.rate) + "," + num(s.ttft_mean) + "," + num(s.ttft_p95) + "," + num(s.tbt_mean) + "," +
+         num(s.tbt_max) + "," + num(s.jct_mean) + "," + num(s.jct_p95) + "," + num(s.cost_eff) + "," +
+         num(s.idle_frac) + "," + num(s.peak_kv_gb) + "," + num(s.link_prefill_gb) + "," + num(s.link_mirror_gb);
+}
+
+jl::Value summary_json(const kvsim_point_summary& s) {
+  jl::Value o = jl::Value::object();
+  auto I = [&](const char* k, int64_t v) { o.set(k, jl::Value::number((double)v)); };
+  auto D = [&](const char* k, double v) { o.set(k, std::isnan(v) ? jl::Value() : jl::Value::number(v)); };
+  I("status", s.status);
+  I("num_instances", s.num_instances);
+  I("n_requests", s.n_requests); I("n_completed", s.n_completed); I("n_measured", s.n_measured);
+  I("tokens_total", s.tokens_total); I("tokens_window", s.tokens_window);
+  I("n_events", s.n_events); I("n_steps", s.n_steps); I("n_prefills", s.n_prefills);
+  I("n_moves", s.n_moves); I("n_preemptions", s.n_preemptions); I("n_evictions", s.n_evictions);
+  I("peak_kv_tokens", s.peak_kv_tokens); I("link_prefill_tokens", s.link_prefill_tokens);
+  I("link_mirror_tokens", s.link_mirror_tokens);
+  D("makespan_s", s.makespan_s);
+  D("ttft_mean", s.ttft_mean); D("ttft_p50", s.ttft_p50); D("ttft_p95", s.ttft_p95); D("ttft_max", s.ttft_max);
+  D("tbt_mean", s.tbt_mean); D("tbt_max", s.tbt_max);
+  D("jct_mean", s.jct_mean); D("jct_p50", s.jct_p50); D("jct_p95", s.jct_p95); D("jct_max", s.jct_max);
+  D("cost_eff", s.cost_eff); D("idle_frac", s.idle_frac); D("peak_kv_gb", s.peak_kv_gb);
+  D("link_prefill_gb", s.link_prefill_gb); D("link_mirror_gb", s.link_mirror_gb);
+  D("busy_s_total", s.busy_s_total);
+  return o;
+}
+
+const char* ev_name(int k) {
+  static const char* names[] = {"?", "arrive", "prefill_start", "prefill_done", "step_start", "step_end", "move",
+                                "evict", "preempt", "role", "transfer", "wake", "join", "copy"};
+  return (k >= 0 && k <= 13) ? names[k] : "?";
+}
+
+jl::Value meta_json(const jl::Value& cfg, const std::string& cmd) {
+  jl::Value m = jl::Value::object();
+  const std::string canon = jl::dump(cfg, 0);
+  char h[32];
+  std::snprintf(h, sizeof h, "%016llx", (unsigned long long)fnv1a(canon));
+  m.set("tool_version", jl::Value::string(kToolVersion));
+  m.set("command", jl::Value::string(cmd));
+  m.set("config_hash", jl::Value::string(h));
+  m.set("seeds", *cfg.find("seeds"));
+  m.set("config", cfg);
+  return m;
+}
+
+struct Args {
+  std::string cmd, config, out = "out";
+  bool emit_events = false, has_seed = false;
+  uint64_t seed = 0;
+  int gpus = 1;
+};
+
+[[noreturn]] void usage() {
+  std::fprintf(stderr,
+               "usage: kvsim run|sweep|curves|gen-trace|validate-config --config PATH [--seed N] [--out DIR] "
+               "[--emit-events] [--gpus N]\n");
+  std::exit(2);
+}
+
+Args parse_args(int argc, char** argv) {
+  if (argc < 2) usage();
+  Args a;
+  a.cmd = argv[1];
+  for (int i = 2; i < argc; ++i) {
+    std::string s = argv[i];
+    auto val = [&]() -> std::string {
+      if (i + 1 >= argc) usage();
+      return argv[++i];
+    };
+    if (s == "--config") a.config = val();
+    else if (s == "--out") a.out = val();
+    else if (s == "--seed") { a.seed = std::strtoull(val().c_str(), nullptr, 10); a.has_seed = true; }
+    else if (s == "--emit-events") a.emit_events = true;
+    else if (s == "--gpus") a.gpus = std::atoi(val().c_str());
+    else usage();
+  }
+  if (a.config.empty()) usage();
+  return a;
+}
+
+int cmd_main(const Args& a) {
+  jl::Value raw = jl::parse(read_file(a.config));
+  if (a.has_seed && raw.is_obj()) {
+    jl::Value s = jl::Value::array();
+    s.push(jl::Value::number((double)a.seed));
+    raw.set("seeds", s);
+    for (size_t i = 0; i < raw.obj.size(); ++i)
+      if (raw.obj[i].first == "seed") { raw.obj.erase(raw.obj.begin() + i); break; }
+  }
+  const std::string cmdk = a.cmd == "validate-config" ? "run" : a.cmd;
+  jl::Value cfg = resolve(raw, cmdk);
+  // host-side validation of every point (SPEC.md:416 messages)
+  Trace trace;
+  const bool has_trace = cfg.find("trace") != nullptr;
+  if (has_trace) trace = load_trace(cfg.find("trace")->str);
+  std::vector<kvsim_point_desc> pts;
+  std::vector<PointMeta> meta;
+  expand(cfg, has_trace ? &trace : nullptr, pts, meta);
+  if (a.cmd == "run" || a.cmd == "validate-config") {
+    char err[256];
+    for (auto& p : pts) {
+      if (kvsim_point_validate(&p, err, sizeof err) != 0) throw ConfigError(err);
+    }
+  }
+  if (a.cmd == "validate-config") {
+    std::printf("%s\n", jl::dump(cfg).c_str());
+    return 0;
+  }
+  mkdirs(a.out);
+  if (a.cmd == "curves") {
+    // perfmodel throughput_curves (host API)
+    const jl::Value* cv = cfg.find("curves");
+    std::vector<int64_t> lens = {100, 500, 1000}, batches;
+    for (int b = 1; b <= 256; b *= 2) batches.push_back(b);
+    std::string phase = "decode";
+    if (cv && cv->is_obj()) {
+      if (cv->find("lengths")) { lens.clear(); for (auto& e : cv->find("lengths")->arr) lens.push_back((int64_t)e.num); }
+      if (cv->find("batch_sizes")) { batches.clear(); for (auto& e : cv->find("batch_sizes")->arr) batches.push_back((int64_t)e.num); }
+      if (cv->find("phase") && cv->find("phase")->is_str()) phase = cv->find("phase")->str;
+    }
+    if (lens.empty() || batches.empty()) throw ConfigError("curves: empty lengths or batch_sizes");
+    const kvsim_point_desc& p = pts.at(0);
+    kvsim::ModelSpec ms{"m", p.param_count, p.num_layers, p.hidden_dim, p.num_kv_heads, p.head_dim, p.bytes_per_value};
+    kvsim::InstanceSpec is{{"d", p.peak_flops, p.hbm_capacity, p.hbm_bandwidth, p.link_bandwidth}, p.num_devices,
+                           p.num_devices, p.memory_reserve_fraction};
+    kvsim::EfficiencyFactors ef{p.compute_eff, p.mem_bw_eff, p.link_eff};
+    std::string o = "phase,length,batch,latency_s,tokens_per_s\n";
+    for (const char* ph : {"prefill", "decode"}) {
+      if (phase != "both" && phase != ph) continue;
+      auto rows = kvsim::throughput_curves(ms, is, ef, lens, batches,
+                                           std::string(ph) == "prefill" ? kvsim::Phase::kPrefill : kvsim::Phase::kDecode);
+      for (auto& r : rows)
+        o += std::string(ph) + "," + std::to_string(r.length) + "," + std::to_string(r.batch) + "," + num(r.latency_s) +
+             "," + num(r.tokens_per_s) + "\n";
+    }
+    write_file(a.out + "/curves.csv", o);
+    write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
+    return 0;
+  }
+  if (a.cmd == "gen-trace") {
+    kvsim_gpu_ctx* ctx = nullptr;
+    char err[512];
+    if (kvsim_gpu_open(0, &ctx, err, sizeof err) != 0) throw std::runtime_error(err);
+    const kvsim_point_desc& p = pts.at(0);
+    Trace t;
+    t.arr.resize(p.num_requests);
+    t.pl.resize(p.num_requests);
+    t.dl.resize(p.num_requests);
+    int64_t nn = 0;
+    if (kvsim_gpu_gen_trace(ctx, &p, t.arr.data(), t.pl.data(), t.dl.data(), &nn, err, sizeof err) != 0)
+      throw std::runtime_error(err);
+    kvsim_gpu_close(ctx);
+    t.arr.resize(nn);
+    t.pl.resize(nn);
+    t.dl.resize(nn);
+    write_file(a.out + "/trace.csv", trace_csv(t));
+    return 0;
+  }
+  if (a.cmd != "run" && a.cmd != "sweep") usage();
+  const bool records = cfg.find("emit_records")->b;
+  const size_t ev_cap = a.emit_events ? (size_t)1 << 20 : 0;
+  RunOut r;
+  logf(1, "%s: %zu point(s) on %d GPU(s)", a.cmd.c_str(), pts.size(), a.gpus);
+  run_points(pts, has_trace ? &trace : nullptr, a.gpus, records, ev_cap, r);
+  // summary.csv (stable 13 columns) + sweep axes
+  std::string csv = std::string(kSummaryCols) + ",instances,device,seed,status\n";
+  for (size_t i = 0; i < pts.size(); ++i)
+    csv += summary_row(meta[i], r.sum[i]) + "," + std::to_string(meta[i].instances) + "," + meta[i].device + "," +
+           std::to_string(meta[i].seed) + "," + std::to_string(r.sum[i].status) + "\n";
+  write_file(a.out + "/summary.csv", csv);
+  jl::Value report = jl::Value::object();
+  report.set("tool_version", jl::Value::string(kToolVersion));
+  jl::Value points = jl::Value::array();
+  for (size_t i = 0; i < pts.size(); ++i) {
+    jl::Value e = jl::Value::object();
+    e.set("policy", jl::Value::string(meta[i].policy));
+    e.set("rate", jl::Value::number(meta[i].rate));
+    e.set("instances", jl::Value::number(meta[i].instances));
+    e.set("device", jl::Value::string(meta[i].device));
+    e.set("seed", jl::Value::number((double)meta[i].seed));
+    e.set("summary", summary_json(r.sum[i]));
+    if (records && a.cmd == "run") {
+      jl::Value rq = jl::Value::array();
+      for (int64_t k = 0; k < r.sum[i].n_requests; ++k) {
+        const kvsim_request_record& q = r.recs[r.rec_off[i] + k];
+        jl::Value x = jl::Value::object();
+        x.set("id", jl::Value::number((double)k));
+        x.set("arrival_s", jl::Value::number(q.arrival_s));
+        x.set("ttft_s", jl::Value::number(q.first_token_s - q.arrival_s));
+        x.set("jct_s", jl::Value::number(q.completion_s - q.arrival_s));
+        x.set("tbt_max_s", jl::Value::number(q.tbt_max_s));
+        x.set("tbt_mean_s", q.decode_len > 1 ? jl::Value::number((q.completion_s - q.first_token_s) / (q.decode_len - 1)) : jl::Value());
+        x.set("prompt_len", jl::Value::number(q.prompt_len));
+        x.set("decode_len", jl::Value::number(q.decode_len));
+        rq.push(x);
+      }
+      e.set("requests", rq);
+    }
+    points.push(e);
+  }
+  report.set("points", points);
+  if (a.cmd == "sweep") {
+    // saturation annotation: argmax cost_eff over rate per (policy, instances, device, seed)
+    jl::Value sat = jl::Value::array();
+    std::vector<bool> done(pts.size(), false);
+    for (size_t i = 0; i < pts.size(); ++i) {
+      if (done[i]) continue;
+      double best = -1, best_rate = 0;
+      for (size_t j = i; j < pts.size(); ++j) {
+        if (meta[j].policy != meta[i].policy || meta[j].instances != meta[i].instances ||
+            meta[j].device != meta[i].device || meta[j].seed != meta[i].seed)
+          continue;
+        done[j] = true;
+        if (r.sum[j].cost_eff > best) { best = r.sum[j].cost_eff; best_rate = meta[j].rate; }
+      }
+      jl::Value s = jl::Value::object();
+      s.set("policy", jl::Value::string(meta[i].policy));
+      s.set("instances", jl::Value::number(meta[i].instances));
+      s.set("device", jl::Value::string(meta[i].device));
+      s.set("seed", jl::Value::number((double)meta[i].seed));
+      s.set("saturation_rate", jl::Value::number(best_rate));
+      s.set("max_cost_eff", jl::Value::number(best));
+      sat.push(s);
+    }
+    report.set("saturation", sat);
+    // long form (policy, rate, metric, value)
+    std::string lf = "policy,rate,instances,device,seed,metric,value\n";
+    const char* cols[] = {"ttft_mean", "ttft_p95", "tbt_mean", "tbt_max", "jct_mean", "jct_p95", "cost_eff",
+                          "idle_frac", "peak_kv_gb", "link_prefill_gb", "link_mirror_gb"};
+    for (size_t i = 0; i < pts.size(); ++i) {
+      const kvsim_point_summary& s = r.sum[i];
+      const double vals[] = {s.ttft_mean, s.ttft_p95, s.tbt_mean, s.tbt_max, s.jct_mean, s.jct_p95,
+                             s.cost_eff, s.idle_frac, s.peak_kv_gb, s.link_prefill_gb, s.link_mirror_gb};
+      for (int k = 0; k < 11; ++k)
+        lf += meta[i].policy + "," + num(meta[i].rate) + "," + std::to_string(meta[i].instances) + "," +
+              meta[i].device + "," + std::to_string(meta[i].seed) + "," + cols[k] + "," + num(vals[k]) + "\n";
+    }
+    write_file(a.out + "/sweep_long.csv", lf);
+  }
+  write_file(a.out + "/report.json", jl::dump(report) + "\n");
+  write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
+  if (ev_cap) {
+    std::string ej;
+    for (size_t i = 0; i < pts.size(); ++i) {
+      const int64_t k = std::min<int64_t>(r.ev_cnt[i], (int64_t)ev_cap);
+      for (int64_t j = 0; j < k; ++j) {
+        const kvsim_event_record& e = r.ev[i * ev_cap + j];
+        ej += "{\"point\":" + std::to_string(i) + ",\"t\":" + num(e.t) + ",\"kind\":\"" + ev_name(e.kind) +
+              "\",\"inst\":" + std::to_string(e.inst) + ",\"a\":" + std::to_string(e.a) + ",\"b\":" +
+              std::to_string(e.b) + ",\"c\":" + std::to_string(e.c) + "}\n";
+      }
+      if (r.ev_cnt[i] > (int64_t)ev_cap) logf(1, "point %zu: event log truncated at %zu", i, ev_cap);
+    }
+    write_file(a.out + "/events.jsonl", ej);
+  }
+  int bad = 0;
+  for (auto& s : r.sum) bad += s.status != 0;
+  if (bad) logf(1, "%d point(s) reported errors (see status column)", bad);
+  return 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (const char* l = std::getenv("KVSIM_LOG")) g_log = std::atoi(l);
+  Args a = parse_args(argc, argv);
+  try {
+    return cmd_main(a);
+  } catch (const ConfigError& e) {
+    std::string o;
+    jl::escape(o, e.what());
+    std::fprintf(stderr, "{\"error\": %s, \"kind\": \"config\"}\n", o.c_str());
+    return 2;
+  } catch (const jl::ParseError& e) {
+    std::string o;
+    jl::escape(o, e.what());
+    std::fprintf(stderr, "{\"error\": %s, \"kind\": \"config\"}\n", o.c_str());
+    return 2;
+  } catch (const std::exception& e) {
+    std::string o;
+    jl::escape(o, e.what());
+    std::fprintf(stderr, "{\"error\": %s, \"kind\": \"runtime\"}\n", o.c_str());
+    return 3;
+  }
+}

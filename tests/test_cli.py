@@ -1,0 +1,163 @@
+"""The C++ host entry point `kvsim` (reference SPEC.md:400-455): config
+validation on CPU; run / sweep / gen-trace / curves end to end on the GPU,
+checked against the CPU oracle."""
+import csv
+import json
+import math
+import os
+import subprocess
+
+import pytest
+
+from harness import run_oracle
+from paper_2411_05555_b200 import build
+from paper_2411_05555_b200.abi import make_point
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def kvsim():
+    return build.build_cli()
+
+
+def run(kvsim, *args, cwd=None):
+    return subprocess.run([kvsim, *args], capture_output=True, text=True, cwd=cwd)
+
+
+def write(tmp_path, name, obj):
+    p = tmp_path / name
+    p.write_text(json.dumps(obj) if not isinstance(obj, str) else obj)
+    return str(p)
+
+
+def test_validate_echoes_defaults(kvsim, tmp_path):
+    r = run(kvsim, "validate-config", "--config", write(tmp_path, "c.json", {"instances": 4}))
+    assert r.returncode == 0, r.stderr
+    c = json.loads(r.stdout)
+    assert c["policies"] == ["accellm"] and c["prefill_token_budget"] == 8192
+    assert c["duration_s"] == 300 and c["warmup_s"] == 30          # SPEC.md:189 defaults
+    assert c["efficiency"] == {"compute_eff": 0.5, "mem_bw_eff": 0.8, "link_eff": 0.8}
+    assert c["model"]["num_layers"] == 80 and c["device"]["hbm_capacity"] == 80e9
+    r = run(kvsim, "validate-config", "--config", write(tmp_path, "d.json", {"num_requests": 10}))
+    c = json.loads(r.stdout)
+    assert c["duration_s"] == "inf" and c["warmup_s"] == 0
+
+
+@pytest.mark.parametrize("cfg,msg", [
+    ({"instancez": 4}, "unknown config key: instancez"),
+    ({"instances": 5, "policy": "accellm"}, "even instance count required"),
+    ({"device": {"name": "tiny", "peak_flops": 1e12, "hbm_capacity": 1e9, "hbm_bandwidth": 1e12,
+                 "link_bandwidth": 1e9}}, "model does not fit in instance memory"),
+    ({"workload": {"prompt_range": [10, 5], "decode_range": [1, 2]}}, "1 <= min <= max"),
+    ({"policy": "fcfs"}, "unknown policy"),
+    ({"degraded_mode": True}, "not modelled"),
+])
+def test_config_errors(kvsim, tmp_path, cfg, msg):
+    r = run(kvsim, "validate-config", "--config", write(tmp_path, "c.json", cfg))
+    assert r.returncode == 2
+    err = json.loads(r.stderr.strip().splitlines()[-1])
+    assert msg in err["error"] and err["kind"] == "config"
+
+
+def test_sweep_empty_rates_rejected(kvsim, tmp_path):
+    r = run(kvsim, "sweep", "--config", write(tmp_path, "c.json", {"rates": [], "num_requests": 5}),
+            "--out", str(tmp_path / "o"))
+    assert r.returncode == 2 and "empty rate list" in r.stderr
+
+
+def test_trace_errors_name_the_line(kvsim, tmp_path):
+    t = tmp_path / "t.csv"
+    t.write_text("#kvsim-trace v1\nid,arrival_s,prompt_len,decode_len\n0,0.5,10,5\n1,0.4,10,5\n")
+    r = run(kvsim, "run", "--config", write(tmp_path, "c.json", {"trace": str(t), "instances": 2}),
+            "--out", str(tmp_path / "o"))
+    assert r.returncode == 2 and "t.csv:4: arrival_s decreases" in r.stderr
+
+
+def test_no_gpu_fails_loudly(kvsim, tmp_path):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU visible")
+    r = run(kvsim, "run", "--config", write(tmp_path, "c.json", {"num_requests": 5}), "--out", str(tmp_path / "o"))
+    assert r.returncode == 3 and "no CPU fallback" in r.stderr
+
+
+# ------------------------------------------------------------------ GPU
+CFG1 = {"model": "llama2-7b", "device": "h100", "instances": 4, "policy": "accellm", "rate": 2.0,
+        "num_requests": 1000, "workload": {"prompt_range": [512, 512], "decode_range": [10, 10]}, "seed": 3}
+
+
+@pytest.mark.gpu
+def test_run_records_match_oracle(kvsim, tmp_path):
+    out = tmp_path / "o"
+    r = run(kvsim, "run", "--config", write(tmp_path, "c.json", CFG1), "--out", str(out), "--emit-events")
+    assert r.returncode == 0, r.stderr
+    rep = json.load(open(out / "report.json"))
+    p = make_point(model="llama2-7b", device="h100", policy="accellm", instances=4, rate=2.0, num_requests=1000,
+                   prompt=512, decode=10, seed=3)
+    ref = run_oracle(p, ev_cap=0)
+    got = rep["points"][0]
+    assert got["summary"]["n_completed"] == 1000
+    for q, rr in zip(got["requests"], ref.recs):
+        assert q["ttft_s"] == rr.first_token_s - rr.arrival_s
+        assert q["jct_s"] == rr.completion_s - rr.arrival_s
+        assert q["tbt_max_s"] == rr.tbt_max_s
+    rows = list(csv.DictReader(open(out / "summary.csv")))
+    assert float(rows[0]["jct_mean"]) == ref.summary.jct_mean
+    assert (out / "events.jsonl").stat().st_size > 0
+    meta = json.load(open(out / "meta.json"))
+    assert meta["config"]["seeds"] == [3] and len(meta["config_hash"]) == 16
+
+
+@pytest.mark.gpu
+def test_sweep_matches_oracle_and_is_deterministic(kvsim, tmp_path):
+    cfg = {"policies": ["accellm", "splitwise_static", "unified"], "rates": [2, 6, 12], "instances": 8,
+           "num_requests": 800, "workload": "mixed", "seed": 1}
+    c = write(tmp_path, "c.json", cfg)
+    a, b = tmp_path / "a", tmp_path / "b"
+    assert run(kvsim, "sweep", "--config", c, "--out", str(a)).returncode == 0
+    assert run(kvsim, "sweep", "--config", c, "--out", str(b)).returncode == 0
+    assert (a / "summary.csv").read_bytes() == (b / "summary.csv").read_bytes()
+    rows = list(csv.DictReader(open(a / "summary.csv")))
+    assert len(rows) == 9
+    for row in rows:
+        p = make_point(policy=row["policy"], instances=8, rate=float(row["rate"]), num_requests=800,
+                       workload="mixed", seed=1, warmup_s=0.0)
+        ref = run_oracle(p, ev_cap=0, recs=False).summary
+        for k in ("ttft_mean", "ttft_p95", "tbt_mean", "tbt_max", "jct_mean", "jct_p95", "cost_eff"):
+            assert float(row[k]) == getattr(ref, k), (row["policy"], k)
+    rep = json.load(open(a / "report.json"))
+    assert len(rep["saturation"]) == 3
+    long = list(csv.DictReader(open(a / "sweep_long.csv")))
+    assert len(long) == 9 * 11
+
+
+@pytest.mark.gpu
+def test_trace_round_trip(kvsim, tmp_path):  # SPEC.md:172 generate -> save -> load
+    cfg = dict(CFG1, workload="mixed", num_requests=300, policy="splitwise_static", instances=4)
+    g = tmp_path / "g"
+    assert run(kvsim, "gen-trace", "--config", write(tmp_path, "c.json", cfg), "--out", str(g)).returncode == 0
+    tr = str(g / "trace.csv")
+    lines = open(tr).read().splitlines()
+    assert lines[0] == "#kvsim-trace v1" and len(lines) == 302
+    a, b = tmp_path / "a", tmp_path / "b"
+    assert run(kvsim, "run", "--config", write(tmp_path, "d.json", cfg), "--out", str(a)).returncode == 0
+    cfg_t = {k: v for k, v in cfg.items() if k not in ("rate", "num_requests", "workload", "seed")}
+    cfg_t["trace"] = tr
+    r = run(kvsim, "run", "--config", write(tmp_path, "e.json", cfg_t), "--out", str(b))
+    assert r.returncode == 0, r.stderr
+    ra = json.load(open(a / "report.json"))["points"][0]
+    rb = json.load(open(b / "report.json"))["points"][0]
+    assert ra["requests"] == rb["requests"]
+
+
+def test_curves(kvsim, tmp_path):  # host perfmodel only
+    cfg = {"efficiency": {"compute_eff": 1.0, "mem_bw_eff": 1.0, "link_eff": 1.0},
+           "curves": {"phase": "both", "lengths": [500], "batch_sizes": [1, 32]}}
+    o = tmp_path / "o"
+    assert run(kvsim, "curves", "--config", write(tmp_path, "c.json", cfg), "--out", str(o)).returncode == 0
+    rows = list(csv.DictReader(open(o / "curves.csv")))
+    dec = {int(r["batch"]): r for r in rows if r["phase"] == "decode"}
+    assert abs(float(dec[1]["latency_s"]) - 0.01046) < 1e-5 and abs(float(dec[32]["tokens_per_s"]) - 2952) < 1
+    pre = [r for r in rows if r["phase"] == "prefill"]
+    assert math.isclose(float(pre[0]["tokens_per_s"]), float(pre[1]["tokens_per_s"]), rel_tol=1e-12)
