@@ -98,7 +98,7 @@ const char* const kKeys[] = {"model", "device", "num_devices", "memory_reserve_f
                              "arrival_process", "rate", "rates", "duration_s", "num_requests", "warmup_s", "seed",
                              "seeds", "efficiency", "link_aggregation", "trace", "sweep_instances",
                              "sweep_devices", "curves", "emit_records", "splitwise_cobatch", "degraded_mode",
-                             "inter_pair_leveling", "output"};
+                             "inter_pair_leveling", "output", "resource"};
 
 struct Resolved {
   jl::Value cfg;  // resolved config (defaults filled)
@@ -328,6 +328,23 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
   }
   c.set("sweep_devices", sd);
   if (const jl::Value* cv = in.find("curves")) c.set("curves", *cv);
+  if (const jl::Value* rs = in.find("resource")) {
+    // resource-sweep: {"kind": "hbm_capacity"|"link_bandwidth", "values": [...]}
+    if (!rs->is_obj()) throw ConfigError("resource must be an object");
+    for (auto& kv : rs->obj)
+      if (kv.first != "kind" && kv.first != "values") throw ConfigError("unknown resource key: " + kv.first);
+    const jl::Value* k = rs->find("kind");
+    if (!k || !k->is_str() || (k->str != "hbm_capacity" && k->str != "link_bandwidth"))
+      throw ConfigError("resource.kind: hbm_capacity | link_bandwidth");
+    jl::Value vals = num_list(rs->find("values"), "resource.values");
+    if (vals.arr.empty()) throw ConfigError("resource.values must be non-empty");
+    jl::Value r = jl::Value::object();
+    r.set("kind", *k);
+    r.set("values", vals);
+    c.set("resource", r);
+  } else if (cmd == "resource-sweep") {
+    throw ConfigError("resource-sweep needs a \"resource\" block");
+  }
   c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
                                                ? in.find("emit_records")->b
                                                : cmd == "run"));
@@ -385,6 +402,7 @@ struct PointMeta {
   double rate;
   int instances;
   uint64_t seed;
+  double resource = NAN;  // resource-sweep: the swept per-device value
 };
 
 kvsim_point_desc base_point(const jl::Value& c, const jl::Value& dev) {
@@ -433,13 +451,22 @@ int64_t derive_requests(double rate, double duration) {
   return (int64_t)std::ceil(m + 20.0 * std::sqrt(m) + 1000.0);
 }
 
-void expand(const jl::Value& c, const Trace* trace, std::vector<kvsim_point_desc>& pts, std::vector<PointMeta>& meta) {
+void expand(const jl::Value& c, const Trace* trace, std::vector<kvsim_point_desc>& pts, std::vector<PointMeta>& meta,
+            bool resource_axis = false) {
   const int64_t nreq = (int64_t)c.find("num_requests")->num;
   const jl::Value& d = *c.find("duration_s");
   const double dur = d.is_str() ? INFINITY : d.num;
   std::vector<double> rates;
   for (auto& r : c.find("rates")->arr) rates.push_back(r.num);
   if (trace) rates = {0.0};
+  std::vector<double> rvals = {NAN};
+  std::string rkind;
+  if (resource_axis) {
+    rvals.clear();
+    for (auto& e : c.find("resource")->find("values")->arr) rvals.push_back(e.num);
+    rkind = c.find("resource")->find("kind")->str;
+  }
+  for (double rv : rvals)
   for (auto& dev : c.find("sweep_devices")->arr)
     for (auto& ni : c.find("sweep_instances")->arr)
       for (auto& pol : c.find("policies")->arr)
@@ -456,9 +483,13 @@ void expand(const jl::Value& c, const Trace* trace, std::vector<kvsim_point_desc
             } else {
               p.num_requests = nreq > 0 ? nreq : derive_requests(rate, std::isinf(dur) ? 300.0 : dur);
             }
+            if (resource_axis) {
+              if (rkind == "hbm_capacity") p.hbm_capacity = rv;
+              else p.link_bandwidth = rv;
+            }
             p.user_tag = pts.size();
             pts.push_back(p);
-            meta.push_back(PointMeta{pol.str, dev.find("name")->str, rate, p.num_instances, p.seed});
+            meta.push_back(PointMeta{pol.str, dev.find("name")->str, rate, p.num_instances, p.seed, rv});
           }
 }
 
@@ -569,6 +600,78 @@ jl::Value meta_json(const jl::Value& cfg, const std::string& cmd) {
   return m;
 }
 
+// compare: per (rate, instances, device, seed) group, every
+// policy's metrics as ratios to the first policy of the config. The trace
+// fingerprint hashes everything that defines the generated trace (the
+// generator is a pure function of it), so equal fingerprints = identical traces.
+jl::Value compare_table(const jl::Value& cfg, const std::vector<PointMeta>& meta,
+                        const std::vector<kvsim_point_summary>& sum) {
+  jl::Value rows = jl::Value::array();
+  const std::string first = cfg.find("policies")->arr.at(0).str;
+  const std::string wl = jl::dump(*cfg.find("workload"), 0) + jl::dump(*cfg.find("duration_s"), 0) +
+                         jl::dump(*cfg.find("num_requests"), 0) + cfg.find("arrival_process")->str;
+  for (size_t i = 0; i < meta.size(); ++i) {
+    if (meta[i].policy != first) continue;
+    jl::Value g = jl::Value::object();
+    char fp[32];
+    std::snprintf(fp, sizeof fp, "%016llx",
+                  (unsigned long long)fnv1a(wl + num(meta[i].rate) + std::to_string(meta[i].seed)));
+    g.set("rate", jl::Value::number(meta[i].rate));
+    g.set("instances", jl::Value::number(meta[i].instances));
+    g.set("device", jl::Value::string(meta[i].device));
+    g.set("seed", jl::Value::number((double)meta[i].seed));
+    g.set("trace_fingerprint", jl::Value::string(fp));
+    jl::Value ratios = jl::Value::object();
+    for (size_t j = 0; j < meta.size(); ++j) {
+      if (meta[j].rate != meta[i].rate || meta[j].instances != meta[i].instances || meta[j].device != meta[i].device ||
+          meta[j].seed != meta[i].seed)
+        continue;
+      jl::Value m = jl::Value::object();
+      auto ratio = [](double a, double b) { return (std::isnan(a) || std::isnan(b) || b == 0) ? jl::Value() : jl::Value::number(a / b); };
+      m.set("cost_eff", ratio(sum[j].cost_eff, sum[i].cost_eff));
+      m.set("jct_mean", ratio(sum[j].jct_mean, sum[i].jct_mean));
+      m.set("ttft_mean", ratio(sum[j].ttft_mean, sum[i].ttft_mean));
+      m.set("tbt_mean", ratio(sum[j].tbt_mean, sum[i].tbt_mean));
+      m.set("tbt_max", ratio(sum[j].tbt_max, sum[i].tbt_max));
+      ratios.set(meta[j].policy, m);
+    }
+    g.set("ratios_vs_" + first, ratios);
+    rows.push(g);
+  }
+  return rows;
+}
+
+// resource-sweep knees: per policy, the smallest resource value
+// whose JCT is within 1% of the policy's best JCT and whose cost efficiency is
+// within 1% of its best; failed points (e.g. capacity below the weights) are
+// skipped.
+jl::Value resource_knees(const std::vector<PointMeta>& meta, const std::vector<kvsim_point_summary>& sum) {
+  jl::Value out = jl::Value::array();
+  std::vector<std::string> pols;
+  for (auto& m : meta)
+    if (std::find(pols.begin(), pols.end(), m.policy) == pols.end()) pols.push_back(m.policy);
+  for (auto& pol : pols) {
+    double best_jct = INFINITY, best_ce = -INFINITY;
+    for (size_t i = 0; i < meta.size(); ++i)
+      if (meta[i].policy == pol && sum[i].status == 0) {
+        best_jct = std::min(best_jct, sum[i].jct_mean);
+        best_ce = std::max(best_ce, sum[i].cost_eff);
+      }
+    double knee = NAN;
+    for (size_t i = 0; i < meta.size(); ++i)
+      if (meta[i].policy == pol && sum[i].status == 0 && sum[i].jct_mean <= 1.01 * best_jct &&
+          sum[i].cost_eff >= 0.99 * best_ce)
+        if (std::isnan(knee) || meta[i].resource < knee) knee = meta[i].resource;
+    jl::Value k = jl::Value::object();
+    k.set("policy", jl::Value::string(pol));
+    k.set("knee", std::isnan(knee) ? jl::Value() : jl::Value::number(knee));
+    k.set("best_jct_mean", std::isinf(best_jct) ? jl::Value() : jl::Value::number(best_jct));
+    k.set("best_cost_eff", std::isinf(best_ce) ? jl::Value() : jl::Value::number(best_ce));
+    out.push(k);
+  }
+  return out;
+}
+
 struct Args {
   std::string cmd, config, out = "out";
   bool emit_events = false, has_seed = false;
@@ -578,7 +681,7 @@ struct Args {
 
 [[noreturn]] void usage() {
   std::fprintf(stderr,
-               "usage: kvsim run|sweep|curves|gen-trace|validate-config --config PATH [--seed N] [--out DIR] "
+               "usage: kvsim run|sweep|resource-sweep|curves|gen-trace|validate-config --config PATH [--seed N] [--out DIR] "
                "[--emit-events] [--gpus N]\n");
   std::exit(2);
 }
@@ -614,6 +717,7 @@ int cmd_main(const Args& a) {
       if (raw.obj[i].first == "seed") { raw.obj.erase(raw.obj.begin() + i); break; }
   }
   const std::string cmdk = a.cmd == "validate-config" ? "run" : a.cmd;
+  if (a.cmd == "resource-sweep" && !raw.find("resource")) throw ConfigError("resource-sweep needs a \"resource\" block");
   jl::Value cfg = resolve(raw, cmdk);
   // host-side validation of every point (SPEC.md:416 messages)
   Trace trace;
@@ -621,7 +725,7 @@ int cmd_main(const Args& a) {
   if (has_trace) trace = load_trace(cfg.find("trace")->str);
   std::vector<kvsim_point_desc> pts;
   std::vector<PointMeta> meta;
-  expand(cfg, has_trace ? &trace : nullptr, pts, meta);
+  expand(cfg, has_trace ? &trace : nullptr, pts, meta, a.cmd == "resource-sweep");
   if (a.cmd == "run" || a.cmd == "validate-config") {
     char err[256];
     for (auto& p : pts) {
@@ -682,7 +786,7 @@ int cmd_main(const Args& a) {
     write_file(a.out + "/trace.csv", trace_csv(t));
     return 0;
   }
-  if (a.cmd != "run" && a.cmd != "sweep") usage();
+  if (a.cmd != "run" && a.cmd != "sweep" && a.cmd != "resource-sweep") usage();
   const bool records = cfg.find("emit_records")->b;
   const size_t ev_cap = a.emit_events ? (size_t)1 << 20 : 0;
   RunOut r;
@@ -749,6 +853,7 @@ int cmd_main(const Args& a) {
       sat.push(s);
     }
     report.set("saturation", sat);
+    report.set("compare", compare_table(cfg, meta, r.sum));
     // long form (policy, rate, metric, value)
     std::string lf = "policy,rate,instances,device,seed,metric,value\n";
     const char* cols[] = {"ttft_mean", "ttft_p95", "tbt_mean", "tbt_max", "jct_mean", "jct_p95", "cost_eff",
@@ -762,6 +867,17 @@ int cmd_main(const Args& a) {
               meta[i].device + "," + std::to_string(meta[i].seed) + "," + cols[k] + "," + num(vals[k]) + "\n";
     }
     write_file(a.out + "/sweep_long.csv", lf);
+  }
+  if (a.cmd == "resource-sweep") {
+    const std::string kind = cfg.find("resource")->find("kind")->str;
+    std::string rc = "policy,rate,instances,seed," + kind + ",jct_mean,cost_eff,ttft_mean,tbt_mean,peak_kv_gb,status\n";
+    for (size_t i = 0; i < pts.size(); ++i)
+      rc += meta[i].policy + "," + num(meta[i].rate) + "," + std::to_string(meta[i].instances) + "," +
+            std::to_string(meta[i].seed) + "," + num(meta[i].resource) + "," + num(r.sum[i].jct_mean) + "," +
+            num(r.sum[i].cost_eff) + "," + num(r.sum[i].ttft_mean) + "," + num(r.sum[i].tbt_mean) + "," +
+            num(r.sum[i].peak_kv_gb) + "," + std::to_string(r.sum[i].status) + "\n";
+    write_file(a.out + "/resource_sweep.csv", rc);
+    report.set("knees", resource_knees(meta, r.sum));
   }
   write_file(a.out + "/report.json", jl::dump(report) + "\n");
   write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");

@@ -47,6 +47,13 @@ KV_HD double kdiv(double a, double b) {
 #endif
 }
 KV_HD double kmax(double a, double b) { return a > b ? a : b; }
+KV_HD double kfma(double a, double b, double c) {
+#if defined(__CUDA_ARCH__)
+  return __fma_rn(a, b, c);
+#else
+  return __builtin_fma(a, b, c);
+#endif
+}
 
 KV_HD uint64_t as_u64(double d) {
 #if defined(__CUDA_ARCH__)
@@ -145,6 +152,26 @@ KV_HD double poisson_gap(uint64_t key, int64_t i, double rate) {
   return kdiv(-plog(unit_open0(draw_k(key, i, 2))), rate);
 }
 
+// Correctly rounded n / d for positive normal operands, given rd = RN(1/d).
+// q1 = q0 + (n - q0 d) rd is accepted only if its exact remainder
+// r1 = n - q1 d (one FMA; exact whenever q1 is the correctly rounded
+// quotient) satisfies |r1| < d * ulp(q1)/2 with q1 not a power of two. That
+// inequality holds iff q1 == RN(n / d) and n / d is not a tie, so the result
+// equals IEEE division bit for bit; otherwise the IEEE division is used.
+KV_HD double kdiv_rcp(double n, double d, double rd) {
+  const double q0 = kmul(n, rd);
+  const double q1 = kfma(kfma(-q0, d, n), rd, q0);
+  const double r1 = kfma(-q1, d, n);
+  const uint64_t qb = as_u64(q1);
+  const uint64_t ex = (qb >> 52) & 0x7ffull;
+  if ((qb & 0x000fffffffffffffull) != 0 && ex > 54 && ex < 0x7ff) {
+    const double h = kmul(d, as_f64((ex - 53) << 52));  // d * ulp(q1) / 2, exact (power of two)
+    const double ar = r1 < 0.0 ? -r1 : r1;
+    if (ar < h) return q1;
+  }
+  return kdiv(n, d);
+}
+
 // ----------------------------------------------------------- cost model (§1)
 struct Perf {
   double kvb;        // bytes of K+V per token, all layers
@@ -152,6 +179,7 @@ struct Perf {
   double W;          // weight bytes
   double pf_den;     // num_devices * peak_flops * compute_eff
   double mem_den;    // num_devices * hbm_bandwidth * mem_bw_eff
+  double mem_rcp;    // RN(1 / mem_den), for kdiv_rcp
   double two_p;      // 2 * param_count
   double attn;       // 4 * hidden * layers
   double link_bw;    // effective inter-instance bandwidth
@@ -166,6 +194,7 @@ KV_HD Perf make_perf(const kvsim_point_desc& p) {
   f.W = kmul(p.param_count, (double)p.bytes_per_value);
   f.pf_den = kmul(kmul((double)p.num_devices, p.peak_flops), p.compute_eff);
   f.mem_den = kmul(kmul((double)p.num_devices, p.hbm_bandwidth), p.mem_bw_eff);
+  f.mem_rcp = kdiv(1.0, f.mem_den);
   f.two_p = kmul(2.0, p.param_count);
   f.attn = (double)(4ll * p.hidden_dim * p.num_layers);
   f.link_bw = p.link_mode == KVSIM_LINK_SINGLE

@@ -22,6 +22,14 @@
 namespace kvsim_dev {
 using namespace kvsim_math;
 
+#if defined(KVSIM_EMU) && defined(KVSIM_EMU_PROFILE)
+// emulator-only call counters (tests/emu profiling of the event mix)
+inline long long emu_prof[32];
+#define EMU_COUNT(i) do { if (simt::lane_id() == 0) emu_prof[i]++; } while (0)
+#else
+#define EMU_COUNT(i) do {} while (0)
+#endif
+
 constexpr int kMaxInst = 32;
 constexpr int32_t kRemMask = 0x1fffffff;
 constexpr int32_t kJoin = 0x40000000;  // no decode step since joining the batch
@@ -43,6 +51,8 @@ struct PointConst {
 struct Counters {
   int64_t n_steps, n_prefills, n_moves, n_preempt, n_evict;
   int64_t tok_total, tok_window, pf_tokens, mir_tokens, n_loop;
+  int64_t ev_n;  // event-log cursor (atomic; lanes log concurrently)
+  int64_t adv_events;  // virtual step ends processed by advance() (lane atomics)
 };
 struct WarpScratch {
   PointConst pc;  // written by lane 0 at point start, read (broadcast) by all
@@ -105,10 +115,10 @@ struct Sim {
   int64_t next_rid;
   bool has_next;
   // uniform counters that steer control flow
-  int64_t n_events, ev_n;
+  int64_t n_events;
   double now;     // time of the event being processed (event-log timestamps)
   double t_last;  // latest event time processed (makespan)
-  bool chain_steps = true;  // exact step chaining (fast_forward); off = plain event loop
+  static constexpr bool chain_steps = true;  // exact step chaining (advance); off = plain event loop
   static constexpr bool logging = LOG;  // event log compiled in (parity runs) or out (sweeps)
   int32_t status;
   // lane-owned instance state (lane x <-> instance x)
@@ -116,6 +126,11 @@ struct Sim {
   int64_t L_used, L_peak, L_skv, L_skv_in, L_job_s1, L_copy_tok;
   int32_t L_role, L_job, L_nb, L_ni, L_pend, L_njob, L_ncopy;
   int32_t L_minrem;  // lower bound of remaining tokens over the batch
+  // chained steps not yet applied to the batch arrays (see advance/flush)
+  int32_t L_dj, L_compB;
+  double L_dG, L_de1, L_dpe, L_comp;
+  int64_t L_kvmin;   // AcceLLM: lower bound of kv over copy-holding members
+  double L_tlast;    // latest virtual event time this lane processed (makespan)
   int64_t L_final;   // splitwise: sum of final KV (prompt+decode-1) over batch + incoming
   // lane-owned queue state (lane q <-> queue q)
   int32_t Q_head, Q_n;
@@ -167,28 +182,29 @@ struct Sim {
     }
   }
 
+  KV_DEV void put_event(int64_t k, double t, int kind, int inst, int a, int b, int64_t c) {
+    if (k < A->ev_cap) {
+      kvsim_event_record r;
+      r.t = t; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
+      evlog()[k] = r;
+    }
+  }
+  // uniform call: one record at the current event time
   KV_DEV void log(int kind, int inst, int a, int b, int64_t c) {
     if constexpr (!LOG) return;
-    if (lane == 0 && ev_n < A->ev_cap) {
-      kvsim_event_record r;
-      r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
-      evlog()[ev_n] = r;
-    }
-    ev_n += 1;
+    if (lane == 0) put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
+    simt::sync();
+  }
+  // divergent call: this lane logs one record at time t
+  KV_DEV void log_one(double t, int kind, int inst, int a, int b, int64_t c) {
+    if constexpr (!LOG) return;
+    put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), t, kind, inst, a, b, c);
   }
   // lane-parallel logging: lanes with `p` log one record each (moves)
   KV_DEV void log_lanes(bool p, int kind, int inst, int a, int b, int64_t c) {
     if constexpr (!LOG) return;
-    unsigned m = simt::ballot(p);
-    if (p) {
-      int64_t k = ev_n + simt::popc(m & simt::lanemask_lt());
-      if (k < A->ev_cap) {
-        kvsim_event_record r;
-        r.t = now; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
-        evlog()[k] = r;
-      }
-    }
-    ev_n += simt::popc(m);
+    if (p) put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
+    simt::sync();
   }
 
   // ------------------------------------------------------------- queues
@@ -261,10 +277,10 @@ struct Sim {
     simt::sync();  // previous point's readers are done with the scratch
     if (lane == 0) {
       W->pc = pc;
-      W->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      W->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     }
     simt::sync();
-    n_events = ev_n = 0;
+    n_events = 0;
     now = 0.0;
     t_last = 0.0;
     L_busy_until = L_job_start = L_prev_end = L_mirror_fin = L_busy_time = 0.0;
@@ -276,6 +292,9 @@ struct Sim {
     L_nb = L_ni = L_pend = L_njob = L_ncopy = 0;
     L_minrem = 0x7fffffff;
     L_final = 0;
+    L_dj = 0; L_compB = -1; L_dG = L_de1 = L_dpe = L_comp = 0.0;
+    L_kvmin = INT64_MAX;
+    L_tlast = 0.0;
     Q_head = 0; Q_n = 0; Q_tok = 0;
     // splitwise directed links
     if (policy == KVSIM_POLICY_SPLITWISE)
@@ -339,9 +358,10 @@ struct Sim {
   // requests holding a copy, and the number of members holding a copy.
   struct StepOut {
     int32_t nb_old, completed, m_copies, copy_done, minrem;
-    int64_t kv_done, copy_free;
+    int64_t kv_done, copy_free, kvmin;
   };
   KV_DEV_NOINLINE StepOut step_loop(int x, double t) {
+    EMU_COUNT(0);
     StepOut o;
     const int32_t nb = get(L_nb, x);
     const double prev = get(L_prev_end, x);
@@ -350,7 +370,7 @@ struct Sim {
     int32_t* kvb_a = b_kvb(x);
     double* tbt_a = b_tbt(x);
     int32_t wpos = 0, completed = 0, m = 0, copy_done = 0, minrem = 0x7fffffff;
-    int64_t kv_done = 0, copy_free = 0;  // per-lane partials
+    int64_t kv_done = 0, copy_free = 0, kvmin = INT64_MAX;  // per-lane partials
     for (int32_t j0 = 0; j0 < nb; j0 += 32) {
       const int32_t j = j0 + lane;
       const bool act = j < nb;
@@ -382,6 +402,10 @@ struct Sim {
       simt::sync();  // all reads of this chunk precede its compaction writes
       if (surv) {
         if (rem < minrem) minrem = rem;
+        if (hasc) {
+          const int64_t kvn = (int64_t)(kvb_a[j]) - rem;  // kv after this step
+          if (kvn < kvmin) kvmin = kvn;
+        }
         rem_a[dst] = rem | (rf & kCopy);
         if (moved) {
           rid_a[dst] = rid;
@@ -411,12 +435,20 @@ struct Sim {
     o.kv_done = simt::warp_sum(kv_done);
     o.copy_free = simt::warp_sum(copy_free);
     o.minrem = simt::warp_min(minrem);
+    o.kvmin = simt::warp_min(kvmin);
     simt::sync();
     return o;
   }
 
   // -------------------------------------------------------------- joins
-  KV_DEV_NOINLINE void join(int x, double t) {
+  KV_DEV void join(int x, double t) {
+    if (get(L_ni, x) == 0) return;
+    if (get(L_min_ready, x) > t) return;
+    join_slow(x, t);
+  }
+  KV_DEV_NOINLINE void join_slow(int x, double t) {
+    EMU_COUNT(1);
+    flush(x);
     const int32_t ni = get(L_ni, x);
     if (ni == 0) return;
     if (get(L_min_ready, x) > t) return;
@@ -424,7 +456,7 @@ struct Sim {
     int32_t* irid = i_rid(x);
     double* irdy = i_ready(x);
     int32_t keep = 0, add = 0, ncopy = 0, minrem = 0x7fffffff;
-    int64_t kvsum = 0;
+    int64_t kvsum = 0, kvmin = INT64_MAX;
     double mn = as_f64(0x7ff0000000000000ull);
     for (int32_t j0 = 0; j0 < ni; j0 += 32) {
       const int32_t j = j0 + lane;
@@ -452,6 +484,7 @@ struct Sim {
         b_tbt(x)[k] = c_tbt()[rid];
         kvsum += (int64_t)pl + em - 1;
         if (dl - em < minrem) minrem = dl - em;
+        if (hasc && (int64_t)pl + em - 1 < kvmin) kvmin = (int64_t)pl + em - 1;
       }
       ncopy += simt::popc(simt::ballot(go && c_cpy()[go ? rid : 0] >= 0));
       keep += simt::popc(sm);
@@ -460,9 +493,11 @@ struct Sim {
     kvsum = simt::warp_sum(kvsum);
     mn = simt::warp_min(mn);
     minrem = simt::warp_min(minrem);
+    kvmin = simt::warp_min(kvmin);
     simt::sync();
     if (own(x)) {
       if (minrem < L_minrem) L_minrem = minrem;
+      if (kvmin < L_kvmin) L_kvmin = kvmin;
       L_nb += add;
       L_ni -= add;
       L_skv += kvsum;
@@ -514,6 +549,7 @@ struct Sim {
   };
   // largest redundant copy held on instance x (max kv, ties lowest rid)
   KV_DEV_NOINLINE Found largest_copy_on(int x) {
+    flush(x ^ 1);
     const int y = x ^ 1;
     uint64_t best = 0;
     int32_t bidx = -1, bwhere = 0;
@@ -547,6 +583,7 @@ struct Sim {
     return r;
   }
   KV_DEV_NOINLINE void evict(int x, const Found& v) {
+    EMU_COUNT(14);
     const int y = x ^ 1;
     int64_t held = v.kv;
     if (v.where == 1) {
@@ -564,6 +601,8 @@ struct Sim {
 
   // ------------------------------------------------------ preemption (P9)
   KV_DEV_NOINLINE void preempt_newest(int x) {
+    EMU_COUNT(15);
+    flush(x);
     const int32_t nb = get(L_nb, x);
     int32_t best = -1, bidx = -1;
     for (int32_t j = lane; j < nb; j += 32) {
@@ -630,6 +669,7 @@ struct Sim {
 
   // ------------------------------------------- decode step (splitwise/accellm)
   KV_DEV_NOINLINE void step_start(int x, double t) {
+    EMU_COUNT(2);
     int32_t nb = get(L_nb, x);
     if (nb == 0) return;
     const bool acc = policy == KVSIM_POLICY_ACCELLM;
@@ -672,15 +712,14 @@ struct Sim {
     }
     log(KVSIM_EV_STEP_START, x, nb, 0, K);
     if (preempted && acc) ensure_prefill(x >> 1, t);
-    else if (!preempted && chain_steps) {
-      if (acc) fast_forward_pair(x);
-      else fast_forward(x, t);
-    }
+
   }
 
   KV_DEV_NOINLINE void step_end(int x, double t) {
+    EMU_COUNT(3);
     account_job(x, t);
     if (lane == 0) W->ct.n_steps += 1;
+    flush(x);
     const StepOut o = step_loop(x, t);
     const int32_t surv = o.nb_old - o.completed;
     if (own(x)) {
@@ -690,6 +729,7 @@ struct Sim {
       L_nb = surv;
       L_prev_end = t;
       L_minrem = o.minrem;
+      L_kvmin = o.kvmin;
       L_final -= o.kv_done + o.completed;
     }
     count_tokens(o.nb_old, t);
@@ -711,29 +751,107 @@ struct Sim {
 
 
   // ------------------------------------------------ exact step chaining
-  // Called right after x started a decode step at boundary t. If x's next
-  // step ends cannot interact with any other pending event (no completion,
-  // join, admission, policy action or memory pressure on x, and every
-  // interacting event -- the next arrival, x's pair partner (AcceLLM), the
-  // prefill instances (Splitwise) -- is later), those step-end events are
-  // processed here in one register loop plus a single pass over the batch.
-  // Events of independent instances/pairs commute with them, so every
-  // per-request timestamp, ledger value and decision is unchanged.
-  KV_DEV_NOINLINE void fast_forward(int x, double t) {
-    (void)t;
+  // A decode step end of instance x is *virtual* when nothing can interact
+  // with it: no member completes (remaining-token bound), nobody joins (min
+  // incoming ready time), the next step's KV growth fits (and, AcceLLM, the
+  // partner's mirror lines), no rebalance move is possible (closed-form
+  // bound on the smallest copy-holding KV vs the growing token imbalance),
+  // no admission is pending, and every event that can read or change x's
+  // state -- the next arrival, the prefill instances (Splitwise), the pair
+  // partner (AcceLLM) -- comes later in (time, kind, id) order. Events of
+  // independent instances/pairs commute with it, so results are unchanged.
+  //
+  // advance(): every driving lane (an instance, or the even lane of an
+  // AcceLLM pair) processes its virtual step ends in registers, in parallel
+  // across lanes. The per-request part (remaining tokens, TBT maxima) is
+  // deferred: L_dj steps, first-step end L_de1, previous end L_dpe, max later
+  // gap L_dG; flush() applies it in one pass when the batch is next touched.
+  KV_DEV void flush(int x) {
+    if (get(L_dj, x) == 0) return;
+    flush_slow(x);
+  }
+  KV_DEV_NOINLINE void flush_slow(int x) {
+    const int32_t j = get(L_dj, x);
+    const double e1 = get(L_de1, x), pe = get(L_dpe, x), G = get(L_dG, x);
     const int32_t B = get(L_nb, x);
-    if (B <= 0) return;
-    int64_t kmax = (int64_t)get(L_minrem, x) - 1;
-    if (kmax < 1) return;
+    int32_t* rem_a = b_rem(x);
+    double* tbt_a = b_tbt(x);
+    for (int32_t q = lane; q < B; q += 32) {
+      const int32_t rf = rem_a[q];
+      const double tb = tbt_a[q];
+      const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe;
+      double g1 = ksub(e1, last);
+      if (G > g1) g1 = G;
+      rem_a[q] = ((rf & kRemMask) - j) | (rf & kCopy);
+      if (g1 > tb) tbt_a[q] = g1;
+    }
+    simt::sync();
+    if (own(x)) { L_dj = 0; L_dG = 0.0; }
+  }
+
+  // decode compute floor for batch B and mirror time for m lines (lane cache)
+  KV_DEV double comp_floor(int32_t B) {
+    if (B != L_compB) { L_compB = B; L_comp = kdiv(kmul(PC.f.two_p, (double)B), PC.f.pf_den); }
+    return L_comp;
+  }
+
+  // per-member register state of an AcceLLM pair chain (driver lane)
+  struct MemberChain {
+    double e, js, busy, link, mfin, prev, de1, dpe, dG, mr, comp, mlat;
+    int64_t skv, skv_in, used, peak, copy_tok, kvmin, tw;
+    int32_t B, ni, m, minrem, dj, role, steps;
+    bool stepping;
+  };
+  KV_DEV bool pair_step(MemberChain& c, MemberChain& o, int cid, const double ht, const int32_t hk,
+                        const int64_t cap, const double warmup, int64_t& budget) {
+    if (!(c.e < ht || (c.e == ht && 3 * 64 + cid < hk))) return false;
+    if (c.minrem < 2 || c.e >= c.mr || budget <= 0) return false;
+    if (o.role == ROLE_DECODE && c.kvmin != INT64_MAX) {  // rebalance_pair at cid's next boundary
+      const int64_t cz = (int64_t)c.B + c.ni - o.B - o.ni;
+      if (cz >= 1) {
+        const int64_t dz = (c.skv + c.skv_in + c.B) - (o.skv + o.skv_in);
+        const int64_t lim = cz >= 2 ? dz : dz - 1;
+        if (c.kvmin + 1 <= lim) return false;
+      }
+    }
+    if (c.used + c.B > cap || o.used + c.m > cap) return false;
+    const double e = c.e;
+    if (c.js >= warmup) c.busy = kadd(c.busy, ksub(e, c.js));
+    if (e >= warmup) c.tw += c.B;
+    if (c.dj == 0) { c.de1 = e; c.dpe = c.prev; }
+    else { const double g = ksub(e, c.prev); if (g > c.dG) c.dG = g; }
+    if (c.m > 0) {
+      const double st = e > c.link ? e : c.link;
+      c.link = kadd(st, c.mlat);
+      c.mfin = c.link;
+      if constexpr (LOG) log_one(e, KVSIM_EV_TRANSFER, cid, cid ^ 1, 1, c.m);
+    }
+    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, cid, c.B, 0, 0);
+    c.skv += c.B;
+    c.used += c.B;
+    if (c.used > c.peak) c.peak = c.used;
+    o.used += c.m;
+    o.copy_tok += c.m;
+    if (o.used > o.peak) o.peak = o.used;
+    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv);
+    c.prev = e;
+    c.js = e;
+    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(PC.f.W, kmul((double)c.skv, PC.f.kvb)), PC.f.mem_den, PC.f.mem_rcp), c.comp));
+    c.dj += 1;
+    c.minrem -= 1;
+    if (c.kvmin != INT64_MAX) c.kvmin += 1;
+    c.steps += 1;
+    budget -= 1;
+    return true;
+  }
+
+  // drive: bitmask of lanes allowed to advance (instances; AcceLLM: any lane
+  // of a pair selects the pair)
+  KV_DEV_NOINLINE void advance(unsigned drive) {
     const double kInf = as_f64(0x7ff0000000000000ull);
-    const int y = x ^ 1;
-    const bool acc = policy == KVSIM_POLICY_ACCELLM;
     double ht = has_next ? t_next : kInf;
-    int32_t hk = -1;  // arrivals precede every instance event at equal time
-    int32_t m = 0;
-    if (policy == KVSIM_POLICY_UNIFIED) {
-      if (get(Q_n, x) != 0) return;
-    } else if (policy == KVSIM_POLICY_SPLITWISE) {
+    int32_t hk = -1;  // arrivals precede instance events at equal time
+    if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
       const bool all_busy = simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
       if (!all_busy) {
         if (get(Q_n, 0) != 0) return;
@@ -747,320 +865,160 @@ struct Sim {
         if (ot < pt || (ot == pt && ok < pk)) { pt = ot; pk = ok; }
       }
       if (pt < ht || (pt == ht && pk < hk)) { ht = pt; hk = pk; }
+    }
+    const int64_t cap = PC.f.cap;
+    const double warmup = PC.warmup;
+    int64_t budget = PC.event_budget - n_events - W->ct.adv_events;
+    int64_t steps = 0, tw = 0, mir = 0, tok = 0;
+    double tmax = 0.0;
+    if constexpr (POL != KVSIM_POLICY_ACCELLM) {
+      bool go = ((drive >> lane) & 1) && lane < n && L_job == JOB_STEP;
+      // unified: only pure decode iterations (no co-batched prefill in flight, none pending)
+      if constexpr (POL == KVSIM_POLICY_UNIFIED) go = go && Q_n == 0 && L_njob == 0 && L_nb > 0;
+      else go = go && lane >= n_prefill && L_nb > 0;
+      if (go) {
+        const int32_t B = L_nb;
+        const double mr = L_ni > 0 ? L_min_ready : kInf;
+        const double comp = comp_floor(B);
+        const int32_t key = 3 * 64 + lane;
+        while (L_minrem >= 2 && L_used + B <= cap && steps < budget) {
+          const double e = L_busy_until;
+          if (!(e < ht || (e == ht && key < hk))) break;
+          if (e >= mr) break;
+          if (L_job_start >= warmup) L_busy_time = kadd(L_busy_time, ksub(e, L_job_start));
+          if (e >= warmup) tw += B;
+          if (L_dj == 0) { L_de1 = e; L_dpe = L_prev_end; }
+          else { const double g = ksub(e, L_prev_end); if (g > L_dG) L_dG = g; }
+          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+          L_skv += B;
+          L_used += B;
+          if (L_used > L_peak) L_peak = L_used;
+          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, L_skv);
+          L_prev_end = e;
+          L_job_start = e;
+          L_busy_until = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(PC.f.W, kmul((double)L_skv, PC.f.kvb)), PC.f.mem_den, PC.f.mem_rcp), comp));
+          L_dj += 1;
+          L_minrem -= 1;
+          steps += 1;
+          tmax = e;
+        }
+        tok = steps * B;
+      }
     } else {
-      if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
-      const int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
-      if (get(L_role, y) == ROLE_DECODE && c >= 1) {
-        // rebalance_pair at chained boundary i moves iff some copy-holding
-        // member has kv0 + i <= lim0 + i*B (d grows by B per step, each kv by 1)
-        const int64_t d0 = load_of(x) - load_of(y);
-        const int64_t lim0 = c >= 2 ? d0 : d0 - 1;
-        int64_t kvmin = INT64_MAX;
-        for (int32_t q = lane; q < B; q += 32) {
-          const int32_t rf = b_rem(x)[q];
-          if (rf & kCopy) {
-            const int64_t kv = (int64_t)b_kvb(x)[q] - (rf & kRemMask);
-            if (kv < kvmin) kvmin = kv;
-          }
+      // AcceLLM: the even lane of each pair drives both members in merged order
+      const int pl = lane | 1;  // partner lane (valid for even lanes)
+      {
+        const int32_t pj = simt::shfl(L_job, pl), pp = simt::shfl(L_pend, pl);
+        const int32_t qn = simt::shfl(Q_n, (lane >> 1) & 31);
+        const bool cand = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qn == 0 &&
+                          !L_pend && !pp && (L_job == JOB_STEP || pj == JOB_STEP);
+        if (simt::ballot(cand) == 0) return;
+      }
+      MemberChain b;
+      b.stepping = simt::shfl(L_job, pl) == JOB_STEP;
+      const int32_t bjob = simt::shfl(L_job, pl);
+      b.B = simt::shfl(L_nb, pl); b.ni = simt::shfl(L_ni, pl);
+      b.e = simt::shfl(L_busy_until, pl); b.js = simt::shfl(L_job_start, pl);
+      b.busy = simt::shfl(L_busy_time, pl); b.link = simt::shfl(L_link, pl);
+      b.mfin = simt::shfl(L_mirror_fin, pl); b.prev = simt::shfl(L_prev_end, pl);
+      b.skv = simt::shfl(L_skv, pl); b.skv_in = simt::shfl(L_skv_in, pl);
+      b.used = simt::shfl(L_used, pl); b.peak = simt::shfl(L_peak, pl);
+      b.copy_tok = simt::shfl(L_copy_tok, pl); b.m = simt::shfl(L_ncopy, pl);
+      b.minrem = simt::shfl(L_minrem, pl); b.role = simt::shfl(L_role, pl);
+      b.kvmin = simt::shfl(L_kvmin, pl); b.dj = simt::shfl(L_dj, pl);
+      b.dG = simt::shfl(L_dG, pl); b.de1 = simt::shfl(L_de1, pl); b.dpe = simt::shfl(L_dpe, pl);
+      const double bmr = simt::shfl(L_min_ready, pl);
+      const int32_t bpend = simt::shfl(L_pend, pl);
+      const int32_t qn_pair = simt::shfl(Q_n, (lane >> 1) & 31);
+      const int32_t bcompB = simt::shfl(L_compB, pl);
+      const double bcomp = simt::shfl(L_comp, pl);
+      b.mr = b.ni > 0 ? bmr : kInf;
+      b.tw = 0; b.steps = 0;
+      const bool drv = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qn_pair == 0 &&
+                       !L_pend && !bpend && (L_job == JOB_STEP || b.stepping);
+      MemberChain a;
+      a.stepping = L_job == JOB_STEP;
+      a.B = L_nb; a.ni = L_ni; a.e = L_busy_until; a.js = L_job_start; a.busy = L_busy_time; a.link = L_link;
+      a.mfin = L_mirror_fin; a.prev = L_prev_end; a.skv = L_skv; a.skv_in = L_skv_in; a.used = L_used;
+      a.peak = L_peak; a.copy_tok = L_copy_tok; a.m = L_ncopy; a.minrem = L_minrem; a.role = L_role;
+      a.kvmin = L_kvmin; a.dj = L_dj; a.dG = L_dG; a.de1 = L_de1; a.dpe = L_dpe;
+      a.mr = L_ni > 0 ? L_min_ready : kInf;
+      a.tw = 0; a.steps = 0;
+      if (drv) {
+        double pht = ht;
+        int32_t phk = hk;
+        if (!b.stepping) {  // the idle / prefilling partner's own next event bounds the chain
+          double yt = kInf;
+          int32_t yk = 0;
+          if (bjob == JOB_PREFILL) { yt = b.e; yk = 2 * 64 + lane + 1; }
+          else if (b.role == ROLE_DECODE && b.ni > 0) { yt = bmr; yk = 64 + lane + 1; }
+          if (yt < pht || (yt == pht && yk < phk)) { pht = yt; phk = yk; }
+          b.e = kInf;
         }
-        kvmin = simt::warp_min(kvmin);
-        if (kvmin != INT64_MAX) {
-          if (kvmin <= lim0) return;
-          if (B >= 2) {
-            const int64_t istar = (kvmin - lim0 + (B - 2)) / (B - 1);  // first boundary with a move
-            if (istar - 1 < kmax) kmax = istar - 1;
-          }
+        if (!a.stepping) {
+          double yt = kInf;
+          int32_t yk = 0;
+          if (L_job == JOB_PREFILL) { yt = a.e; yk = 2 * 64 + lane; }
+          else if (a.role == ROLE_DECODE && a.ni > 0) { yt = L_min_ready; yk = 64 + lane; }
+          if (yt < pht || (yt == pht && yk < phk)) { pht = yt; phk = yk; }
+          a.e = kInf;
         }
+        a.comp = a.stepping ? comp_floor(a.B) : 0.0;
+        b.comp = b.stepping ? (bcompB == b.B ? bcomp : kdiv(kmul(PC.f.two_p, (double)b.B), PC.f.pf_den)) : 0.0;
+        a.mlat = transfer_latency(PC.f, kmul((double)a.m, PC.f.kvb));
+        b.mlat = transfer_latency(PC.f, kmul((double)b.m, PC.f.kvb));
+        if (!a.stepping) a.B = 0;
+        for (;;) {
+          const bool pickA = a.stepping && (!b.stepping || !(b.e < a.e));  // ties: lower id (even lane)
+          bool ok;
+          if (pickA) ok = pair_step(a, b, lane, pht, phk, cap, warmup, budget);
+          else ok = b.stepping && pair_step(b, a, lane + 1, pht, phk, cap, warmup, budget);
+          if (!ok) break;
+        }
+        if (!a.stepping) a.B = L_nb;
+        steps = a.steps + b.steps;
+        tok = (int64_t)a.steps * a.B + (int64_t)b.steps * b.B;
+        tw = a.tw + b.tw;
+        mir = (int64_t)a.steps * a.m + (int64_t)b.steps * b.m;
+        tmax = a.prev > b.prev ? a.prev : b.prev;
+        // commit the driver's member
+        L_busy_until = a.stepping ? a.e : L_busy_until; L_job_start = a.js; L_busy_time = a.busy;
+        L_link = a.link; L_mirror_fin = a.mfin; L_prev_end = a.prev; L_skv = a.skv; L_used = a.used;
+        L_peak = a.peak; L_copy_tok = a.copy_tok; L_minrem = a.minrem; L_kvmin = a.kvmin; L_dj = a.dj;
+        L_dG = a.dG; L_de1 = a.de1; L_dpe = a.dpe;
       }
-      const int32_t jy = get(L_job, y);
-      double yt = kInf;
-      int32_t yk = 0;
-      if (jy != JOB_NONE) { yt = get(L_busy_until, y); yk = (jy == JOB_PREFILL ? 2 : 3) * 64 + y; }
-      else if (get(L_role, y) == ROLE_DECODE && get(L_ni, y) > 0) { yt = get(L_min_ready, y); yk = 64 + y; }
-      if (yt < ht || (yt == ht && yk < hk)) { ht = yt; hk = yk; }
-      m = get(L_ncopy, x);
-      if (m > 0) {
-        const int64_t roomy = (PC.f.cap - get(L_used, y)) / m;
-        if (roomy < kmax) kmax = roomy;
+      // scatter the partner member back to the odd lanes
+      const int dl = lane & ~1;
+      const bool got = simt::shfl((int32_t)drv, dl) != 0;
+      const double be = simt::shfl(b.e, dl), bjs = simt::shfl(b.js, dl), bbusy = simt::shfl(b.busy, dl);
+      const double blink = simt::shfl(b.link, dl), bmfin = simt::shfl(b.mfin, dl), bprev = simt::shfl(b.prev, dl);
+      const double bdG = simt::shfl(b.dG, dl), bde1 = simt::shfl(b.de1, dl), bdpe = simt::shfl(b.dpe, dl);
+      const int64_t bskv = simt::shfl(b.skv, dl), bused = simt::shfl(b.used, dl), bpeak = simt::shfl(b.peak, dl);
+      const int64_t bct = simt::shfl(b.copy_tok, dl), bkv = simt::shfl(b.kvmin, dl);
+      const int32_t bmin = simt::shfl(b.minrem, dl), bdj = simt::shfl(b.dj, dl);
+      const bool bst = simt::shfl((int32_t)b.stepping, dl) != 0;
+      if ((lane & 1) && got) {
+        if (bst) { L_busy_until = be; L_job_start = bjs; L_busy_time = bbusy; L_link = blink; L_mirror_fin = bmfin;
+                   L_prev_end = bprev; L_skv = bskv; L_minrem = bmin; L_kvmin = bkv; L_dj = bdj; L_dG = bdG;
+                   L_de1 = bde1; L_dpe = bdpe; }
+        L_used = bused;
+        L_peak = bpeak;
+        L_copy_tok = bct;
       }
     }
-    {
-      const int64_t roomx = (PC.f.cap - get(L_used, x)) / B;
-      if (roomx < kmax) kmax = roomx;
-      const int64_t ev_room = PC.event_budget - n_events;
-      if (ev_room < kmax) kmax = ev_room;
-    }
-    if (kmax < 1) return;
-    const double mr = get(L_ni, x) > 0 ? get(L_min_ready, x) : kInf;
-    const int32_t xkey = 3 * 64 + x;
-    double e = get(L_busy_until, x);
-    const double e1 = e;
-    double js = get(L_job_start, x);
-    double busy = get(L_busy_time, x);
-    double link = acc ? get(L_link, x) : 0.0;
-    double mfin = acc ? get(L_mirror_fin, x) : 0.0;
-    const double pe_old = get(L_prev_end, x);
-    int64_t K = get(L_skv, x);
-    double prev = js, G = 0.0;
-    int64_t j = 0, tw = 0;
-    const double mlat = transfer_latency(PC.f, kmul((double)m, PC.f.kvb));
-    const double comp = kdiv(kmul(PC.f.two_p, (double)B), PC.f.pf_den);  // decode compute floor
-    const double kvb = PC.f.kvb, Wb = PC.f.W, mden = PC.f.mem_den;
-    const double now0 = now;
-    while (j < kmax) {
-      if (!(e < ht || (e == ht && xkey < hk))) break;
-      if (e >= mr) break;
-      // virtual step-end event at e ...
-      if constexpr (LOG) now = e;
-      if (js >= PC.warmup) busy = kadd(busy, ksub(e, js));
-      if (e >= PC.warmup) tw += B;
-      if (j >= 1) {
-        const double g = ksub(e, prev);
-        if (g > G) G = g;
-      }
-      if (m > 0) {
-        const double st = e > link ? e : link;
-        link = kadd(st, mlat);
-        mfin = link;
-        log(KVSIM_EV_TRANSFER, x, y, 1, m);
-      }
-      log(KVSIM_EV_STEP_END, x, B, 0, 0);
-      // ... and the next step started at its boundary
-      K += B;
-      log(KVSIM_EV_STEP_START, x, B, 0, K);
-      prev = e;
-      js = e;
-      e = kadd(e, kvsim_math::kmax(kdiv(kadd(Wb, kmul((double)K, kvb)), mden), comp));
-      ++j;
-    }
-    now = now0;
-    if (j == 0) return;
-    if (lane == 0) W->ct.n_steps += j;
-    n_events += j;
-    if (lane == 0) W->ct.tok_total += j * B;
-    if (lane == 0) W->ct.tok_window += tw;
-    if (lane == 0) W->ct.mir_tokens += j * m;
-    if (prev > t_last) t_last = prev;
-    if (own(x)) {
-      L_busy_time = busy;
-      L_job_start = js;
-      L_busy_until = e;
-      L_prev_end = prev;
-      L_skv = K;
-      L_minrem -= (int32_t)j;
-      L_used += j * B;
-      if (L_used > L_peak) L_peak = L_used;
-      if (acc) { L_link = link; L_mirror_fin = mfin; }
-    }
-    if (acc && m > 0 && own(y)) {
-      L_used += j * m;
-      L_copy_tok += j * m;
-      if (L_used > L_peak) L_peak = L_used;
-    }
-    // one pass over the batch: j tokens each, TBT max over the chained gaps
-    int32_t* rem_a = b_rem(x);
-    double* tbt_a = b_tbt(x);
-    for (int32_t q = lane; q < B; q += 32) {
-      const int32_t rf = rem_a[q];
-      double tb = tbt_a[q];
-      const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe_old;
-      double g1 = ksub(e1, last);
-      if (G > g1) g1 = G;
-      rem_a[q] = ((rf & kRemMask) - (int32_t)j) | (rf & kCopy);
-      if (g1 > tb) tbt_a[q] = g1;
+    if (steps > 0) {  // divergent: only lanes that advanced touch the counters
+      simt::atomic_add_smem(&W->ct.adv_events, steps);
+      simt::atomic_add_smem(&W->ct.n_steps, steps);
+      simt::atomic_add_smem(&W->ct.tok_total, tok);
+      simt::atomic_add_smem(&W->ct.tok_window, tw);
+      if (mir) simt::atomic_add_smem(&W->ct.mir_tokens, mir);
+      if (tmax > L_tlast) L_tlast = tmax;
     }
     simt::sync();
   }
-
-  // AcceLLM pair chaining: co-advance the step ends of both pair members in
-  // their merged (time, id) order while no boundary could act (completion,
-  // join, memory shortfall, rebalance move, switch) and before the next
-  // arrival. Other pairs only interact through arrivals.
-  struct Chain {
-    double e, js, busy, link, mfin, prev, G, e1, pe_old, mr, comp, mlat;
-    int64_t K, used, tw, lim_kv, i;
-    int32_t B, m, minrem, z;
-  };
-  KV_DEV void chain_init(Chain& c, int z, bool need_kvmin) {
-    c.z = z;
-    c.B = get(L_nb, z);
-    c.e = get(L_busy_until, z);
-    c.e1 = c.e;
-    c.js = get(L_job_start, z);
-    c.busy = get(L_busy_time, z);
-    c.link = get(L_link, z);
-    c.mfin = get(L_mirror_fin, z);
-    c.pe_old = get(L_prev_end, z);
-    c.prev = c.js;
-    c.G = 0.0;
-    c.K = get(L_skv, z);
-    c.used = get(L_used, z);
-    c.tw = 0;
-    c.i = 0;
-    c.m = get(L_ncopy, z);
-    c.minrem = get(L_minrem, z);
-    c.mr = get(L_ni, z) > 0 ? get(L_min_ready, z) : as_f64(0x7ff0000000000000ull);
-    // smallest kv among copy-holding members (rebalance candidates); only
-    // needed when z holds more requests than its partner
-    int64_t kvmin = INT64_MAX;
-    if (need_kvmin) {
-      for (int32_t q = lane; q < c.B; q += 32) {
-        const int32_t rf = b_rem(z)[q];
-        if (rf & kCopy) {
-          const int64_t kv = (int64_t)b_kvb(z)[q] - (rf & kRemMask);
-          if (kv < kvmin) kvmin = kv;
-        }
-      }
-      kvmin = simt::warp_min(kvmin);
-    }
-    c.lim_kv = kvmin;
-    c.comp = kdiv(kmul(PC.f.two_p, (double)c.B), PC.f.pf_den);
-    c.mlat = transfer_latency(PC.f, kmul((double)c.m, PC.f.kvb));
-  }
-  KV_DEV void chain_commit(Chain& c, int64_t used_partner_add) {
-    const int z = c.z;
-    if (c.i > 0) {
-      if (lane == 0) W->ct.n_steps += c.i;
-      n_events += c.i;
-      if (lane == 0) W->ct.tok_total += c.i * c.B;
-      if (lane == 0) W->ct.tok_window += c.tw;
-      if (lane == 0) W->ct.mir_tokens += c.i * c.m;
-      if (c.prev > t_last) t_last = c.prev;
-      if (own(z)) {
-        L_busy_time = c.busy;
-        L_job_start = c.js;
-        L_busy_until = c.e;
-        L_prev_end = c.prev;
-        L_skv = c.K;
-        L_minrem -= (int32_t)c.i;
-        L_link = c.link;
-        L_mirror_fin = c.mfin;
-      }
-      int32_t* rem_a = b_rem(z);
-      double* tbt_a = b_tbt(z);
-      for (int32_t q = lane; q < c.B; q += 32) {
-        const int32_t rf = rem_a[q];
-        const double tb = tbt_a[q];
-        const double last = (rf & kJoin) ? c_last()[b_rid(z)[q]] : c.pe_old;
-        double g1 = ksub(c.e1, last);
-        if (c.G > g1) g1 = c.G;
-        rem_a[q] = ((rf & kRemMask) - (int32_t)c.i) | (rf & kCopy);
-        if (g1 > tb) tbt_a[q] = g1;
-      }
-      simt::sync();
-    }
-    if (own(z)) {
-      L_used = c.used;
-      if (L_used > L_peak) L_peak = L_used;
-      L_copy_tok += used_partner_add;
-    }
-  }
-  struct ChainEnv {
-    double ht, warmup, W, kvb, mden;
-    int64_t loadx0, loady0, cx, cap, copy_add_x, copy_add_y, budget_left;
-    int32_t hk;
-    bool rb_ok;
-  };
-  // one chained step end of member c (o = its partner); false = stop chaining
-  KV_DEV bool chain_step(Chain& c, Chain& o, bool isA, ChainEnv& v) {
-    const int z = c.z;
-    if (c.B <= 0) return false;
-    if (!(c.e < v.ht || (c.e == v.ht && 3 * 64 + z < v.hk))) return false;
-    if (c.i + 1 >= c.minrem) return false;  // a member completes at this step end
-    if (c.e >= c.mr) return false;          // a join at this boundary
-    if (v.budget_left <= 0) return false;
-    if (v.rb_ok) {                           // rebalance at z's boundary after this step end
-      const int64_t cz = isA ? v.cx : -v.cx;
-      if (cz >= 1 && c.lim_kv != INT64_MAX) {
-        const int64_t lz = (isA ? v.loadx0 : v.loady0) + (c.i + 1) * c.B;
-        const int64_t lw = (isA ? v.loady0 : v.loadx0) + o.i * o.B;
-        const int64_t dz = lz - lw;
-        const int64_t lim = cz >= 2 ? dz : dz - 1;
-        if (c.lim_kv + c.i + 1 <= lim) return false;
-      }
-    }
-    // memory for z's next step start: B on z, m mirror lines on the partner
-    if (c.used + c.B > v.cap || o.used + c.m > v.cap) return false;
-    // ---- the virtual step end of z at c.e and its next step start
-    if constexpr (LOG) now = c.e;
-    if (c.js >= v.warmup) c.busy = kadd(c.busy, ksub(c.e, c.js));
-    if (c.e >= v.warmup) c.tw += c.B;
-    if (c.i >= 1) {
-      const double g = ksub(c.e, c.prev);
-      if (g > c.G) c.G = g;
-    }
-    if (c.m > 0) {
-      const double st = c.e > c.link ? c.e : c.link;
-      c.link = kadd(st, c.mlat);
-      c.mfin = c.link;
-      log(KVSIM_EV_TRANSFER, z, z ^ 1, 1, c.m);
-    }
-    log(KVSIM_EV_STEP_END, z, c.B, 0, 0);
-    c.K += c.B;
-    c.used += c.B;
-    o.used += c.m;
-    if (isA) v.copy_add_y += c.m; else v.copy_add_x += c.m;
-    log(KVSIM_EV_STEP_START, z, c.B, 0, c.K);
-    c.prev = c.e;
-    c.js = c.e;
-    c.e = kadd(c.e, kvsim_math::kmax(kdiv(kadd(v.W, kmul((double)c.K, v.kvb)), v.mden), c.comp));
-    c.i += 1;
-    v.budget_left -= 1;
-    return true;
-  }
-  KV_DEV_NOINLINE void fast_forward_pair(int x) {
-    const int y = x ^ 1;
-    if (get(Q_n, x >> 1) != 0 || get(L_pend, x) || get(L_pend, y)) return;
-    if (get(L_nb, x) <= 0 || get(L_minrem, x) < 2) return;
-    const double kInf = as_f64(0x7ff0000000000000ull);
-    double ht = has_next ? t_next : kInf;
-    int32_t hk = -1;
-    const int32_t jy = get(L_job, y);
-    const bool ystep = jy == JOB_STEP;
-    if (!ystep) {
-      double yt = kInf;
-      int32_t yk = 0;
-      if (jy == JOB_PREFILL) { yt = get(L_busy_until, y); yk = 2 * 64 + y; }
-      else if (get(L_role, y) == ROLE_DECODE && get(L_ni, y) > 0) { yt = get(L_min_ready, y); yk = 64 + y; }
-      if (yt < ht || (yt == ht && yk < hk)) { ht = yt; hk = yk; }
-    }
-    const bool rb_ok = get(L_role, y) == ROLE_DECODE;  // rebalances possible in this pair
-    const int64_t cx = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
-    Chain a, b;
-    chain_init(a, x, rb_ok && cx >= 1);
-    if (ystep) chain_init(b, y, rb_ok && -cx >= 1);
-    else {
-      b.z = y; b.B = 0; b.i = 0; b.e = kInf; b.m = 0; b.used = get(L_used, y); b.K = get(L_skv, y);
-      b.lim_kv = INT64_MAX; b.minrem = 0; b.mr = kInf;
-    }
-    ChainEnv env;
-    env.ht = ht; env.hk = hk; env.rb_ok = rb_ok;
-    env.loadx0 = load_of(x); env.loady0 = load_of(y);
-    env.cx = cx;
-    env.cap = PC.f.cap; env.warmup = PC.warmup;
-    env.W = PC.f.W; env.kvb = PC.f.kvb; env.mden = PC.f.mem_den;
-    env.copy_add_x = 0; env.copy_add_y = 0;
-    env.budget_left = PC.event_budget - n_events;
-    const double now0 = now;
-    for (;;) {
-      // next chained event: the earlier step end, ties to the lower id
-      const bool pickA = !(b.e < a.e || (b.e == a.e && y < x));
-      const bool ok = pickA ? chain_step(a, b, true, env) : chain_step(b, a, false, env);
-      if (!ok) break;
-    }
-    const int64_t copy_add_x = env.copy_add_x, copy_add_y = env.copy_add_y;
-    now = now0;
-    chain_commit(a, copy_add_x);
-    if (ystep) chain_commit(b, copy_add_y);
-    else if (own(y)) {
-      L_used = b.used;
-      if (L_used > L_peak) L_peak = L_used;
-      L_copy_tok += copy_add_y;
-    }
-  }
-
   // ------------------------------------------------------------- unified
   KV_DEV_NOINLINE void unified_start(int x, double t) {
+    EMU_COUNT(17);
     int32_t nb = get(L_nb, x);
     while (get(L_used, x) + nb > PC.f.cap) {
       preempt_newest(x);
@@ -1109,12 +1067,14 @@ struct Sim {
       L_job_s1 = s1;
     }
     log(KVSIM_EV_STEP_START, x, nb, k, K);
-    if (k == 0 && chain_steps) fast_forward(x, t);
+
   }
 
   KV_DEV_NOINLINE void unified_end(int x, double t) {
+    EMU_COUNT(18);
     account_job(x, t);
     if (lane == 0) W->ct.n_steps += 1;
+    flush(x);
     const StepOut o = step_loop(x, t);
     int32_t nb = o.nb_old - o.completed;
     int64_t skv = get(L_skv, x) - o.kv_done + nb;
@@ -1171,6 +1131,7 @@ struct Sim {
 
   // ------------------------------------------------------------ splitwise
   KV_DEV_NOINLINE void sw_try_start(double t) {
+    EMU_COUNT(19);
     for (int p = 0; p < n_prefill; ++p) {
       if (get(L_job, p) != JOB_NONE) continue;
       int32_t qn = get(Q_n, 0);
@@ -1219,6 +1180,7 @@ struct Sim {
   }
 
   KV_DEV_NOINLINE void sw_prefill_done(int p, double t) {
+    EMU_COUNT(20);
     account_job(p, t);
     if (lane == 0) W->ct.n_prefills += 1;
     const int32_t k = get(L_njob, p);
@@ -1303,6 +1265,8 @@ struct Sim {
   }
   // move every request whose primary is x and that holds a copy on x^1
   KV_DEV_NOINLINE void move_all_to_partner(int x, double t) {
+    EMU_COUNT(8);
+    flush(x);
     const int y = x ^ 1;
     const double mfin = get(L_mirror_fin, x);
     const double pend = get(L_prev_end, x);
@@ -1415,6 +1379,7 @@ struct Sim {
   }
 
   KV_DEV_NOINLINE void acc_start_job(int x, double t) {
+    EMU_COUNT(13);
     const int q = x >> 1;
     const int32_t h = get(Q_head, q);
     int32_t k = 0;
@@ -1468,6 +1433,7 @@ struct Sim {
   }
 
   KV_DEV_NOINLINE bool try_switch(int x, double t) {
+    EMU_COUNT(12);
     if (!head_admissible(x)) return false;
     if (own(x)) L_pend = 0;
     move_all_to_partner(x, t);
@@ -1477,7 +1443,12 @@ struct Sim {
     return true;
   }
 
-  KV_DEV_NOINLINE void ensure_prefill(int q, double t) {
+  KV_DEV void ensure_prefill(int q, double t) {
+    if (get(Q_n, q) == 0) return;
+    ensure_prefill_slow(q, t);
+  }
+  KV_DEV_NOINLINE void ensure_prefill_slow(int q, double t) {
+    EMU_COUNT(11);
     if (get(Q_n, q) == 0) return;
     const int a = 2 * q, b = a + 1;
     if (get(L_role, a) == ROLE_PREFILL || get(L_role, b) == ROLE_PREFILL || get(L_pend, a) || get(L_pend, b))
@@ -1488,7 +1459,17 @@ struct Sim {
   }
 
   // rebalance_pair at x's boundary (SEMANTICS §6)
-  KV_DEV_NOINLINE void rebalance(int x, double t) {
+  KV_DEV void rebalance(int x, double t) {
+    const int y = x ^ 1;
+    if (get(L_role, y) != ROLE_DECODE || get(L_pend, y)) return;
+    const int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
+    if (c < 1) return;
+    if (load_of(x) - load_of(y) < 1) return;
+    rebalance_slow(x, t);
+  }
+  KV_DEV_NOINLINE void rebalance_slow(int x, double t) {
+    EMU_COUNT(6);
+    flush(x);
     const int y = x ^ 1;
     if (get(L_role, y) != ROLE_DECODE || get(L_pend, y)) return;
     int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
@@ -1521,6 +1502,7 @@ struct Sim {
   }
   // move batch slot idx of x to y's incoming (zero-byte label swap)
   KV_DEV_NOINLINE void move_one(int x, int32_t idx, double t) {
+    EMU_COUNT(7);
     const int y = x ^ 1;
     const int32_t rid = b_rid(x)[idx];
     const int32_t rf = b_rem(x)[idx];
@@ -1550,6 +1532,7 @@ struct Sim {
   }
 
   KV_DEV_NOINLINE void acc_boundary(int x, double t) {
+    EMU_COUNT(9);
     join(x, t);
     if (get(L_pend, x)) {
       if (own(x)) L_pend = 0;
@@ -1562,6 +1545,8 @@ struct Sim {
   }
 
   KV_DEV_NOINLINE void acc_prefill_done(int x, double t) {
+    EMU_COUNT(10);
+    flush(x);
     account_job(x, t);
     if (lane == 0) W->ct.n_prefills += 1;
     const int y = x ^ 1;
@@ -1653,7 +1638,7 @@ struct Sim {
     // pass 3: survivors join x's batch as joiners (last token = t)
     const int32_t nb = get(L_nb, x);
     int32_t add = 0, addc = 0, minrem = 0x7fffffff;
-    int64_t kvadd = 0;
+    int64_t kvadd = 0, kvmin = INT64_MAX;
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
       const int32_t i = i0 + lane;
       const bool act = i < k;
@@ -1675,12 +1660,14 @@ struct Sim {
         b_tbt(x)[pos] = c_tbt()[rid];
         kvadd += (int64_t)pl + em - 1;
         if (dl - em < minrem) minrem = dl - em;
+        if (hasc && (int64_t)pl + em - 1 < kvmin) kvmin = (int64_t)pl + em - 1;
       }
       addc += simt::popc(simt::ballot(surv && c_cpy()[surv ? rid : 0] == y));
       add += simt::popc(sm);
     }
     kvadd = simt::warp_sum(kvadd);
     minrem = simt::warp_min(minrem);
+    kvmin = simt::warp_min(kvmin);
     simt::sync();
     if (own(x)) {
       L_nb += add;
@@ -1688,6 +1675,7 @@ struct Sim {
       L_ncopy += addc;
       L_njob = 0;
       if (minrem < L_minrem) L_minrem = minrem;
+      if (kvmin < L_kvmin) L_kvmin = kvmin;
     }
     if (head_admissible(x)) {
       move_all_to_partner(x, t);
@@ -1701,6 +1689,7 @@ struct Sim {
 
   // -------------------------------------------------------------- arrival
   KV_DEV_NOINLINE void arrive(double t) {
+    EMU_COUNT(16);
     const int64_t rid64 = next_rid;
     const int32_t rid = (int32_t)rid64;
     int32_t pl, dl;
@@ -1777,8 +1766,9 @@ struct Sim {
       bool is_arrival = false;
       if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
       if (!is_arrival && ck == (1 << 20)) break;
-      if (++n_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
+      if (++n_events + W->ct.adv_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
       if (lane == 0) W->ct.n_loop += 1;
+      unsigned drive = 0xffffffffu;
       if (is_arrival) {
         now = t_next;
         if (now > t_last) t_last = now;
@@ -1788,6 +1778,7 @@ struct Sim {
         now = t;
         if (now > t_last) t_last = now;
         const int kind = ck >> 6, x = ck & 63;
+        if (!(POL == KVSIM_POLICY_SPLITWISE && kind == 2)) drive = 1u << x;
         if (kind == 1) {
           log(KVSIM_EV_WAKE, x, 0, 0, 0);
           if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(x, t);
@@ -1806,6 +1797,7 @@ struct Sim {
         }
       }
       if (policy == KVSIM_POLICY_SPLITWISE) sw_try_start(now);
+      if (chain_steps) advance(drive);
     }
     simt::sync();
   }
@@ -1860,8 +1852,12 @@ struct Sim {
     s.n_requests = status == KVSIM_OK ? N : 0;
     if (status == KVSIM_OK || status == KVSIM_E_EVENT_BUDGET) {
       s.n_requests = N;
+      {
+        const double tl = simt::warp_max(lane < n ? L_tlast : 0.0);
+        if (tl > t_last) t_last = tl;
+      }
       const Counters ct = W->ct;
-      s.n_events = n_events; s.n_steps = ct.n_steps; s.n_prefills = ct.n_prefills; s.n_moves = ct.n_moves;
+      s.n_events = n_events + ct.adv_events; s.n_steps = ct.n_steps; s.n_prefills = ct.n_prefills; s.n_moves = ct.n_moves;
       s.n_preemptions = ct.n_preempt; s.n_evictions = ct.n_evict;
       s.tokens_total = ct.tok_total; s.tokens_window = ct.tok_window;
       s.link_prefill_tokens = ct.pf_tokens; s.link_mirror_tokens = ct.mir_tokens;
@@ -1976,7 +1972,7 @@ struct Sim {
     simt::sync();
     if (lane == 0) {
       A->out[point] = s;
-      if (A->ev_count != nullptr) A->ev_count[point] = ev_n;
+      if (A->ev_count != nullptr) A->ev_count[point] = W->ct.ev_n;
     }
     simt::sync();
   }

@@ -161,3 +161,32 @@ def test_curves(kvsim, tmp_path):  # host perfmodel only
     assert abs(float(dec[1]["latency_s"]) - 0.01046) < 1e-5 and abs(float(dec[32]["tokens_per_s"]) - 2952) < 1
     pre = [r for r in rows if r["phase"] == "prefill"]
     assert math.isclose(float(pre[0]["tokens_per_s"]), float(pre[1]["tokens_per_s"]), rel_tol=1e-12)
+
+
+@pytest.mark.gpu
+def test_resource_sweep_knees_and_failed_points(kvsim, tmp_path):
+    cfg = {"policies": ["accellm", "splitwise_static"], "rate": 6, "instances": 4, "num_requests": 600,
+           "workload": "mixed", "resource": {"kind": "hbm_capacity", "values": [30e9, 40e9, 60e9, 80e9, 120e9]}}
+    o = tmp_path / "o"
+    r = run(kvsim, "resource-sweep", "--config", write(tmp_path, "c.json", cfg), "--out", str(o))
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.DictReader(open(o / "resource_sweep.csv")))
+    assert len(rows) == 10
+    # 4 x 30 GB x 0.9 < 140 GB of weights: per-point error, sweep continues
+    assert all(int(x["status"]) == -2 for x in rows if float(x["hbm_capacity"]) == 30e9)
+    assert all(int(x["status"]) == 0 for x in rows if float(x["hbm_capacity"]) >= 60e9)
+    knees = json.load(open(o / "report.json"))["knees"]
+    assert {k["policy"] for k in knees} == {"accellm", "splitwise_static"}
+    assert all(k["knee"] is not None and k["knee"] >= 40e9 for k in knees)
+
+
+@pytest.mark.gpu
+def test_sweep_compare_table(kvsim, tmp_path):
+    cfg = {"policies": ["accellm", "unified"], "rates": [4, 8], "instances": 4, "num_requests": 300, "seed": 2}
+    o = tmp_path / "o"
+    assert run(kvsim, "sweep", "--config", write(tmp_path, "c.json", cfg), "--out", str(o)).returncode == 0
+    cmp = json.load(open(o / "report.json"))["compare"]
+    assert len(cmp) == 2
+    for g in cmp:
+        assert g["ratios_vs_accellm"]["accellm"]["cost_eff"] == 1.0
+        assert len(g["trace_fingerprint"]) == 16
