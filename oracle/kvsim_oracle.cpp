@@ -13,6 +13,8 @@
 #include "kvsim_oracle.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -24,6 +26,8 @@
 namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
+// SPEC.md:254-259,469 invariant checking after every event (tests only)
+std::atomic<int> g_check_invariants{0};
 constexpr double kNaN = std::numeric_limits<double>::quiet_NaN();
 
 // ---------------------------------------------------------------- RNG (§2)
@@ -218,6 +222,10 @@ struct Sim {
 
   // token emission at time t (first token, recompute token or decode token)
   void emit(Req& r, double t) {
+    if (g_check_invariants && r.emitted > 0 && !(t > r.last_t)) {
+      if (getenv("KVO_DEBUG")) fprintf(stderr, "time order t=%.17g last=%.17g\n", t, r.last_t);
+      status = KVSIM_E_INTERNAL;  // token_times strictly increasing
+    }
     if (r.emitted == 0) r.first_t = t;
     else { double gap = t - r.last_t; if (gap > r.tbt_max) r.tbt_max = gap; }
     r.last_t = t;
@@ -761,7 +769,47 @@ struct Sim {
           break;
       }
       if (policy == KVSIM_POLICY_SPLITWISE) sw_try_start(t);
+      if (g_check_invariants && !invariants_hold()) { status = KVSIM_E_INTERNAL; break; }
+      if (status == KVSIM_E_INTERNAL) break;
     }
+  }
+
+  // Ledger exactness and memory safety: every instance's
+  // `used` equals the tokens its primaries, copies and transient prefill
+  // reservations hold, and never exceeds capacity; redundant copies live on
+  // the partner only (AcceLLM); emitted <= decode_len.
+  bool invariants_hold() const {
+    std::vector<int64_t> sum((size_t)n, 0);
+    std::vector<char> in_job((size_t)next_arrival, 0);
+    for (int x = 0; x < n; ++x)
+      for (int rid : I[x].job_reqs) in_job[rid] = 1;
+    for (int64_t i = 0; i < next_arrival; ++i) {
+      const Req& r = R[i];
+      if (r.emitted > r.decode) return false;
+      if (r.done || r.primary < 0 || in_job[i]) continue;  // job members: reserved below
+      sum[r.primary] += r.held();
+      if (r.copy >= 0) {
+        if (policy != KVSIM_POLICY_ACCELLM || r.copy != (r.primary ^ 1)) return false;
+        sum[r.copy] += r.held();
+      }
+    }
+    for (int x = 0; x < n; ++x) {
+      const Inst& X = I[x];
+      for (int rid : X.job_reqs) {
+        const Req& r = R[rid];
+        if (policy == KVSIM_POLICY_SPLITWISE) { sum[r.primary] += r.qlen; }
+        else sum[x] += r.qlen;
+      }
+      if (policy == KVSIM_POLICY_SPLITWISE && X.job != NONE && x < n_prefill) sum[x] += X.job_s1;
+    }
+    for (int x = 0; x < n; ++x) {
+      if (sum[x] != I[x].used) {
+        if (getenv("KVO_DEBUG")) fprintf(stderr, "ledger x=%d sum=%lld used=%lld t=%.9g policy=%d\n", x, (long long)sum[x], (long long)I[x].used, now, policy);
+        return false;
+      }
+      if (I[x].used > f.cap || I[x].used < 0) return false;
+    }
+    return true;
   }
 };
 
@@ -883,6 +931,7 @@ void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
 extern "C" {
 
 uint64_t kvo_rng_draw(uint64_t seed, int64_t i, int stream) { return draw(seed, i, stream); }
+void kvo_set_invariant_checks(int on) { g_check_invariants = on; }
 double kvo_klog(double x) { return klog(x); }
 double kvo_kv_bytes_per_token(const kvsim_point_desc* p) { return make_perf(*p).kvb; }
 double kvo_weight_bytes(const kvsim_point_desc* p) { return make_perf(*p).W; }

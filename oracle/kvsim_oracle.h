@@ -22,6 +22,9 @@ extern "C" {
 #endif
 
 uint64_t kvo_rng_draw(uint64_t seed, int64_t i, int stream);
+/* enable per-event invariant checking; violations
+ * return KVSIM_E_INTERNAL */
+void kvo_set_invariant_checks(int on);
 double kvo_klog(double x);
 /* perfmodel (perfmodel.hpp:76-106) in sum form */
 double kvo_kv_bytes_per_token(const kvsim_point_desc* p);

@@ -1,0 +1,110 @@
+"""Oracle properties from the reference's invariant lists: workload generator
+statistics, the portable log, and the randomized invariant
+suite of acceptance criterion #11 (memory safety, ledger
+exactness, token-time monotonicity, conservation, determinism) over
+randomized small configurations, half of them memory-starved."""
+import ctypes as C
+import math
+import struct
+
+import numpy as np
+import pytest
+
+from configs import random_small
+from harness import oracle, run_oracle
+from paper_2411_05555_b200.abi import make_point
+
+
+def gen(p, cap):
+    L = oracle()
+    a = (C.c_double * cap)()
+    pr = (C.c_int32 * cap)()
+    de = (C.c_int32 * cap)()
+    n = L.kvo_gen_trace(C.byref(p), a, pr, de, cap)
+    return np.frombuffer(a, dtype=np.float64)[:n].copy(), np.frombuffer(pr, dtype=np.int32)[:n].copy(), \
+        np.frombuffer(de, dtype=np.int32)[:n].copy()
+
+
+def test_lengths_uniform_and_in_range():
+    p = make_point(workload="mixed", rate=8.0, num_requests=100000, seed=5)
+    _, pr, de = gen(p, 100000)
+    for x in (pr, de):
+        assert x.min() >= 20 and x.max() <= 1000
+        assert abs(x.mean() - 510.0) < 0.01 * 510               # exact uniform mean of 20..1000
+        counts = np.bincount(x - 20, minlength=981)
+        exp = len(x) / 981
+        chi2 = ((counts - exp) ** 2 / exp).sum()
+        assert chi2 < 981 + 5 * math.sqrt(2 * 981)              # ~5 sigma of chi2(980)
+
+
+def test_mixed_preset_mean_prompt():  # rate 8, duration 1000 s -> mean within 5% of 500
+    p = make_point(workload="mixed", rate=8.0, num_requests=20000, duration_s=1000.0, seed=9)
+    arr, pr, _ = gen(p, 20000)
+    assert len(arr) >= 7600 and arr.max() < 1000.0
+    assert 475 <= pr.mean() <= 525
+
+
+def test_poisson_gaps():  # mean gap within 5% of 1/rate over >= 1e4 arrivals
+    for rate in (0.5, 3.0, 40.0):
+        p = make_point(rate=rate, num_requests=20000, seed=1)
+        arr, _, _ = gen(p, 20000)
+        gaps = np.diff(np.concatenate([[0.0], arr]))
+        assert np.all(gaps >= 0) and np.all(np.diff(arr) >= 0)
+        assert abs(gaps.mean() * rate - 1.0) < 0.05
+        assert abs(gaps.std() * rate - 1.0) < 0.05               # exponential: sd = mean
+
+
+def test_rate_zero_and_fixed_interval():
+    assert len(gen(make_point(rate=0.0, num_requests=10), 10)[0]) == 0
+    arr, _, _ = gen(make_point(rate=4.0, num_requests=9, arrival="fixed"), 9)
+    assert list(arr) == [i / 4.0 for i in range(9)]
+
+
+def test_generator_deterministic():
+    p = make_point(rate=3.0, num_requests=5000, seed=77)
+    a1, p1, d1 = gen(p, 5000)
+    a2, p2, d2 = gen(p, 5000)
+    assert a1.tobytes() == a2.tobytes() and p1.tobytes() == p2.tobytes() and d1.tobytes() == d2.tobytes()
+    q = make_point(rate=3.0, num_requests=5000, seed=78)
+    assert gen(q, 5000)[0].tobytes() != a1.tobytes()
+
+
+def ulp_diff(a, b):
+    ia = struct.unpack("<q", struct.pack("<d", a))[0]
+    ib = struct.unpack("<q", struct.pack("<d", b))[0]
+    return abs(ia - ib)
+
+
+def test_portable_log_accuracy():
+    L = oracle()
+    rng = np.random.default_rng(3)
+    xs = list(rng.random(200000) + 1e-300) + [1.0, 0.5, 2.0 ** -53, 1 - 2.0 ** -53, 0.75, 1e-10]
+    worst = max(ulp_diff(L.kvo_klog(float(x)), math.log(x)) for x in xs)
+    assert worst <= 1
+    assert L.kvo_klog(1.0) == 0.0
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_randomized_invariant_suite(chunk):  # SPEC.md:469 acceptance #11
+    L = oracle()
+    L.kvo_set_invariant_checks(1)
+    try:
+        for i in range(chunk * 50, chunk * 50 + 50):
+            p = random_small(i, max_req=50)
+            r = run_oracle(p, ev_cap=0)
+            s = r.summary
+            assert r.status == 0, (i, r.status)                     # ledger / memory safety / time order
+            assert s.n_completed == s.n_requests                    # every request completes
+            assert s.tokens_total == sum(x.decode_len for x in r.recs)   # conservation
+            for x in r.recs:
+                assert x.first_token_s >= x.arrival_s and x.completion_s >= x.first_token_s
+                if x.decode_len == 1:
+                    assert x.completion_s == x.first_token_s and x.tbt_max_s == 0.0
+            if p.policy != 2:
+                assert s.n_moves == 0 and s.link_mirror_tokens == 0
+            if p.policy == 0:
+                assert s.link_prefill_tokens == 0                   # unified never uses links
+            again = run_oracle(p, ev_cap=0)
+            assert bytes(again.summary) == bytes(s)                 # determinism
+    finally:
+        L.kvo_set_invariant_checks(0)
