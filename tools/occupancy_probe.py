@@ -1,0 +1,14 @@
+"""Config-4 sweep wall time per KVSIM_MINB variant (exploratory; run as
+`KVSIM_MINB=k python tools/occupancy_probe.py`)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2411_05555_b200 as pkg
+from bench import config4_points
+rates = int(sys.argv[1]) if len(sys.argv) > 1 else 833
+nreq = int(sys.argv[2]) if len(sys.argv) > 2 else 10000
+pts = config4_points(0, rates, nreq)
+sim = pkg.KvSim(0)
+sim.run(pts[:16])
+t0 = time.time(); s = sim.run(pts); dt = time.time() - t0
+reqs = sum(x.n_requests for x in s)
+print(f"MINB={os.environ.get('KVSIM_MINB','2')} pts={len(pts)} wall={dt:.3f}s req/s={reqs/dt:.4e} bad={sum(x.status!=0 for x in s)}", flush=True)
