@@ -204,6 +204,8 @@ struct Sim {
 
   template <class T>
   KV_DEV T get(T v, int x) { return simt::shfl(v, x); }
+  // warp min of event times (non-negative or +inf; bit order == value order)
+  static KV_DEV double warp_min_time(double t) { return as_f64(simt::warp_min_u64(as_u64(t))); }
   KV_DEV bool own(int x) const { return lane == x; }
   KV_DEV int queue_of(int x) const {
     return policy == KVSIM_POLICY_UNIFIED ? x : policy == KVSIM_POLICY_SPLITWISE ? 0 : (x >> 1);
@@ -465,10 +467,10 @@ struct Sim {
     o.completed = completed;
     o.m_copies = m;
     o.copy_done = copy_done;
-    o.kv_done = simt::warp_sum(kv_done);
-    o.copy_free = simt::warp_sum(copy_free);
-    o.minrem = simt::warp_min(minrem);
-    o.kvmin = simt::warp_min(kvmin);
+    o.kv_done = simt::warp_sum_nn(kv_done);
+    o.copy_free = simt::warp_sum_nn(copy_free);
+    o.minrem = simt::warp_min_i32(minrem);
+    o.kvmin = simt::warp_min_i64(kvmin);
     simt::sync();
     return o;
   }
@@ -523,10 +525,10 @@ struct Sim {
       keep += simt::popc(sm);
       add += simt::popc(gm);
     }
-    kvsum = simt::warp_sum(kvsum);
-    mn = simt::warp_min(mn);
-    minrem = simt::warp_min(minrem);
-    kvmin = simt::warp_min(kvmin);
+    kvsum = simt::warp_sum_nn(kvsum);
+    mn = warp_min_time(mn);
+    minrem = simt::warp_min_i32(minrem);
+    kvmin = simt::warp_min_i64(kvmin);
     simt::sync();
     if (own(x)) {
       if (minrem < L_minrem) L_minrem = minrem;
@@ -603,7 +605,7 @@ struct Sim {
         if (k > best) { best = k; bidx = j; bwhere = 2; }
       }
     }
-    const uint64_t wbest = simt::warp_max(best);
+    const uint64_t wbest = simt::warp_max_u64(best);
     Found r;
     r.where = 0; r.idx = -1; r.rid = -1; r.kv = 0;
     if (wbest == 0) return r;
@@ -642,7 +644,7 @@ struct Sim {
       const int32_t r = b_rid(x)[j];
       if (r > best) { best = r; bidx = j; }
     }
-    const int32_t rid = simt::warp_max(best);
+    const int32_t rid = simt::warp_max_i32(best);
     const int src = simt::ffs(simt::ballot(best == rid)) - 1;
     const int32_t idx = simt::shfl(bidx, src);
     const int32_t rf = b_rem(x)[idx];
@@ -897,12 +899,9 @@ struct Sim {
         if (simt::ballot(lane >= n_prefill && lane < n && L_final > PC.f.cap) != 0) return;
       }
       double pt = (lane < n_prefill && L_job != JOB_NONE) ? L_busy_until : kInf;
-      int32_t pk = 2 * 64 + lane;
-      for (int mm = 16; mm; mm >>= 1) {
-        const double ot = simt::shfl_xor(pt, mm);
-        const int32_t ok = simt::shfl_xor(pk, mm);
-        if (ot < pt || (ot == pt && ok < pk)) { pt = ot; pk = ok; }
-      }
+      uint32_t pku = 2 * 64 + lane;
+      simt::warp_min_tk(pt, pku);
+      const int32_t pk = (int32_t)pku;
       if (pt < ht || (pt == ht && pk < hk)) { ht = pt; hk = pk; }
     }
     const int64_t cap = PC.f.cap;
@@ -1099,7 +1098,7 @@ struct Sim {
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
       if (lane < take) j_rid(x)[k + lane] = rid;
       const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
-      const int64_t tsq = simt::warp_sum(lane < take ? len * len : (int64_t)0);
+      const int64_t tsq = simt::warp_sum_nn(lane < take ? len * len : (int64_t)0);
       s1 += tsum;
       s2 += tsq;
       used += tsum;
@@ -1164,9 +1163,9 @@ struct Sim {
       add += simt::popc(jm);
       completed += simt::popc(simt::ballot(done));
     }
-    kvadd = simt::warp_sum(kvadd);
-    kvfree = simt::warp_sum(kvfree);
-    minrem = simt::warp_min(minrem);
+    kvadd = simt::warp_sum_nn(kvadd);
+    kvfree = simt::warp_sum_nn(kvfree);
+    minrem = simt::warp_min_i32(minrem);
     simt::sync();
     count_tokens(k, t);
     if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
@@ -1207,7 +1206,7 @@ struct Sim {
           if (k > 0 && s1 + len > PC.budget) { stop = true; break; }
           // destination: decode instance with most free tokens, ties lowest id
           int64_t fr = (lane >= n_prefill && lane < n) ? PC.f.cap - L_used : INT64_MIN;
-          const int64_t best = simt::warp_max(fr);
+          const int64_t best = simt::warp_max_i64(fr);
           const int d = simt::ffs(simt::ballot(fr == best)) - 1;
           if (best < len) { stop = true; break; }
           add_used(d, len);
@@ -1367,7 +1366,7 @@ struct Sim {
       moved += simt::popc(mm);
     }
     const int32_t moved_b = moved;
-    const int64_t kv_b = simt::warp_sum(kv_moved);
+    const int64_t kv_b = simt::warp_sum_nn(kv_moved);
     kv_moved = 0;
     // incoming entries of x that hold a copy on y
     const int32_t ni = get(L_ni, x);
@@ -1403,15 +1402,15 @@ struct Sim {
       ikeep += simt::popc(sm);
       moved += simt::popc(mm);
     }
-    const int64_t kv_i = simt::warp_sum(kv_moved);
-    mn = simt::warp_min(mn);
+    const int64_t kv_i = simt::warp_sum_nn(kv_moved);
+    mn = warp_min_time(mn);
     // min ready of what stays in x's incoming
     double mx = as_f64(0x7ff0000000000000ull);
     for (int32_t j = lane; j < ikeep; j += 32) {
       const double r = i_ready(x)[j];
       if (r < mx) mx = r;
     }
-    mx = simt::warp_min(mx);
+    mx = warp_min_time(mx);
     simt::sync();
     const int64_t kv_all = kv_b + kv_i;
     if (lane == 0) ws()->ct.n_moves += moved;
@@ -1455,7 +1454,7 @@ struct Sim {
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
       if (lane < take) j_rid(x)[k + lane] = rid;
       const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
-      const int64_t tsq = simt::warp_sum(lane < take ? len * len : (int64_t)0);
+      const int64_t tsq = simt::warp_sum_nn(lane < take ? len * len : (int64_t)0);
       s1 += tsum;
       s2 += tsq;
       k += take;
@@ -1544,7 +1543,7 @@ struct Sim {
           }
         }
       }
-      const uint64_t wb = simt::warp_max(best);
+      const uint64_t wb = simt::warp_max_u64(best);
       if (wb == 0) break;
       const int src = simt::ffs(simt::ballot(best == wb)) - 1;
       const int32_t idx = simt::shfl(bidx, src);
@@ -1625,7 +1624,7 @@ struct Sim {
       }
       completed += simt::popc(simt::ballot(done));
     }
-    kvfree = simt::warp_sum(kvfree);
+    kvfree = simt::warp_sum_nn(kvfree);
     simt::sync();
     if (own(x)) L_used -= kvfree;
     count_tokens(k, t);
@@ -1680,7 +1679,7 @@ struct Sim {
       }
       if (cp) c_cpy()[rid] = y;
       else if (surv) c_cpy()[rid] = -1;
-      s1c += simt::warp_sum(cp ? kv : (int64_t)0);
+      s1c += simt::warp_sum_nn(cp ? kv : (int64_t)0);
       ncopy += simt::popc(simt::ballot(cp));
     }
     simt::sync();
@@ -1719,9 +1718,9 @@ struct Sim {
       addc += simt::popc(simt::ballot(surv && c_cpy()[surv ? rid : 0] == y));
       add += simt::popc(sm);
     }
-    kvadd = simt::warp_sum(kvadd);
-    minrem = simt::warp_min(minrem);
-    kvmin = simt::warp_min(kvmin);
+    kvadd = simt::warp_sum_nn(kvadd);
+    minrem = simt::warp_min_i32(minrem);
+    kvmin = simt::warp_min_i64(kvmin);
     simt::sync();
     if (own(x)) {
       L_nb += add;
@@ -1776,7 +1775,7 @@ struct Sim {
     gen_next();
     if (policy == KVSIM_POLICY_UNIFIED) {
       const int64_t fr = lane < n ? PC.f.cap - L_used - Q_tok : INT64_MIN;
-      const int64_t best = simt::warp_max(fr);
+      const int64_t best = simt::warp_max_i64(fr);
       const int x = simt::ffs(simt::ballot(fr == best)) - 1;
       log(KVSIM_EV_ARRIVE, x, rid, pl, 0);
       q_push_back(x, rid, pl);
@@ -1789,7 +1788,7 @@ struct Sim {
       const int64_t ua = simt::shfl(L_used, (2 * lane) & 31);
       const int64_t ub = simt::shfl(L_used, (2 * lane + 1) & 31);
       const int64_t fr = lane < np ? (PC.f.cap - ua) + (PC.f.cap - ub) - Q_tok : INT64_MIN;
-      const int64_t best = simt::warp_max(fr);
+      const int64_t best = simt::warp_max_i64(fr);
       const int q = simt::ffs(simt::ballot(fr == best)) - 1;
       log(KVSIM_EV_ARRIVE, q, rid, pl, 0);
       q_push_back(q, rid, pl);
@@ -1802,21 +1801,18 @@ struct Sim {
     const double kInf = as_f64(0x7ff0000000000000ull);
     for (;;) {
       double ct = kInf;
-      int32_t ck = 1 << 20;
+      uint32_t cku = 1u << 20;
       if (lane < n) {
         if (L_job != JOB_NONE) {
           ct = L_busy_until;
-          ck = (L_job == JOB_PREFILL ? 2 : 3) * 64 + lane;
+          cku = (L_job == JOB_PREFILL ? 2 : 3) * 64 + lane;
         } else if (L_role == ROLE_DECODE && L_ni > 0) {
           ct = L_min_ready;
-          ck = 1 * 64 + lane;
+          cku = 1 * 64 + lane;
         }
       }
-      for (int m = 16; m; m >>= 1) {
-        const double ot = simt::shfl_xor(ct, m);
-        const int32_t ok = simt::shfl_xor(ck, m);
-        if (ot < ct || (ot == ct && ok < ck)) { ct = ot; ck = ok; }
-      }
+      simt::warp_min_tk(ct, cku);
+      const int32_t ck = (int32_t)cku;
       bool is_arrival = false;
       if (has_next && (t_next < ct || (t_next == ct))) is_arrival = true;
       if (!is_arrival && ck == (1 << 20)) break;

@@ -156,6 +156,79 @@ __device__ __forceinline__ double floor_d(double x) { return floor(x); }
 #endif
 
 namespace simt {
+// 32-bit unsigned warp reductions: one REDUX instruction on sm_100a
+#if defined(KVSIM_EMU)
+inline uint32_t reduce_min_u32(uint32_t v) {
+  for (int m = 16; m; m >>= 1) { uint32_t o = shfl_xor(v, m); v = o < v ? o : v; }
+  return v;
+}
+inline uint32_t reduce_max_u32(uint32_t v) {
+  for (int m = 16; m; m >>= 1) { uint32_t o = shfl_xor(v, m); v = o > v ? o : v; }
+  return v;
+}
+inline uint32_t reduce_add_u32(uint32_t v) {
+  for (int m = 16; m; m >>= 1) v += shfl_xor(v, m);
+  return v;
+}
+#else
+__device__ __forceinline__ uint32_t reduce_min_u32(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t reduce_max_u32(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t reduce_add_u32(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+#endif
+// lexicographic warp min of (t, k) for t >= 0 (IEEE bit order == numeric
+// order for non-negative doubles, +inf included): three REDUX instead of
+// five shuffle rounds of (double, int)
+KV_DEV void warp_min_tk(double& t, uint32_t& k) {
+  uint64_t b;
+#if defined(KVSIM_EMU)
+  __builtin_memcpy(&b, &t, 8);
+#else
+  b = (uint64_t)__double_as_longlong(t);
+#endif
+  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+  const uint32_t mh = reduce_min_u32(hi);
+  const uint32_t ml = reduce_min_u32(hi == mh ? lo : 0xffffffffu);
+  const uint32_t mk = reduce_min_u32(hi == mh && lo == ml ? k : 0xffffffffu);
+  b = ((uint64_t)mh << 32) | ml;
+#if defined(KVSIM_EMU)
+  __builtin_memcpy(&t, &b, 8);
+#else
+  t = __longlong_as_double((long long)b);
+#endif
+  k = mk;
+}
+// 64-bit unsigned min / max: REDUX on the high words, then on the low words
+// of the lanes holding the extreme high word
+KV_DEV uint64_t warp_min_u64(uint64_t v) {
+  const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = reduce_min_u32(hi);
+  const uint32_t ml = reduce_min_u32(hi == mh ? lo : 0xffffffffu);
+  return ((uint64_t)mh << 32) | ml;
+}
+KV_DEV uint64_t warp_max_u64(uint64_t v) {
+  const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = reduce_max_u32(hi);
+  const uint32_t ml = reduce_max_u32(hi == mh ? lo : 0u);
+  return ((uint64_t)mh << 32) | ml;
+}
+// signed variants: flipping the sign bit maps int order onto unsigned order
+KV_DEV int64_t warp_min_i64(int64_t v) {
+  return (int64_t)(warp_min_u64((uint64_t)v ^ 0x8000000000000000ull) ^ 0x8000000000000000ull);
+}
+KV_DEV int64_t warp_max_i64(int64_t v) {
+  return (int64_t)(warp_max_u64((uint64_t)v ^ 0x8000000000000000ull) ^ 0x8000000000000000ull);
+}
+KV_DEV int32_t warp_min_i32(int32_t v) { return (int32_t)(reduce_min_u32((uint32_t)v ^ 0x80000000u) ^ 0x80000000u); }
+KV_DEV int32_t warp_max_i32(int32_t v) { return (int32_t)(reduce_max_u32((uint32_t)v ^ 0x80000000u) ^ 0x80000000u); }
+// exact sum of non-negative int64 lanes: one REDUX when every lane is below
+// 2^26 (the 32-lane total then fits 31 bits), shuffle tree otherwise
+template <class T>
+KV_DEV T warp_sum(T v);
+KV_DEV int64_t warp_sum_nn(int64_t v) {
+  if (ballot((uint64_t)v >= (1ull << 26)) == 0) return (int64_t)reduce_add_u32((uint32_t)v);
+  return warp_sum(v);
+}
+KV_DEV int32_t warp_sum_i32(int32_t v) { return (int32_t)reduce_add_u32((uint32_t)v); }
 // ---------------------------------------------------------- warp reductions
 template <class T>
 KV_DEV T warp_sum(T v) {

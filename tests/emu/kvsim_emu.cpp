@@ -82,3 +82,10 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
   std::free(base);
   return KVSIM_OK;
 }
+
+#if defined(KVSIM_EMU_PROFILE)
+// call counts of the kernel's handlers (EMU_COUNT sites), for event-mix studies
+extern "C" void kvemu_prof(long long* out) {
+  for (int i = 0; i < 32; ++i) out[i] = kvsim_dev::emu_prof[i];
+}
+#endif
