@@ -261,6 +261,12 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   int bps = 1;
   KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
   c->blocks_per_sm = bps > 0 ? bps : 1;
+  // resident blocks per SM actually used (<= the occupancy limit): fewer
+  // co-resident warps thrash the instruction cache less
+  if (const char* e = std::getenv("KVSIM_BLOCKS_PER_SM")) {
+    const int want = std::atoi(e);
+    if (want >= 1 && want < c->blocks_per_sm) c->blocks_per_sm = want;
+  }
   KV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   *out = c;
   return KVSIM_OK;
