@@ -91,9 +91,21 @@ typedef struct kvsim_point_desc {
   uint64_t seed;
   int64_t num_requests;         /* max requests generated (P10) */
   uint64_t user_tag;            /* opaque, echoed */
-  int32_t reserved_i[8];
-  double reserved_d[7];
+  /* AcceLLM extensions driven by the policy timer (
+   * PAPER.md:309,457; docs/SEMANTICS.md §6b). Zero = off / default. */
+  int32_t accellm_flags;        /* bit 0 degraded mode, bit 1 inter-pair leveling */
+  int32_t degraded_trigger_ticks;   /* 0 => 3 consecutive timer ticks */
+  int32_t reserved_i[6];
+  double policy_timer_s;        /* 0 => 1.0 s timer period */
+  double leveling_link_fraction;/* 0 => 0.10 of link capacity per timer period */
+  double degraded_redundancy;   /* 0 => 0.5: enter when copies < this x live */
+  double degraded_exit_fill;    /* 0 => 0.5: leave when group KV <= this x capacity */
+  double dual_copy_fraction;    /* 0 => 1/3: dual instance's copy budget per decoder */
+  double reserved_d[2];
 } kvsim_point_desc;
+
+#define KVSIM_ACCELLM_DEGRADED 1
+#define KVSIM_ACCELLM_LEVELING 2
 
 /* Caller-supplied trace (load_trace). */
 typedef struct kvsim_trace_view {
@@ -118,7 +130,10 @@ typedef struct kvsim_point_summary {
   double cost_eff, idle_frac, peak_kv_gb, link_prefill_gb, link_mirror_gb;
   double busy_s_total;
   uint64_t user_tag;
-  int64_t reserved[4];
+  int64_t link_leveling_tokens; /* KV moved by inter-pair leveling */
+  int64_t n_timer_ticks;        /* policy timer events */
+  int64_t n_mode_switches;      /* degraded-mode entries + exits */
+  int64_t reserved[1];
 } kvsim_point_summary;
 
 /* Per-request record (parity configs). ttft = first_token_s - arrival_s,
@@ -143,7 +158,10 @@ enum kvsim_event_kind {
   KVSIM_EV_TRANSFER = 10,     /* inst=src, a=dst, b=kind (0 prefill,1 mirror), c=tokens */
   KVSIM_EV_WAKE = 11,         /* inst */
   KVSIM_EV_JOIN = 12,         /* inst, a=n joined */
-  KVSIM_EV_COPY = 13          /* inst=holder, a=n copies created */
+  KVSIM_EV_COPY = 13,         /* inst=holder, a=n copies created */
+  KVSIM_EV_TIMER = 14,        /* inst=-1, a=tick index */
+  KVSIM_EV_LEVEL = 15,        /* inst=from, a=rid, b=to, c=kv tokens moved */
+  KVSIM_EV_MODE = 16          /* inst=group, a=1 enter degraded / 0 leave */
 };
 typedef struct kvsim_event_record {
   double t;

@@ -186,6 +186,18 @@ struct Sim {
   int64_t n_events = 0, n_steps = 0, n_prefills = 0, n_moves = 0, n_preempt = 0, n_evict = 0;
   int64_t tokens_total = 0, tokens_window = 0, prefill_tokens = 0, mirror_tokens = 0;
   double now = 0;
+  // AcceLLM timer-driven extensions (SEMANTICS §6b): degraded mode
+  // and inter-pair leveling (
+  // PAPER.md:309). partner[x] = holder of the copies of x's primaries
+  // (x^1 normally; the dual instance for a degraded group's decoders; -1 for
+  // the dual instance itself).
+  bool ext = false, deg_on = false, lvl_on = false;
+  double timer_P = 1.0, red_thr = 0.5, exit_fill = 0.5, lvl_frac = 0.10, dual_frac = 1.0 / 3.0;
+  int trig = 3;
+  int64_t tick = 1;
+  std::vector<int> partner, gmode, gcnt, lvl_dst;
+  std::vector<int64_t> lvl_budget;
+  int64_t level_tokens = 0, n_ticks = 0, n_modes = 0;
   // event log
   kvsim_event_record* ev;
   int64_t ev_cap, ev_n = 0;
@@ -203,7 +215,29 @@ struct Sim {
       for (int i = 0; i < n_prefill; ++i) I[i].role = PREFILL;
     } else Q.resize(n / 2);
     qtokens.assign(Q.size(), 0);
+    if (policy == KVSIM_POLICY_ACCELLM && (p.accellm_flags & 3)) {
+      ext = true;
+      deg_on = (p.accellm_flags & KVSIM_ACCELLM_DEGRADED) != 0;
+      lvl_on = (p.accellm_flags & KVSIM_ACCELLM_LEVELING) != 0;
+      if (p.policy_timer_s > 0) timer_P = p.policy_timer_s;
+      if (p.degraded_redundancy > 0) red_thr = p.degraded_redundancy;
+      if (p.degraded_exit_fill > 0) exit_fill = p.degraded_exit_fill;
+      if (p.leveling_link_fraction > 0) lvl_frac = p.leveling_link_fraction;
+      if (p.dual_copy_fraction > 0) dual_frac = p.dual_copy_fraction;
+      if (p.degraded_trigger_ticks > 0) trig = p.degraded_trigger_ticks;
+    }
+    partner.resize(n);
+    for (int x = 0; x < n; ++x) partner[x] = x ^ 1;
+    gmode.assign((size_t)(n / 4) + 1, 0);
+    gcnt.assign((size_t)(n / 4) + 1, 0);
+    lvl_dst.assign(n, -1);
+    lvl_budget.assign(n, 0);
   }
+  // degraded-mode helpers: group of pair q (valid iff q/2 < n/4), the queue a
+  // pair's requests wait in (a degraded group shares its first pair's queue)
+  bool degraded_pair(int q) const { return ext && (q >> 1) < n / 4 && gmode[q >> 1]; }
+  int qid(int q) const { return degraded_pair(q) ? (q & ~1) : q; }
+  bool is_dual(int x) const { return degraded_pair(x >> 1) && (x & 3) == 0; }
 
   void log(int kind, int inst, int a, int b, int64_t c) {
     if (ev && ev_n < ev_cap) ev[ev_n] = kvsim_event_record{now, kind, inst, a, b, c};
@@ -214,7 +248,7 @@ struct Sim {
     if (I[i].used > I[i].peak) I[i].peak = I[i].used;
   }
   int queue_of(int i) const {
-    return policy == KVSIM_POLICY_UNIFIED ? i : policy == KVSIM_POLICY_SPLITWISE ? 0 : i / 2;
+    return policy == KVSIM_POLICY_UNIFIED ? i : policy == KVSIM_POLICY_SPLITWISE ? 0 : qid(i / 2);
   }
   void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; }
   void push_front(int q, int rid) { Q[q].push_front(rid); qtokens[q] += R[rid].qlen; }
@@ -250,15 +284,18 @@ struct Sim {
   // largest copy held on instance x: candidates are requests whose primary is
   // the partner (batch + incoming). Returns rid or -1.
   int largest_copy_on(int x) {
-    int y = x ^ 1;
     int best = -1;
     auto consider = [&](int rid) {
       const Req& r = R[rid];
       if (r.copy != x) return;
       if (best < 0 || r.kv() > R[best].kv() || (r.kv() == R[best].kv() && rid < best)) best = rid;
     };
-    for (int rid : I[y].batch) consider(rid);
-    for (auto& in : I[y].incoming) consider(in.rid);
+    // clients of x: instances whose copies x holds (partner relation)
+    for (int y = 0; y < n; ++y) {
+      if (y == x || partner[y] != x) continue;
+      for (int rid : I[y].batch) consider(rid);
+      for (auto& in : I[y].incoming) consider(in.rid);
+    }
     return best;
   }
   void evict_copy(int rid) {
@@ -325,12 +362,12 @@ struct Sim {
       else { preempt_newest(x); preempted = true; if (X.batch.empty()) break; }
     }
     if (X.batch.empty()) {
-      if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(x / 2, t);
+      if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(qid(x / 2), t);
       return;
     }
     int64_t m = 0;
-    if (policy == KVSIM_POLICY_ACCELLM) {
-      int y = x ^ 1;
+    if (policy == KVSIM_POLICY_ACCELLM && partner[x] >= 0) {
+      int y = partner[x];
       for (;;) {
         m = 0;
         for (int rid : X.batch) if (R[rid].copy == y) ++m;
@@ -347,7 +384,7 @@ struct Sim {
     X.job_start = t;
     X.busy_until = t + decode_lat(f, B, K);
     log(KVSIM_EV_STEP_START, x, (int)B, 0, K);
-    if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(x / 2, t);
+    if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(qid(x / 2), t);
   }
 
   void step_end(int x, double t) {
@@ -355,9 +392,9 @@ struct Sim {
     account_job(X, t);
     ++n_steps;
     X.job = NONE;
-    int y = x ^ 1;
+    int y = policy == KVSIM_POLICY_ACCELLM ? partner[x] : -1;
     int64_t m = 0;
-    if (policy == KVSIM_POLICY_ACCELLM)
+    if (y >= 0)
       for (int rid : X.batch) if (R[rid].copy == y) ++m;
     std::vector<int> keep;
     int completed = 0;
@@ -514,13 +551,15 @@ struct Sim {
   }
   // head of the pair queue admissible on x after evicting every copy on x?
   bool head_admissible(int x) {
-    int q = x / 2;
+    int q = qid(x / 2);
     if (Q[q].empty()) return false;
     int64_t len = R[Q[q].front()].qlen;
     int64_t copies = 0;
-    int y = x ^ 1;
-    for (int rid : I[y].batch) if (R[rid].copy == x) copies += R[rid].held();
-    for (auto& in : I[y].incoming) if (R[in.rid].copy == x) copies += R[in.rid].held();
+    for (int y = 0; y < n; ++y) {
+      if (y == x || partner[y] != x) continue;
+      for (int rid : I[y].batch) if (R[rid].copy == x) copies += R[rid].held();
+      for (auto& in : I[y].incoming) if (R[in.rid].copy == x) copies += R[in.rid].held();
+    }
     return I[x].used - copies + len <= f.cap;
   }
   void move_req(int rid, int from, int to, double t) {
@@ -537,7 +576,8 @@ struct Sim {
   // move every request with primary x that holds a copy on the partner
   void move_all_to_partner(int x, double t) {
     Inst& X = I[x];
-    int y = x ^ 1;
+    int y = partner[x];
+    if (y < 0) return;  // a degraded group's dual instance holds no movable requests
     std::vector<int> keep;
     for (int rid : X.batch) {
       if (R[rid].copy == y) move_req(rid, x, y, t);
@@ -555,7 +595,7 @@ struct Sim {
   }
   void acc_start_job(int x, double t) {
     Inst& X = I[x];
-    int q = x / 2;
+    int q = qid(x / 2);
     X.job_reqs.clear();
     int64_t s1 = 0, s2 = 0;
     while (!Q[q].empty()) {
@@ -593,6 +633,13 @@ struct Sim {
   }
   void ensure_prefill(int q, double t) {
     if (Q[q].empty()) return;
+    if (degraded_pair(q)) {  // the dual instance is the group's only prefill instance
+      int d = 4 * (q >> 1);
+      if (I[d].role == PREFILL || I[d].switch_pending) return;
+      if (I[d].job == NONE) try_switch(d, t);
+      else I[d].switch_pending = true;
+      return;
+    }
     int a = 2 * q, b = a + 1;
     if (I[a].role == PREFILL || I[b].role == PREFILL || I[a].switch_pending || I[b].switch_pending) return;
     int m = load_of(b) < load_of(a) ? b : a;
@@ -600,6 +647,7 @@ struct Sim {
     else I[m].switch_pending = true;
   }
   void rebalance(int x, double t) {
+    if (ext && degraded_pair(x / 2)) { if (!is_dual(x)) dual_push(x, t); return; }
     int y = x ^ 1;
     Inst& X = I[x];
     Inst& Y = I[y];
@@ -639,8 +687,9 @@ struct Sim {
       X.switch_pending = false;
       if (try_switch(x, t)) return;
     }
-    ensure_prefill(x / 2, t);
+    ensure_prefill(qid(x / 2), t);
     if (X.role == PREFILL) return;  // ensure_prefill switched x
+    if (lvl_dst[x] >= 0) level_from(x, t);
     rebalance(x, t);
     step_start(x, t);
   }
@@ -662,6 +711,15 @@ struct Sim {
       } else survivors.push_back(rid);
     }
     log(KVSIM_EV_PREFILL_DONE, x, (int)X.job_reqs.size(), completed, 0);
+    if (is_dual(x)) {
+      dual_handoff(x, survivors, t);
+      X.job_reqs.clear();
+      if (head_admissible(x)) { acc_start_job(x, t); return; }
+      X.role = DECODE;
+      log(KVSIM_EV_ROLE, x, DECODE, 0, 0);
+      acc_boundary(x, t);
+      return;
+    }
     int64_t s1c = 0;
     int ncopy = 0;
     for (int rid : survivors) {
@@ -690,6 +748,239 @@ struct Sim {
     acc_boundary(x, t);
   }
 
+  // ------------------------------------------- degraded mode (SEMANTICS §6b)
+  // tokens of decoder x's requests that the dual instance d holds as copies
+  int64_t dual_copy_tokens(int d, int x) const {
+    int64_t s = 0;
+    for (int rid : I[x].batch) if (R[rid].copy == d) s += R[rid].held();
+    for (auto& in : I[x].incoming) if (R[in.rid].copy == d) s += R[in.rid].held();
+    return s;
+  }
+  // prefill survivors of the dual instance d go to the decoder with the most
+  // free tokens (full KV transfer, one per destination); d keeps its
+  // computed KV as the redundant copy while that decoder's copy budget
+  // (dual_copy_fraction x capacity) allows ("retains about
+  // one-third of the KV caches of each decoding instance").
+  void dual_handoff(int d, const std::vector<int>& survivors, double t) {
+    Inst& D = I[d];
+    const int64_t budget = (int64_t)(dual_frac * (double)f.cap);
+    int64_t ct[3];
+    for (int k = 0; k < 3; ++k) ct[k] = dual_copy_tokens(d, d + 1 + k);
+    int64_t per_dst[3] = {0, 0, 0}, s1c = 0;
+    int ncopy = 0;
+    std::vector<int> stay;
+    for (int rid : survivors) {
+      Req& r = R[rid];
+      const int64_t kv = r.kv();
+      int best = -1;
+      int64_t bf = 0;
+      for (int k = 0; k < 3; ++k) {
+        int64_t fr = f.cap - I[d + 1 + k].used;
+        if (best < 0 || fr > bf) { best = k; bf = fr; }
+      }
+      if (bf < kv) { stay.push_back(rid); continue; }  // no decoder has room: decodes on d
+      const int xk = d + 1 + best;
+      bump(xk, kv);
+      r.primary = xk;
+      per_dst[best] += kv;
+      if (ct[best] + kv <= budget) {
+        r.copy = d;
+        r.fresh_at = t;
+        ct[best] += kv;
+        s1c += kv;
+        ++ncopy;
+      } else {
+        r.copy = -1;
+        D.used -= kv;
+      }
+    }
+    if (ncopy) log(KVSIM_EV_COPY, d, ncopy, 1, s1c);
+    for (int k = 0; k < 3; ++k) {
+      if (per_dst[k] == 0) continue;
+      const int xk = d + 1 + k;
+      double fin = prefill_transfer(d, xk, per_dst[k], D.job_start, t);
+      for (int rid : survivors)
+        if (R[rid].primary == xk) I[xk].incoming.push_back({rid, fin});
+    }
+    for (int rid : stay) D.batch.push_back(rid);
+  }
+  // at decoder x's boundary: hand requests whose copy the dual instance holds
+  // over to it (zero bytes; x drops its KV, "overwrite") while
+  // no prefill is pending, with rebalance_pair's greedy
+  void dual_push(int x, double t) {
+    const int d = x & ~3;
+    Inst& X = I[x];
+    Inst& D = I[d];
+    if (D.role != DECODE || D.switch_pending || !Q[qid(x / 2)].empty()) return;
+    int64_t c = (int64_t)X.batch.size() + (int64_t)X.incoming.size() - (int64_t)D.batch.size() -
+                (int64_t)D.incoming.size();
+    int64_t dd = load_of(x) - load_of(d);
+    std::vector<int> cand;
+    for (int rid : X.batch) if (R[rid].copy == d) cand.push_back(rid);
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+      if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
+      return a < b;
+    });
+    std::vector<int> moved;
+    for (int rid : cand) {
+      int64_t k = R[rid].kv();
+      int64_t v = std::max<int64_t>(0, std::llabs(c) - 1), Dv = std::llabs(dd);
+      int64_t c2 = c - 2, d2 = dd - 2 * k;
+      int64_t v2 = std::max<int64_t>(0, std::llabs(c2) - 1), D2 = std::llabs(d2);
+      if (v2 <= v && D2 <= Dv && (v2 < v || D2 < Dv)) { moved.push_back(rid); c = c2; dd = d2; }
+    }
+    if (moved.empty()) return;
+    std::vector<int> keep;
+    for (int rid : X.batch)
+      if (std::find(moved.begin(), moved.end(), rid) == moved.end()) keep.push_back(rid);
+    X.batch.swap(keep);
+    for (int rid : moved) {
+      Req& r = R[rid];
+      double ready = r.fresh_at > t ? r.fresh_at : t;
+      X.used -= r.held();
+      r.primary = d;
+      r.copy = -1;
+      r.n_moves += 1;
+      ++n_moves;
+      D.incoming.push_back({rid, ready});
+      log(KVSIM_EV_MOVE, x, rid, d, 0);
+    }
+  }
+  // evict the copies instance h holds for the instances in [lo, hi]
+  void evict_copies_from(int h, int lo, int hi) {
+    for (;;) {
+      int best = -1;
+      for (int y = lo; y <= hi; ++y) {
+        if (y == h) continue;
+        auto consider = [&](int rid) {
+          const Req& r = R[rid];
+          if (r.copy != h) return;
+          if (best < 0 || r.kv() > R[best].kv() || (r.kv() == R[best].kv() && rid < best)) best = rid;
+        };
+        for (int rid : I[y].batch) consider(rid);
+        for (auto& in : I[y].incoming) consider(in.rid);
+      }
+      if (best < 0) return;
+      evict_copy(best);
+    }
+  }
+  void enter_degraded(int g, double t) {
+    const int a = 4 * g;
+    // the decoders overwrite the redundant copies they hold
+    for (int h = a + 1; h <= a + 3; ++h) evict_copies_from(h, a, a + 3);
+    partner[a] = -1;
+    for (int h = a + 1; h <= a + 3; ++h) partner[h] = a;
+    gmode[g] = 1;
+    ++n_modes;
+    while (!Q[2 * g + 1].empty()) push_back(2 * g, pop_front(2 * g + 1));
+    log(KVSIM_EV_MODE, g, 1, 0, 0);
+    ensure_prefill(2 * g, t);
+  }
+  void leave_degraded(int g, double t) {
+    const int a = 4 * g;
+    evict_copies_from(a, a + 2, a + 3);  // pairs are restored: copies live on partners only
+    for (int h = a; h <= a + 3; ++h) partner[h] = h ^ 1;
+    gmode[g] = 0;
+    ++n_modes;
+    log(KVSIM_EV_MODE, g, 0, 0, 0);
+    ensure_prefill(2 * g, t);
+    ensure_prefill(2 * g + 1, t);
+  }
+  // ------------------------------------- inter-pair leveling (SEMANTICS §6b)
+  int64_t pair_load(int q) const { return load_of(2 * q) + load_of(2 * q + 1); }
+  void schedule_leveling() {
+    int A = -1, B = -1;
+    int64_t la = 0, lb = 0;
+    for (int q = 0; q < n / 2; ++q) {
+      if (degraded_pair(q) || !Q[q].empty()) continue;
+      const Inst &u = I[2 * q], &v = I[2 * q + 1];
+      if (u.role != DECODE || v.role != DECODE || u.switch_pending || v.switch_pending) continue;
+      const int64_t l = pair_load(q);
+      if (A < 0 || l > la) { A = q; la = l; }
+      if (B < 0 || l < lb) { B = q; lb = l; }
+    }
+    if (A < 0 || A == B || la - lb < 2) return;
+    const int x = load_of(2 * A + 1) > load_of(2 * A) ? 2 * A + 1 : 2 * A;
+    const int y = (f.cap - I[2 * B + 1].used) > (f.cap - I[2 * B].used) ? 2 * B + 1 : 2 * B;
+    lvl_dst[x] = y;
+    lvl_budget[x] = (int64_t)std::floor(((lvl_frac * f.link_bw) * timer_P) / f.kvb);
+  }
+  // at x's boundary: migrate batch members (largest first) to the lighter
+  // pair while each move strictly narrows the pair-load gap, within the
+  // per-period link budget and the destination's memory
+  void level_from(int x, double t) {
+    const int y = lvl_dst[x];
+    int64_t bud = lvl_budget[x];
+    lvl_dst[x] = -1;
+    Inst& X = I[x];
+    Inst& Y = I[y];
+    if (Y.role != DECODE || Y.switch_pending || degraded_pair(x / 2) || degraded_pair(y / 2)) return;
+    int64_t d = pair_load(x / 2) - pair_load(y / 2);
+    std::vector<int> cand(X.batch.begin(), X.batch.end());
+    std::sort(cand.begin(), cand.end(), [&](int a, int b) {
+      if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
+      return a < b;
+    });
+    std::vector<int> moved;
+    for (int rid : cand) {
+      const int64_t k = R[rid].kv();
+      if (!(k < d) || k > bud || Y.used + k > f.cap) continue;
+      moved.push_back(rid);
+      bump(y, k);
+      d -= 2 * k;
+      bud -= k;
+    }
+    if (moved.empty()) return;
+    std::vector<int> keep;
+    for (int rid : X.batch)
+      if (std::find(moved.begin(), moved.end(), rid) == moved.end()) keep.push_back(rid);
+    X.batch.swap(keep);
+    for (int rid : moved) {
+      Req& r = R[rid];
+      const int64_t k = r.kv();
+      X.used -= k;
+      if (r.copy >= 0) I[r.copy].used -= k;
+      r.copy = -1;
+      r.primary = y;
+      double& busy = link_busy[(size_t)x * n + y];
+      double start = t > busy ? t : busy;
+      double fin = start + transfer_lat(f, (double)k * f.kvb);
+      busy = fin;
+      level_tokens += k;
+      r.n_moves += 1;
+      ++n_moves;
+      Y.incoming.push_back({rid, fin});
+      log(KVSIM_EV_LEVEL, x, rid, y, k);
+    }
+  }
+  void on_timer(double t) {
+    ++n_ticks;
+    log(KVSIM_EV_TIMER, -1, (int)(tick - 1), 0, 0);
+    if (deg_on) {
+      for (int g = 0; g < n / 4; ++g) {
+        const int a = 4 * g;
+        bool pf = false;
+        for (int h = a; h <= a + 3; ++h) pf = pf || I[h].role == PREFILL || I[h].switch_pending;
+        if (!gmode[g]) {
+          int64_t live = 0, red = 0;
+          for (int h = a; h <= a + 3; ++h) {
+            live += (int64_t)I[h].batch.size() + (int64_t)I[h].incoming.size();
+            for (int rid : I[h].batch) if (R[rid].copy >= 0) ++red;
+            for (auto& in : I[h].incoming) if (R[in.rid].copy >= 0) ++red;
+          }
+          gcnt[g] = (live > 0 && (double)red < red_thr * (double)live) ? gcnt[g] + 1 : 0;
+          if (gcnt[g] >= trig && !pf) { gcnt[g] = 0; enter_degraded(g, t); }
+        } else {
+          int64_t u = 0;
+          for (int h = a; h <= a + 3; ++h) u += I[h].used;
+          gcnt[g] = ((double)u <= exit_fill * (4.0 * (double)f.cap)) ? gcnt[g] + 1 : 0;
+          if (gcnt[g] >= trig && !pf) { gcnt[g] = 0; leave_degraded(g, t); }
+        }
+      }
+    }
+    if (lvl_on) schedule_leveling();
+  }
+
   // ---------------------------------------------------------------- arrival
   void arrive(int rid, double t) {
     Req& r = R[rid];
@@ -708,11 +999,19 @@ struct Sim {
       log(KVSIM_EV_ARRIVE, 0, rid, r.prompt, 0);
       push_back(0, rid);
     } else {
-      int best = 0;
+      int best = -1;
       int64_t bf = 0;
       for (int q = 0; q < n / 2; ++q) {
-        int64_t fr = (f.cap - I[2 * q].used) + (f.cap - I[2 * q + 1].used) - qtokens[q];
-        if (q == 0 || fr > bf) { best = q; bf = fr; }
+        int64_t fr;
+        if (degraded_pair(q)) {  // a degraded group is one routing unit (its first pair's queue)
+          if (q & 1) continue;
+          fr = 0;
+          for (int h = 2 * q; h < 2 * q + 4; ++h) fr += f.cap - I[h].used;
+          fr -= qtokens[q];
+        } else {
+          fr = (f.cap - I[2 * q].used) + (f.cap - I[2 * q + 1].used) - qtokens[q];
+        }
+        if (best < 0 || fr > bf) { best = q; bf = fr; }
       }
       log(KVSIM_EV_ARRIVE, best, rid, r.prompt, 0);
       push_back(best, rid);
@@ -742,6 +1041,17 @@ struct Sim {
         }
       }
       if (bk == 9) break;
+      if (ext) {  // policy timer: kind 4, after every other kind at equal time
+        const double tt = (double)tick * timer_P;
+        if (tt < bt) {
+          if (++n_events > budget_events) { status = KVSIM_E_EVENT_BUDGET; break; }
+          now = tt;
+          ++tick;
+          on_timer(tt);
+          if (g_check_invariants && !invariants_hold()) { status = KVSIM_E_INTERNAL; break; }
+          continue;
+        }
+      }
       if (++n_events > budget_events) { status = KVSIM_E_EVENT_BUDGET; break; }
       now = bt;
       double t = bt;
@@ -789,7 +1099,7 @@ struct Sim {
       if (r.done || r.primary < 0 || in_job[i]) continue;  // job members: reserved below
       sum[r.primary] += r.held();
       if (r.copy >= 0) {
-        if (policy != KVSIM_POLICY_ACCELLM || r.copy != (r.primary ^ 1)) return false;
+        if (policy != KVSIM_POLICY_ACCELLM || r.copy != partner[r.primary]) return false;
         sum[r.copy] += r.held();
       }
     }
@@ -865,6 +1175,9 @@ void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
   out->tokens_window = S.tokens_window;
   out->link_prefill_tokens = S.prefill_tokens;
   out->link_mirror_tokens = S.mirror_tokens;
+  out->link_leveling_tokens = S.level_tokens;
+  out->n_timer_ticks = S.n_ticks;
+  out->n_mode_switches = S.n_modes;
   out->makespan_s = S.now;
   int64_t peak = 0;
   double busy = 0;

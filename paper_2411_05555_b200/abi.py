@@ -42,7 +42,11 @@ class PointDesc(C.Structure):
         ("arrival_process", C.c_int32), ("trace_index", C.c_int32),
         ("rate", C.c_double), ("duration_s", C.c_double), ("warmup_s", C.c_double),
         ("seed", C.c_uint64), ("num_requests", C.c_int64), ("user_tag", C.c_uint64),
-        ("reserved_i", C.c_int32 * 8), ("reserved_d", C.c_double * 7),
+        ("accellm_flags", C.c_int32), ("degraded_trigger_ticks", C.c_int32),
+        ("reserved_i", C.c_int32 * 6),
+        ("policy_timer_s", C.c_double), ("leveling_link_fraction", C.c_double),
+        ("degraded_redundancy", C.c_double), ("degraded_exit_fill", C.c_double),
+        ("dual_copy_fraction", C.c_double), ("reserved_d", C.c_double * 2),
     ]
 
 
@@ -74,7 +78,9 @@ class PointSummary(C.Structure):
         ("link_prefill_gb", C.c_double), ("link_mirror_gb", C.c_double),
         ("busy_s_total", C.c_double),
         ("user_tag", C.c_uint64),
-        ("reserved", C.c_int64 * 4),
+        ("link_leveling_tokens", C.c_int64), ("n_timer_ticks", C.c_int64),
+        ("n_mode_switches", C.c_int64),
+        ("reserved", C.c_int64 * 1),
     ]
 
 
@@ -126,7 +132,9 @@ def make_point(*, model="llama2-70b", device="h100", policy="accellm", instances
                arrival="poisson", eff=(0.5, 0.8, 0.8), link="striped",
                num_devices=4, reserve=0.10, warmup_s=0.0, duration_s=math.inf,
                prefill_budget=8192, num_prefill=0, prompt=None, decode=None,
-               trace_index=-1, user_tag=0) -> PointDesc:
+               trace_index=-1, user_tag=0, degraded=False, leveling=False, timer_s=0.0,
+               trigger_ticks=0, leveling_fraction=0.0, degraded_redundancy=0.0,
+               degraded_exit_fill=0.0, dual_copy_fraction=0.0) -> PointDesc:
     p = PointDesc()
     (p.param_count, p.num_layers, p.hidden_dim, p.num_kv_heads, p.head_dim,
      p.bytes_per_value) = MODELS[model] if isinstance(model, str) else model
@@ -157,6 +165,14 @@ def make_point(*, model="llama2-70b", device="h100", policy="accellm", instances
     p.seed = seed
     p.num_requests = num_requests
     p.user_tag = user_tag
+    # AcceLLM timer-driven extensions (docs/SEMANTICS.md §6b); 0 = default
+    p.accellm_flags = (1 if degraded else 0) | (2 if leveling else 0)
+    p.degraded_trigger_ticks = trigger_ticks
+    p.policy_timer_s = timer_s
+    p.leveling_link_fraction = leveling_fraction
+    p.degraded_redundancy = degraded_redundancy
+    p.degraded_exit_fill = degraded_exit_fill
+    p.dual_copy_fraction = dual_copy_fraction
     return p
 
 

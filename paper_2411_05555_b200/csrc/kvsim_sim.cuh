@@ -52,12 +52,17 @@ struct PointConst {
   const double* tr_arr;
   const int32_t *tr_pl, *tr_dl;
   int32_t pmin, pmax, dmin, dmax, fixed_arrivals;
+  // AcceLLM timer-driven extensions (SEMANTICS §6b)
+  double timer_P, red_thr, exit_fill;
+  int64_t lvl_budget, dual_budget;
+  int32_t deg_on, lvl_on, trig;
 };
 struct Counters {
   int64_t n_steps, n_prefills, n_moves, n_preempt, n_evict;
   int64_t tok_total, tok_window, pf_tokens, mir_tokens, n_loop;
   int64_t ev_n;  // event-log cursor (atomic; lanes log concurrently)
   int64_t adv_events;  // virtual step ends processed by advance() (lane atomics)
+  int64_t lvl_tokens, n_ticks, n_modes;
 };
 struct WarpScratch {
   PointConst pc;  // written by lane 0 at point start, read (broadcast) by all
@@ -106,7 +111,11 @@ struct SweepArgs {
 #define PC (ws()->pc)
 // One specialisation per policy: every `policy == ...` test folds at compile
 // time, so a warp only ever executes (and caches) its own policy's code.
-template <int POL, bool LOG>
+// EXT: AcceLLM with the policy timer (degraded mode / inter-pair leveling,
+// SEMANTICS §6b): copies live on the instance partner[x] names (x^1, or the
+// dual instance of a degraded group), all links use the directed-link matrix,
+// and step chaining is off (plain event loop).
+template <int POL, bool LOG, bool EXT = false>
 struct Sim {
   const SweepArgs* A;  // kernel parameters (param space; __grid_constant__)
   WarpScratch* W;      // per-warp shared scratch: point constants, counters
@@ -123,7 +132,7 @@ struct Sim {
   int64_t n_events;
   double now;     // time of the event being processed (event-log timestamps)
   double t_last;  // latest event time processed (makespan)
-  static constexpr bool chain_steps = true;  // exact step chaining (advance); off = plain event loop
+  static constexpr bool chain_steps = !EXT;  // exact step chaining (advance); off = plain event loop
   static constexpr bool logging = LOG;  // event log compiled in (parity runs) or out (sweeps)
   int32_t status;
   // lane-owned instance state (lane x <-> instance x)
@@ -140,6 +149,12 @@ struct Sim {
   // lane-owned queue state (lane q <-> queue q)
   int32_t Q_head, Q_n;
   int64_t Q_tok;
+  // EXT: copy holder of this instance's primaries (-1 none), pending leveling
+  // migration (destination, token budget); lane g owns degraded group g
+  int32_t L_partner, L_lvl_dst;
+  int64_t L_lvl_bud;
+  int32_t G_mode, G_cnt;
+  int64_t tick;
 
   // per-slot arena offsets, computed once (the accessors below run on every
   // arena access; recomputing slot * capacity from the parameter block each
@@ -207,8 +222,21 @@ struct Sim {
   // warp min of event times (non-negative or +inf; bit order == value order)
   static KV_DEV double warp_min_time(double t) { return as_f64(simt::warp_min_u64(as_u64(t))); }
   KV_DEV bool own(int x) const { return lane == x; }
-  KV_DEV int queue_of(int x) const {
-    return policy == KVSIM_POLICY_UNIFIED ? x : policy == KVSIM_POLICY_SPLITWISE ? 0 : (x >> 1);
+  // copy holder of x's primaries: the pair partner, or (EXT) partner[x]
+  KV_DEV int partner_of(int x) {
+    if constexpr (EXT) return get(L_partner, x);
+    return x ^ 1;
+  }
+  // EXT degraded groups: pair q belongs to group q>>1 (if q>>1 < n/4); a
+  // degraded group's requests wait in its first pair's queue
+  KV_DEV bool degraded_pair(int q) {
+    if constexpr (!EXT) return false;
+    return (q >> 1) < (n >> 2) && get(G_mode, q >> 1) != 0;
+  }
+  KV_DEV int qid(int q) { return degraded_pair(q) ? (q & ~1) : q; }
+  KV_DEV bool is_dual(int x) { return (x & 3) == 0 && degraded_pair(x >> 1); }
+  KV_DEV int queue_of(int x) {
+    return policy == KVSIM_POLICY_UNIFIED ? x : policy == KVSIM_POLICY_SPLITWISE ? 0 : qid(x >> 1);
   }
   KV_DEV void add_used(int x, int64_t tok) {
     if (own(x)) {
@@ -290,6 +318,18 @@ struct Sim {
     pc.duration = d.duration_s;
     pc.rate = d.rate;
     pc.key = stream_key(d.seed);
+    pc.deg_on = EXT && (d.accellm_flags & KVSIM_ACCELLM_DEGRADED) != 0;
+    pc.lvl_on = EXT && (d.accellm_flags & KVSIM_ACCELLM_LEVELING) != 0;
+    pc.timer_P = d.policy_timer_s > 0.0 ? d.policy_timer_s : 1.0;
+    pc.red_thr = d.degraded_redundancy > 0.0 ? d.degraded_redundancy : 0.5;
+    pc.exit_fill = d.degraded_exit_fill > 0.0 ? d.degraded_exit_fill : 0.5;
+    pc.trig = d.degraded_trigger_ticks > 0 ? d.degraded_trigger_ticks : 3;
+    {
+      const double lf = d.leveling_link_fraction > 0.0 ? d.leveling_link_fraction : 0.10;
+      const double df = d.dual_copy_fraction > 0.0 ? d.dual_copy_fraction : 1.0 / 3.0;
+      pc.lvl_budget = (int64_t)simt::floor_d(kdiv(kmul(kmul(lf, pc.f.link_bw), pc.timer_P), pc.f.kvb));
+      pc.dual_budget = (int64_t)kmul(df, (double)pc.f.cap);
+    }
     status = KVSIM_OK;
     const int64_t nreq = d.num_requests < A->Ncap ? d.num_requests : A->Ncap;
     int32_t evd = pc.dmax;
@@ -312,7 +352,7 @@ struct Sim {
     simt::sync();  // previous point's readers are done with the scratch
     if (lane == 0) {
       ws()->pc = pc;
-      ws()->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      ws()->ct = Counters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     }
     simt::sync();
     n_events = 0;
@@ -331,8 +371,13 @@ struct Sim {
     L_kvmin = INT64_MAX;
     L_tlast = 0.0;
     Q_head = 0; Q_n = 0; Q_tok = 0;
-    // splitwise directed links
-    if (policy == KVSIM_POLICY_SPLITWISE)
+    L_partner = lane ^ 1;
+    L_lvl_dst = -1;
+    L_lvl_bud = 0;
+    G_mode = G_cnt = 0;
+    tick = 1;
+    // directed links (splitwise; AcceLLM EXT)
+    if (policy == KVSIM_POLICY_SPLITWISE || EXT)
       for (int i = lane; i < n * n; i += 32) link_()[i] = 0.0;
     next_rid = 0;
     t_prev = 0.0;
@@ -579,47 +624,58 @@ struct Sim {
 
   // ------------------------------------------------------- copies (AcceLLM)
   struct Found {
-    int32_t rid, idx, where;  // where: 0 none, 1 batch of partner, 2 incoming of partner
+    int32_t rid, idx, where;  // where: 0 none, 1 batch of client y, 2 incoming of client y
+    int32_t y;                // the instance whose primary the copy belongs to
     int64_t kv;
   };
+  // instances whose copies x holds (its pair partner; EXT: every y with
+  // partner[y] == x)
+  KV_DEV unsigned clients_of(int x) {
+    if constexpr (EXT) return simt::ballot(lane < n && lane != x && L_partner == x);
+    return 1u << (x ^ 1);
+  }
   // largest redundant copy held on instance x (max kv, ties lowest rid)
-  KV_DEV_NOINLINE Found largest_copy_on(int x) {
-    flush(x ^ 1);
-    const int y = x ^ 1;
+  KV_DEV Found largest_copy_on(int x) { return largest_copy_on_from(x, clients_of(x)); }
+  KV_DEV_NOINLINE Found largest_copy_on_from(int x, unsigned clients) {
     uint64_t best = 0;
-    int32_t bidx = -1, bwhere = 0;
-    const int32_t nb = get(L_nb, y), ni = get(L_ni, y);
-    for (int32_t j = lane; j < nb; j += 32) {
-      const int32_t rf = b_rem(y)[j];
-      if (rf & kCopy) {
-        const int64_t kv = (int64_t)b_kvb(y)[j] - (rf & kRemMask);
-        const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(y)[j]);
-        if (k > best) { best = k; bidx = j; bwhere = 1; }
+    int32_t bidx = -1, bwhere = 0, by = -1;
+    for (unsigned cm = clients; cm; cm &= cm - 1) {
+      const int y = simt::ffs(cm) - 1;
+      flush(y);
+      const int32_t nb = get(L_nb, y), ni = get(L_ni, y);
+      for (int32_t j = lane; j < nb; j += 32) {
+        const int32_t rf = b_rem(y)[j];
+        if (rf & kCopy) {
+          const int64_t kv = (int64_t)b_kvb(y)[j] - (rf & kRemMask);
+          const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(y)[j]);
+          if (k > best) { best = k; bidx = j; bwhere = 1; by = y; }
+        }
       }
-    }
-    for (int32_t j = lane; j < ni; j += 32) {
-      const int32_t rid = i_rid(y)[j];
-      if (c_cpy()[rid] == x) {
-        const int64_t kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
-        const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - rid);
-        if (k > best) { best = k; bidx = j; bwhere = 2; }
+      for (int32_t j = lane; j < ni; j += 32) {
+        const int32_t rid = i_rid(y)[j];
+        if (c_cpy()[rid] == x) {
+          const int64_t kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+          const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - rid);
+          if (k > best) { best = k; bidx = j; bwhere = 2; by = y; }
+        }
       }
     }
     const uint64_t wbest = simt::warp_max_u64(best);
     Found r;
-    r.where = 0; r.idx = -1; r.rid = -1; r.kv = 0;
+    r.where = 0; r.idx = -1; r.rid = -1; r.kv = 0; r.y = -1;
     if (wbest == 0) return r;
     const unsigned holder = simt::ballot(best == wbest);
     const int src = simt::ffs(holder) - 1;
     r.idx = simt::shfl(bidx, src);
     r.where = simt::shfl(bwhere, src);
+    r.y = simt::shfl(by, src);
     r.rid = 0x7fffffff - (int32_t)(uint32_t)(wbest & 0xffffffffu);
     r.kv = (int64_t)(wbest >> 32);
     return r;
   }
   KV_DEV_NOINLINE void evict(int x, const Found& v) {
     EMU_COUNT(14);
-    const int y = x ^ 1;
+    const int y = v.y;
     int64_t held = v.kv;
     if (v.where == 1) {
       if (get(L_job, y) == JOB_STEP) held += 1;
@@ -666,7 +722,7 @@ struct Sim {
     }
     if (own(x)) { L_used -= kv; L_skv -= kv; L_final -= (int64_t)pl + dl - 1; }
     if (rf & kCopy) {
-      const int y = x ^ 1;
+      const int y = partner_of(x);
       if (own(y)) { L_used -= kv; L_copy_tok -= kv; }
       if (own(x)) L_ncopy -= 1;
     }
@@ -678,11 +734,11 @@ struct Sim {
 
   // ------------------------------------------------------------ link FIFO
   KV_DEV double link_get(int s, int d) {
-    if (policy == KVSIM_POLICY_ACCELLM) return get(L_link, s);  // only (s, s^1)
+    if (policy == KVSIM_POLICY_ACCELLM && !EXT) return get(L_link, s);  // only (s, s^1)
     return link_()[s * n + d];
   }
   KV_DEV void link_set(int s, int d, double v) {
-    if (policy == KVSIM_POLICY_ACCELLM) {
+    if (policy == KVSIM_POLICY_ACCELLM && !EXT) {
       if (own(s)) L_link = v;
     } else {
       simt::sync();  // every lane has read the old value
@@ -721,11 +777,11 @@ struct Sim {
       if (nb == 0) break;
     }
     if (nb == 0) {
-      if (preempted && acc) ensure_prefill(x >> 1, t);
+      if (preempted && acc) ensure_prefill(qid(x >> 1), t);
       return;
     }
-    if (acc) {
-      const int y = x ^ 1;
+    if (acc && partner_of(x) >= 0) {
+      const int y = partner_of(x);
       for (;;) {
         const int32_t m = get(L_ncopy, x);
         if (get(L_used, y) + m <= PC.f.cap) {
@@ -746,7 +802,7 @@ struct Sim {
       L_busy_until = kadd(t, lat);
     }
     log(KVSIM_EV_STEP_START, x, nb, 0, K);
-    if (preempted && acc) ensure_prefill(x >> 1, t);
+    if (preempted && acc) ensure_prefill(qid(x >> 1), t);
 
   }
 
@@ -769,14 +825,15 @@ struct Sim {
     }
     count_tokens(o.nb_old, t);
     if (policy == KVSIM_POLICY_ACCELLM) {
-      const int y = x ^ 1;
+      const int y = partner_of(x);
       if (own(y)) { L_used -= o.copy_free; L_copy_tok -= o.copy_free; }
       if (own(x)) L_ncopy -= o.copy_done;
       if (o.m_copies > 0) {
-        const double busy = get(L_link, x);
+        const double busy = link_get(x, y);
         const double start = t > busy ? t : busy;
         const double fin = kadd(start, transfer_latency(PC.f, kmul((double)o.m_copies, PC.f.kvb)));
-        if (own(x)) { L_link = fin; L_mirror_fin = fin; }
+        link_set(x, y, fin);
+        if (own(x)) L_mirror_fin = fin;
         if (lane == 0) ws()->ct.mir_tokens += o.m_copies;
         log(KVSIM_EV_TRANSFER, x, y, 1, o.m_copies);
       }
@@ -1310,7 +1367,7 @@ struct Sim {
   // -------------------------------------------------------------- accellm
   KV_DEV int64_t load_of(int x) { return get(L_skv, x) + get(L_skv_in, x); }
   KV_DEV bool head_admissible(int x) {
-    const int q = x >> 1;
+    const int q = qid(x >> 1);
     if (get(Q_n, q) == 0) return false;
     const int32_t rid = q_at(q, get(Q_head, q), 0);
     const int64_t len = c_qlen()[rid];
@@ -1319,8 +1376,9 @@ struct Sim {
   // move every request whose primary is x and that holds a copy on x^1
   KV_DEV_NOINLINE void move_all_to_partner(int x, double t) {
     EMU_COUNT(8);
+    const int y = partner_of(x);
+    if (y < 0) return;  // a degraded group's dual instance: its requests stall
     flush(x);
-    const int y = x ^ 1;
     const double mfin = get(L_mirror_fin, x);
     const double pend = get(L_prev_end, x);
     int32_t nb = get(L_nb, x);
@@ -1433,7 +1491,7 @@ struct Sim {
 
   KV_DEV_NOINLINE void acc_start_job(int x, double t) {
     EMU_COUNT(13);
-    const int q = x >> 1;
+    const int q = qid(x >> 1);
     const int32_t h = get(Q_head, q);
     int32_t k = 0;
     int64_t s1 = 0, s2 = 0;
@@ -1503,6 +1561,13 @@ struct Sim {
   KV_DEV_NOINLINE void ensure_prefill_slow(int q, double t) {
     EMU_COUNT(11);
     if (get(Q_n, q) == 0) return;
+    if (degraded_pair(q)) {  // the dual instance is the group's only prefill instance
+      const int d = 4 * (q >> 1);
+      if (get(L_role, d) == ROLE_PREFILL || get(L_pend, d)) return;
+      if (get(L_job, d) == JOB_NONE) try_switch(d, t);
+      else if (own(d)) L_pend = 1;
+      return;
+    }
     const int a = 2 * q, b = a + 1;
     if (get(L_role, a) == ROLE_PREFILL || get(L_role, b) == ROLE_PREFILL || get(L_pend, a) || get(L_pend, b))
       return;
@@ -1513,6 +1578,12 @@ struct Sim {
 
   // rebalance_pair at x's boundary (SEMANTICS §6)
   KV_DEV void rebalance(int x, double t) {
+    if constexpr (EXT) {
+      if (degraded_pair(x >> 1)) {
+        if ((x & 3) != 0) dual_push(x, t);
+        return;
+      }
+    }
     const int y = x ^ 1;
     if (get(L_role, y) != ROLE_DECODE || get(L_pend, y)) return;
     const int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, y) - get(L_ni, y);
@@ -1591,8 +1662,11 @@ struct Sim {
       if (own(x)) L_pend = 0;
       if (try_switch(x, t)) return;
     }
-    ensure_prefill(x >> 1, t);
+    ensure_prefill(qid(x >> 1), t);
     if (get(L_role, x) == ROLE_PREFILL) return;
+    if constexpr (EXT) {
+      if (get(L_lvl_dst, x) >= 0) level_from(x, t);
+    }
     rebalance(x, t);
     step_start(x, t);
   }
@@ -1629,6 +1703,17 @@ struct Sim {
     if (own(x)) L_used -= kvfree;
     count_tokens(k, t);
     log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
+    if constexpr (EXT) {
+      if (is_dual(x)) {
+        dual_handoff(x, jstart, t);
+        if (own(x)) L_njob = 0;
+        if (head_admissible(x)) { acc_start_job(x, t); return; }
+        if (own(x)) L_role = ROLE_DECODE;
+        log(KVSIM_EV_ROLE, x, ROLE_DECODE, 0, 0);
+        acc_boundary(x, t);
+        return;
+      }
+    }
     // pass 2: redundant copies on y in job order while they fit
     int64_t used_y = get(L_used, y);
     int64_t s1c = 0;
@@ -1740,6 +1825,367 @@ struct Sim {
     acc_boundary(x, t);
   }
 
+  // ============================== EXT: degraded mode (SEMANTICS §6b)
+  // tokens the dual instance d holds as copies of decoder x's requests
+  // (held: +1 while x's step is in flight)
+  KV_DEV int64_t dual_copy_tokens(int d, int x) {
+    flush(x);
+    const int32_t nb = get(L_nb, x), ni = get(L_ni, x);
+    const int64_t st = get(L_job, x) == JOB_STEP ? 1 : 0;
+    int64_t s = 0;
+    for (int32_t j = lane; j < nb; j += 32) {
+      const int32_t rf = b_rem(x)[j];
+      if (rf & kCopy) s += (int64_t)b_kvb(x)[j] - (rf & kRemMask) + st;
+    }
+    for (int32_t j = lane; j < ni; j += 32) {
+      const int32_t rid = i_rid(x)[j];
+      if (c_cpy()[rid] == d) s += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+    }
+    return simt::warp_sum_nn(s);
+  }
+  // prefill survivors of the dual instance d: each goes to the decoder with
+  // the most free tokens (full KV transfer, one per destination); d keeps
+  // its computed KV as the copy while that decoder's budget allows
+  KV_DEV_NOINLINE void dual_handoff(int d, double jstart, double t) {
+    const int32_t k = get(L_njob, d);
+    const int64_t cap = PC.f.cap, budget = PC.dual_budget;
+    int64_t ct[3], u[3], per[3] = {0, 0, 0};
+    for (int j = 0; j < 3; ++j) { ct[j] = dual_copy_tokens(d, d + 1 + j); u[j] = get(L_used, d + 1 + j); }
+    int64_t freed = 0, kept = 0;
+    int32_t ncopy = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      const bool act = i < k;
+      int32_t rid = 0;
+      bool surv = false;
+      int64_t kv = 0;
+      if (act) {
+        rid = j_rid(d)[i];
+        const int32_t em = c_em()[rid];
+        surv = em != c_dl()[rid];
+        kv = (int64_t)c_pl()[rid] + em - 1;
+      }
+      int32_t dst = d;
+      bool cp = false;
+      const int lim = (k - i0) < 32 ? (k - i0) : 32;
+      for (int l = 0; l < lim; ++l) {
+        if (!simt::shfl((int32_t)surv, l)) continue;
+        const int64_t kl = simt::shfl(kv, l);
+        int b = 0;
+        int64_t bf = cap - u[0];
+        if (cap - u[1] > bf) { b = 1; bf = cap - u[1]; }
+        if (cap - u[2] > bf) { b = 2; bf = cap - u[2]; }
+        int32_t dl_ = d;
+        bool c_ = false;
+        if (bf >= kl) {
+          u[b] += kl;
+          per[b] += kl;
+          dl_ = d + 1 + b;
+          if (ct[b] + kl <= budget) { ct[b] += kl; c_ = true; kept += kl; ncopy += 1; }
+          else freed += kl;
+        }
+        if (lane == l) { dst = dl_; cp = c_; }
+      }
+      if (act && surv) {
+        j_dst(d)[i] = dst;
+        c_cpy()[rid] = cp ? d : -1;
+        if (cp) c_fresh()[rid] = t;
+      }
+    }
+    simt::sync();
+    for (int j = 0; j < 3; ++j)
+      if (own(d + 1 + j)) { L_used = u[j]; if (L_used > L_peak) L_peak = L_used; }
+    if (own(d)) { L_used -= freed; L_copy_tok += kept; }
+    if (ncopy) log(KVSIM_EV_COPY, d, ncopy, 1, kept);
+    for (int j = 0; j < 3; ++j) {
+      if (per[j] == 0) continue;
+      const int X = d + 1 + j;
+      const double fin = prefill_transfer(d, X, per[j], jstart, t);
+      const int32_t base = get(L_ni, X);
+      int32_t add = 0;
+      int64_t kvs = 0;
+      for (int32_t i0 = 0; i0 < k; i0 += 32) {
+        const int32_t i = i0 + lane;
+        bool go = false;
+        int32_t rid = 0;
+        if (i < k) {
+          rid = j_rid(d)[i];
+          go = c_em()[rid] != c_dl()[rid] && j_dst(d)[i] == X;
+        }
+        const unsigned m = simt::ballot(go);
+        if (go) {
+          const int32_t pos = base + add + simt::popc(m & simt::lanemask_lt());
+          i_rid(X)[pos] = rid;
+          i_ready(X)[pos] = fin;
+          kvs += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+        }
+        add += simt::popc(m);
+      }
+      kvs = simt::warp_sum_nn(kvs);
+      simt::sync();
+      if (own(X)) { L_ni += add; L_skv_in += kvs; if (fin < L_min_ready) L_min_ready = fin; }
+    }
+    // survivors no decoder had room for decode on d (joiners, no copy)
+    const int32_t nb = get(L_nb, d);
+    int32_t add = 0, minrem = 0x7fffffff;
+    int64_t kvadd = 0;
+    for (int32_t i0 = 0; i0 < k; i0 += 32) {
+      const int32_t i = i0 + lane;
+      bool go = false;
+      int32_t rid = 0;
+      if (i < k) {
+        rid = j_rid(d)[i];
+        go = c_em()[rid] != c_dl()[rid] && j_dst(d)[i] == d;
+      }
+      const unsigned m = simt::ballot(go);
+      if (go) {
+        const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
+        const int32_t pos = nb + add + simt::popc(m & simt::lanemask_lt());
+        b_rid(d)[pos] = rid;
+        b_rem(d)[pos] = (dl - em) | kJoin;
+        b_kvb(d)[pos] = pl + dl - 1;
+        b_tbt(d)[pos] = c_tbt()[rid];
+        kvadd += (int64_t)pl + em - 1;
+        if (dl - em < minrem) minrem = dl - em;
+      }
+      add += simt::popc(m);
+    }
+    kvadd = simt::warp_sum_nn(kvadd);
+    minrem = simt::warp_min_i32(minrem);
+    simt::sync();
+    if (own(d)) { L_nb += add; L_skv += kvadd; if (minrem < L_minrem) L_minrem = minrem; }
+  }
+  // at decoder x's boundary: requests whose copy the dual instance holds move
+  // to it while no prefill is pending (rebalance_pair's greedy);
+  // x drops its KV ("overwrite")
+  KV_DEV_NOINLINE void dual_push(int x, double t) {
+    const int d = x & ~3;
+    if (get(L_role, d) != ROLE_DECODE || get(L_pend, d) || get(Q_n, qid(x >> 1)) != 0) return;
+    flush(x);
+    int64_t c = (int64_t)get(L_nb, x) + get(L_ni, x) - get(L_nb, d) - get(L_ni, d);
+    int64_t dd = load_of(x) - load_of(d);
+    while (c >= 1 && dd >= 1) {
+      const int64_t lim = c >= 2 ? dd : dd - 1;
+      const int32_t nb = get(L_nb, x);
+      uint64_t best = 0;
+      int32_t bidx = -1;
+      for (int32_t j = lane; j < nb; j += 32) {
+        const int32_t rf = b_rem(x)[j];
+        if (rf & kCopy) {
+          const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
+          if (kv <= lim) {
+            const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
+            if (kk > best) { best = kk; bidx = j; }
+          }
+        }
+      }
+      const uint64_t wb = simt::warp_max_u64(best);
+      if (wb == 0) break;
+      const int src = simt::ffs(simt::ballot(best == wb)) - 1;
+      const int32_t idx = simt::shfl(bidx, src);
+      const int64_t kv = (int64_t)(wb >> 32);
+      // move to d, copy dropped
+      const int32_t rid = b_rid(x)[idx];
+      const int32_t rf = b_rem(x)[idx];
+      const int32_t rem = rf & kRemMask;
+      const double tb = b_tbt(x)[idx];
+      const bool joiner = (rf & kJoin) != 0;
+      const double fresh = joiner ? c_fresh()[rid] : get(L_mirror_fin, x);
+      const double ready = fresh > t ? fresh : t;
+      const double last = joiner ? c_last()[rid] : get(L_prev_end, x);
+      const int32_t dl = c_dl()[rid];
+      simt::sync();
+      if (lane == 0) {
+        c_em()[rid] = dl - rem;
+        c_tbt()[rid] = tb;
+        c_last()[rid] = last;
+        c_cpy()[rid] = -1;
+        c_nmv()[rid] += 1;
+      }
+      batch_remove(x, idx);
+      incoming_append(d, rid, ready);
+      if (own(x)) { L_skv -= kv; L_ncopy -= 1; L_used -= kv; }
+      if (own(d)) { L_skv_in += kv; L_copy_tok -= kv; }
+      if (lane == 0) ws()->ct.n_moves += 1;
+      log(KVSIM_EV_MOVE, x, rid, d, 0);
+      c -= 2;
+      dd -= 2 * kv;
+    }
+  }
+  KV_DEV_NOINLINE void evict_group_copies(int h, unsigned clients) {
+    for (;;) {
+      Found v = largest_copy_on_from(h, clients);
+      if (!v.where) return;
+      evict(h, v);
+    }
+  }
+  KV_DEV_NOINLINE void enter_degraded(int g, double t) {
+    const int a = 4 * g;
+    const unsigned grp = 0xfu << a;
+    for (int h = a + 1; h <= a + 3; ++h) evict_group_copies(h, clients_of(h) & grp);
+    if (lane >= a && lane <= a + 3) L_partner = lane == a ? -1 : a;
+    if (own(g)) G_mode = 1;
+    if (lane == 0) ws()->ct.n_modes += 1;
+    // the group's requests wait in its first pair's queue
+    const int q0 = 2 * g, q1 = 2 * g + 1;
+    const int32_t n1 = get(Q_n, q1), h1 = get(Q_head, q1), h0 = get(Q_head, q0), n0 = get(Q_n, q0);
+    const int64_t tk1 = get(Q_tok, q1);
+    for (int32_t i = lane; i < n1; i += 32) {
+      int64_t dst = (int64_t)h0 + n0 + i;
+      if (dst >= Ncap_) dst -= Ncap_;
+      ring(q0)[dst] = q_at(q1, h1, i);
+    }
+    simt::sync();
+    if (own(q0)) { Q_n += n1; Q_tok += tk1; }
+    if (own(q1)) { Q_n = 0; Q_tok = 0; }
+    log(KVSIM_EV_MODE, g, 1, 0, 0);
+    ensure_prefill(q0, t);
+  }
+  KV_DEV_NOINLINE void leave_degraded(int g, double t) {
+    const int a = 4 * g;
+    evict_group_copies(a, clients_of(a) & (0xcu << a));
+    if (lane >= a && lane <= a + 3) L_partner = lane ^ 1;
+    if (own(g)) G_mode = 0;
+    if (lane == 0) ws()->ct.n_modes += 1;
+    log(KVSIM_EV_MODE, g, 0, 0, 0);
+    ensure_prefill(2 * g, t);
+    ensure_prefill(2 * g + 1, t);
+  }
+  // ====================== EXT: inter-pair leveling (SEMANTICS §6b)
+  KV_DEV_NOINLINE void schedule_leveling() {
+    const int np = n >> 1;
+    int64_t l = 0;
+    bool el = false;
+    {
+      const int q = lane;
+      const int a = (2 * q) & 31, b = (2 * q + 1) & 31;
+      const int32_t ra = simt::shfl(L_role, a), rb = simt::shfl(L_role, b);
+      const int32_t pa = simt::shfl(L_pend, a), pb = simt::shfl(L_pend, b);
+      const int64_t la = simt::shfl(L_skv, a) + simt::shfl(L_skv_in, a);
+      const int64_t lb = simt::shfl(L_skv, b) + simt::shfl(L_skv_in, b);
+      const int32_t gm = simt::shfl(G_mode, (q >> 1) & 31);
+      const bool deg = (q >> 1) < (n >> 2) && gm != 0;
+      el = q < np && !deg && Q_n == 0 && ra == ROLE_DECODE && rb == ROLE_DECODE && !pa && !pb;
+      l = la + lb;
+    }
+    const unsigned em = simt::ballot(el);
+    if (em == 0) return;
+    const int64_t mx = simt::warp_max_i64(el ? l : INT64_MIN);
+    const int64_t mn = simt::warp_min_i64(el ? l : INT64_MAX);
+    const int A = simt::ffs(simt::ballot(el && l == mx)) - 1;
+    const int B = simt::ffs(simt::ballot(el && l == mn)) - 1;
+    if (A == B || mx - mn < 2) return;
+    const int x = load_of(2 * A + 1) > load_of(2 * A) ? 2 * A + 1 : 2 * A;
+    const int y = (PC.f.cap - get(L_used, 2 * B + 1)) > (PC.f.cap - get(L_used, 2 * B)) ? 2 * B + 1 : 2 * B;
+    if (own(x)) { L_lvl_dst = y; L_lvl_bud = PC.lvl_budget; }
+  }
+  // at x's boundary: migrate batch members (largest first) to the lighter
+  // pair while each move strictly narrows the pair-load gap, within the
+  // per-period link budget and the destination's memory
+  KV_DEV_NOINLINE void level_from(int x, double t) {
+    const int y = get(L_lvl_dst, x);
+    int64_t bud = get(L_lvl_bud, x);
+    if (own(x)) L_lvl_dst = -1;
+    if (get(L_role, y) != ROLE_DECODE || get(L_pend, y) || degraded_pair(x >> 1) || degraded_pair(y >> 1)) return;
+    flush(x);
+    int64_t dd = load_of(x) + load_of(x ^ 1) - load_of(y) - load_of(y ^ 1);
+    int64_t room = PC.f.cap - get(L_used, y);
+    for (;;) {
+      int64_t lim = dd - 1;
+      if (bud < lim) lim = bud;
+      if (room < lim) lim = room;
+      if (lim < 1) break;
+      const int32_t nb = get(L_nb, x);
+      uint64_t best = 0;
+      int32_t bidx = -1;
+      for (int32_t j = lane; j < nb; j += 32) {
+        const int32_t rf = b_rem(x)[j];
+        const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
+        if (kv <= lim) {
+          const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
+          if (kk > best) { best = kk; bidx = j; }
+        }
+      }
+      const uint64_t wb = simt::warp_max_u64(best);
+      if (wb == 0) break;
+      const int src = simt::ffs(simt::ballot(best == wb)) - 1;
+      const int32_t idx = simt::shfl(bidx, src);
+      const int64_t kv = (int64_t)(wb >> 32);
+      const int32_t rid = b_rid(x)[idx];
+      const int32_t rf = b_rem(x)[idx];
+      const int32_t rem = rf & kRemMask;
+      const double tb = b_tbt(x)[idx];
+      const bool joiner = (rf & kJoin) != 0;
+      const double last = joiner ? c_last()[rid] : get(L_prev_end, x);
+      const int32_t dl = c_dl()[rid];
+      simt::sync();
+      if (lane == 0) {
+        c_em()[rid] = dl - rem;
+        c_tbt()[rid] = tb;
+        c_last()[rid] = last;
+        c_cpy()[rid] = -1;
+        c_nmv()[rid] += 1;
+      }
+      if (rf & kCopy) {
+        const int h = partner_of(x);
+        if (own(h)) { L_used -= kv; L_copy_tok -= kv; }
+        if (own(x)) L_ncopy -= 1;
+      }
+      batch_remove(x, idx);
+      if (own(x)) { L_skv -= kv; L_used -= kv; }
+      add_used(y, kv);
+      const double busy = link_get(x, y);
+      const double start = t > busy ? t : busy;
+      const double fin = kadd(start, transfer_latency(PC.f, kmul((double)kv, PC.f.kvb)));
+      link_set(x, y, fin);
+      incoming_append(y, rid, fin);
+      if (own(y)) L_skv_in += kv;
+      if (lane == 0) { ws()->ct.n_moves += 1; ws()->ct.lvl_tokens += kv; }
+      log(KVSIM_EV_LEVEL, x, rid, y, kv);
+      dd -= 2 * kv;
+      bud -= kv;
+      room -= kv;
+    }
+  }
+  KV_DEV_NOINLINE void on_timer(double t) {
+    if (lane == 0) ws()->ct.n_ticks += 1;
+    log(KVSIM_EV_TIMER, -1, (int)(tick - 1), 0, 0);
+    if (PC.deg_on) {
+      for (int g = 0; g < (n >> 2); ++g) {
+        const int a = 4 * g;
+        const bool in_g = lane >= a && lane <= a + 3;
+        const bool pf = simt::ballot(in_g && (L_role == ROLE_PREFILL || L_pend)) != 0;
+        int32_t cnt = get(G_cnt, g);
+        bool go;
+        if (!get(G_mode, g)) {
+          int64_t live = 0, red = 0;
+          for (int h = a; h <= a + 3; ++h) {
+            live += (int64_t)get(L_nb, h) + get(L_ni, h);
+            red += get(L_ncopy, h);
+            const int32_t ni = get(L_ni, h);
+            int32_t ri = 0;
+            for (int32_t j = lane; j < ni; j += 32) ri += c_cpy()[i_rid(h)[j]] >= 0 ? 1 : 0;
+            red += simt::warp_sum_i32(ri);
+          }
+          cnt = (live > 0 && (double)red < kmul(PC.red_thr, (double)live)) ? cnt + 1 : 0;
+          go = cnt >= PC.trig && !pf;
+          if (go) cnt = 0;
+          if (own(g)) G_cnt = cnt;
+          if (go) enter_degraded(g, t);
+        } else {
+          int64_t u = 0;
+          for (int h = a; h <= a + 3; ++h) u += get(L_used, h);
+          cnt = ((double)u <= kmul(PC.exit_fill, kmul(4.0, (double)PC.f.cap))) ? cnt + 1 : 0;
+          go = cnt >= PC.trig && !pf;
+          if (go) cnt = 0;
+          if (own(g)) G_cnt = cnt;
+          if (go) leave_degraded(g, t);
+        }
+      }
+    }
+    if (PC.lvl_on) schedule_leveling();
+  }
+
   // -------------------------------------------------------------- arrival
   KV_DEV_NOINLINE void arrive(double t) {
     EMU_COUNT(16);
@@ -1787,7 +2233,14 @@ struct Sim {
       const int np = n >> 1;
       const int64_t ua = simt::shfl(L_used, (2 * lane) & 31);
       const int64_t ub = simt::shfl(L_used, (2 * lane + 1) & 31);
-      const int64_t fr = lane < np ? (PC.f.cap - ua) + (PC.f.cap - ub) - Q_tok : INT64_MIN;
+      int64_t fr = lane < np ? (PC.f.cap - ua) + (PC.f.cap - ub) - Q_tok : INT64_MIN;
+      if constexpr (EXT) {  // a degraded group is one routing unit (its first pair's queue)
+        const int64_t uc = simt::shfl(L_used, (2 * lane + 2) & 31);
+        const int64_t ud = simt::shfl(L_used, (2 * lane + 3) & 31);
+        const int32_t gm = simt::shfl(G_mode, (lane >> 1) & 31);
+        if (lane < np && (lane >> 1) < (n >> 2) && gm != 0)
+          fr = (lane & 1) ? INT64_MIN : (PC.f.cap - ua) + (PC.f.cap - ub) + (PC.f.cap - uc) + (PC.f.cap - ud) - Q_tok;
+      }
       const int64_t best = simt::warp_max_i64(fr);
       const int q = simt::ffs(simt::ballot(fr == best)) - 1;
       log(KVSIM_EV_ARRIVE, q, rid, pl, 0);
@@ -1818,6 +2271,16 @@ struct Sim {
       if (!is_arrival && ck == (1 << 20)) break;
       if (++n_events + ws()->ct.adv_events > PC.event_budget) { status = KVSIM_E_EVENT_BUDGET; break; }
       if (lane == 0) ws()->ct.n_loop += 1;
+      if constexpr (EXT) {  // policy timer: kind 4, after every other kind at equal time
+        const double tt = kmul((double)tick, PC.timer_P);
+        if (tt < (is_arrival ? t_next : ct)) {
+          now = tt;
+          if (now > t_last) t_last = now;
+          tick += 1;
+          on_timer(tt);
+          continue;
+        }
+      }
       unsigned drive = 0xffffffffu;
       if (is_arrival) {
         now = t_next;
@@ -1913,6 +2376,9 @@ struct Sim {
       s.link_prefill_tokens = ct.pf_tokens; s.link_mirror_tokens = ct.mir_tokens;
       s.makespan_s = t_last;
       s.reserved[0] = ct.n_loop;
+      s.link_leveling_tokens = ct.lvl_tokens;
+      s.n_timer_ticks = ct.n_ticks;
+      s.n_mode_switches = ct.n_modes;
       const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
       double busy = 0.0;
       for (int x = 0; x < n; ++x) busy = kadd(busy, get(L_busy_time, x));
@@ -2029,9 +2495,9 @@ struct Sim {
 };
 
 // One point, simulated by the policy-specialised core.
-template <int P, bool LOG>
+template <int P, bool LOG, bool EXT = false>
 KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot, int64_t pt) {
-  Sim<P, LOG> sim(ap, w, slot);
+  Sim<P, LOG, EXT> sim(ap, w, slot);
   if (sim.init_point(pt)) sim.run();
   sim.finalize();
 }
@@ -2052,7 +2518,11 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
     if ((int64_t)p >= a.n_pts) break;
     const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
     const int32_t pol = a.pts[pt].policy;
-    if (a.ev != nullptr) {
+    const bool ext = pol == KVSIM_POLICY_ACCELLM && (a.pts[pt].accellm_flags & 3) != 0;
+    if (ext) {
+      if (a.ev != nullptr) run_point<KVSIM_POLICY_ACCELLM, true, true>(ap, w, slot, pt);
+      else run_point<KVSIM_POLICY_ACCELLM, false, true>(ap, w, slot, pt);
+    } else if (a.ev != nullptr) {
       if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE, true>(ap, w, slot, pt);
       else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_UNIFIED, true>(ap, w, slot, pt);

@@ -60,3 +60,47 @@ def random_small(i: int, max_req: int = 50):
         tokens = r.randint(pmax + dmax + 10, 4 * (pmax + dmax) + 3000)
         p.hbm_capacity = (W + tokens * kvb) / (p.num_devices * (1.0 - p.memory_reserve_fraction))
     return p
+
+
+def random_ext(i: int, max_req: int = 200):
+    """AcceLLM with the timer-driven extensions (docs/SEMANTICS.md §6b):
+    degraded mode and/or inter-pair leveling, short timer periods so small
+    runs see many ticks, memory-starved instances so degraded mode triggers."""
+    r = random.Random(5000 + i)
+    inst = r.choice([4, 4, 6, 8])
+    model = r.choice(["llama2-7b", "llama2-70b"])
+    device = r.choice(["h100", "910b2"])
+    pmin = r.randint(1, 300)
+    pmax = pmin + r.randint(0, 500)
+    dmin = r.randint(1, 60)
+    dmax = dmin + r.randint(0, 200)
+    flags = r.choice([(True, False), (False, True), (True, True)])
+    p = make_point(model=model, device=device, policy="accellm", instances=inst, num_requests=r.randint(20, max_req),
+                   rate=r.choice([4.0, 16.0, 60.0, 200.0]), workload=(pmin, pmax, dmin, dmax),
+                   seed=r.randint(0, 1 << 30), arrival=r.choice(["poisson", "poisson", "fixed"]),
+                   link=r.choice(["striped", "single"]), prefill_budget=r.choice([8192, 2048, 700]),
+                   degraded=flags[0], leveling=flags[1], timer_s=r.choice([0.01, 0.05, 0.2, 1.0]),
+                   trigger_ticks=r.choice([0, 1, 2]), leveling_fraction=r.choice([0.0, 0.5, 5.0]),
+                   degraded_redundancy=r.choice([0.0, 0.9]), degraded_exit_fill=r.choice([0.0, 0.3, 0.9]),
+                   dual_copy_fraction=r.choice([0.0, 0.5]))
+    if r.random() < 0.6:
+        from paper_2411_05555_b200.abi import MODELS
+        W = MODELS[model][0] * MODELS[model][5]
+        kvb = 2 * MODELS[model][1] * MODELS[model][3] * MODELS[model][4] * MODELS[model][5]
+        tokens = r.randint(pmax + dmax + 10, 6 * (pmax + dmax) + 4000)
+        p.hbm_capacity = (W + tokens * kvb) / (p.num_devices * (1.0 - p.memory_reserve_fraction))
+    return p
+
+
+def ext_long_points(n: int = 800):
+    """Longer extension runs: many degraded entries/exits, heavy leveling."""
+    return [
+        make_point(policy="accellm", instances=4, rate=12.0, num_requests=n, workload="heavy", reserve=0.5, seed=3,
+                   degraded=True, timer_s=0.2),
+        make_point(policy="accellm", instances=8, rate=30.0, num_requests=n, workload="heavy", reserve=0.5, seed=4,
+                   degraded=True, leveling=True, timer_s=0.1, trigger_ticks=1),
+        make_point(policy="accellm", instances=6, rate=10.0, num_requests=n, workload="mixed", seed=5,
+                   leveling=True, timer_s=0.05, leveling_fraction=2.0),
+        make_point(policy="accellm", instances=16, rate=40.0, num_requests=n, workload="mixed", seed=6,
+                   leveling=True, degraded=True, device="910b2", reserve=0.4, timer_s=0.1),
+    ]

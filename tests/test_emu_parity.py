@@ -44,3 +44,16 @@ def test_invalid_points_reported():
     assert got[0].status == -3 and got[1].status == -2
     for p, g in zip(pts, got):
         assert run_oracle(p, ev_cap=0, recs=False).status == g.status
+
+
+@pytest.mark.parametrize("chunk", range(3))
+def test_accellm_extensions_random(chunk):
+    """Degraded mode + inter-pair leveling (SEMANTICS §6b): kernel core ==
+    oracle bit for bit, event logs included."""
+    from configs import random_ext
+    check([random_ext(i) for i in range(chunk * 40, chunk * 40 + 40)], ev=1 << 17)
+
+
+def test_accellm_extensions_long():
+    from configs import ext_long_points
+    check(ext_long_points(n=400), ev=1 << 20)

@@ -144,3 +144,25 @@ def test_trace_generator_bitwise(sim):
         k = L.kvo_gen_trace(C.byref(p), a, b, c, n)
         assert len(arr) == k
         assert list(a)[:k] == arr and list(b)[:k] == pl and list(c)[:k] == dl
+
+
+def test_accellm_extensions_random(sim):
+    # degraded mode + inter-pair leveling (SEMANTICS §6b), event logs included
+    from configs import random_ext
+    check(sim, [random_ext(i) for i in range(200)], ev=1 << 17)
+
+
+def test_accellm_extensions_long(sim):
+    from configs import ext_long_points
+    summ = check(sim, ext_long_points(n=3000), ev=1 << 21)
+    assert summ[0].n_mode_switches > 0 and summ[2].link_leveling_tokens > 0
+
+
+def test_extensions_mixed_with_plain_points(sim):
+    # EXT and plain points co-resident in one launch (different specialisations)
+    from configs import random_ext
+    pts = []
+    for i in range(30):
+        pts.append(random_ext(300 + i))
+        pts.append(random_small(700 + i, max_req=120))
+    check(sim, pts, ev=1 << 17)

@@ -108,3 +108,52 @@ def test_randomized_invariant_suite(chunk):  # SPEC.md:469 acceptance #11
             assert bytes(again.summary) == bytes(s)                 # determinism
     finally:
         L.kvo_set_invariant_checks(0)
+
+
+def test_accellm_extensions_invariants():
+    """Degraded mode + inter-pair leveling (SEMANTICS
+    §6b): ledger exactness, memory safety and copy placement (copies only on
+    the holder the partner relation names) after every event, conservation,
+    determinism; and the mechanisms actually fire across the sample."""
+    from configs import random_ext
+    L = oracle()
+    L.kvo_set_invariant_checks(1)
+    modes = lvl = 0
+    try:
+        for i in range(120):
+            p = random_ext(i)
+            r = run_oracle(p, ev_cap=0)
+            s = r.summary
+            assert r.status == 0, (i, r.status)
+            assert s.n_completed == s.n_requests
+            assert s.tokens_total == sum(x.decode_len for x in r.recs)
+            period = p.policy_timer_s or 1.0
+            assert s.n_timer_ticks == 0 or s.makespan_s > period
+            if s.makespan_s > 2 * period:
+                assert s.n_timer_ticks > 0
+            if not (p.accellm_flags & 1):
+                assert s.n_mode_switches == 0
+            if not (p.accellm_flags & 2):
+                assert s.link_leveling_tokens == 0
+            modes += s.n_mode_switches > 0
+            lvl += s.link_leveling_tokens > 0
+            assert bytes(run_oracle(p, ev_cap=0).summary) == bytes(s)
+    finally:
+        L.kvo_set_invariant_checks(0)
+    assert modes >= 5 and lvl >= 5, (modes, lvl)
+
+
+def test_extensions_off_is_plain_accellm():
+    """With both flags off the timer never fires and results are the plain
+    AcceLLM policy's; degraded mode in a memory-starved cluster serves more
+    requests without recompute preemption."""
+    base = make_point(policy="accellm", instances=4, rate=12.0, num_requests=3000, workload="heavy",
+                      reserve=0.5, seed=3)
+    s0 = run_oracle(base, recs=False).summary
+    assert s0.n_timer_ticks == 0 and s0.n_mode_switches == 0
+    deg = make_point(policy="accellm", instances=4, rate=12.0, num_requests=3000, workload="heavy",
+                     reserve=0.5, seed=3, degraded=True)
+    s1 = run_oracle(deg, recs=False).summary
+    assert s1.n_mode_switches >= 1
+    assert s1.n_preemptions < s0.n_preemptions
+    assert s1.link_mirror_tokens < s0.link_mirror_tokens    # decoders stop mirroring most requests
