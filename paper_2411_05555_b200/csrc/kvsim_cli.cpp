@@ -98,7 +98,7 @@ const char* const kKeys[] = {"model", "device", "num_devices", "memory_reserve_f
                              "arrival_process", "rate", "rates", "duration_s", "num_requests", "warmup_s", "seed",
                              "seeds", "efficiency", "link_aggregation", "trace", "sweep_instances",
                              "sweep_devices", "curves", "emit_records", "splitwise_cobatch", "degraded_mode",
-                             "inter_pair_leveling", "output", "resource"};
+                             "inter_pair_leveling", "policy_timer_s", "output", "resource"};
 
 struct Resolved {
   jl::Value cfg;  // resolved config (defaults filled)
@@ -248,10 +248,9 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
     if (std::find_if(std::begin(kKeys), std::end(kKeys), [&](const char* k) { return kv.first == k; }) ==
         std::end(kKeys))
       throw ConfigError("unknown config key: " + kv.first);
-  for (const char* k : {"splitwise_cobatch", "degraded_mode", "inter_pair_leveling"})
-    if (const jl::Value* v = in.find(k))
-      if (!(v->kind == jl::Value::Bool && !v->b))
-        throw ConfigError(std::string(k) + " is not modelled in this version (must be false)");
+  if (const jl::Value* v = in.find("splitwise_cobatch"))
+    if (!(v->kind == jl::Value::Bool && !v->b))
+      throw ConfigError("splitwise_cobatch is not modelled in this version (must be false)");
   jl::Value c = jl::Value::object();
   c.set("model", model_obj(in.find("model")));
   c.set("device", device_obj(in.find("device") ? *in.find("device") : jl::Value::string("h100")));
@@ -344,6 +343,51 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
     c.set("resource", r);
   } else if (cmd == "resource-sweep") {
     throw ConfigError("resource-sweep needs a \"resource\" block");
+  }
+  // AcceLLM timer-driven extensions (SEMANTICS §6b):
+  // `true`/`false` or an object of named thresholds; every default is echoed
+  auto ext_block = [&](const char* key, std::vector<std::pair<const char*, double>> defs) {
+    jl::Value o = jl::Value::object();
+    bool on = false;
+    std::vector<double> vals;
+    for (auto& d : defs) vals.push_back(d.second);
+    if (const jl::Value* v = in.find(key)) {
+      if (v->kind == jl::Value::Bool) {
+        on = v->b;
+      } else if (v->is_obj()) {
+        on = true;
+        for (auto& kv : v->obj) {
+          if (kv.first == "enabled") {
+            if (kv.second.kind != jl::Value::Bool) throw ConfigError(std::string(key) + ".enabled must be a boolean");
+            on = kv.second.b;
+            continue;
+          }
+          size_t i = 0;
+          for (; i < defs.size(); ++i)
+            if (kv.first == defs[i].first) break;
+          if (i == defs.size()) throw ConfigError(std::string("unknown ") + key + " key: " + kv.first);
+          vals[i] = req_num(kv.second, defs[i].first);
+          if (!(vals[i] > 0)) throw ConfigError(std::string(key) + "." + defs[i].first + " must be > 0");
+        }
+      } else {
+        throw ConfigError(std::string(key) + " must be a boolean or an object");
+      }
+    }
+    o.set("enabled", jl::Value::boolean(on));
+    for (size_t i = 0; i < defs.size(); ++i) o.set(defs[i].first, jl::Value::number(vals[i]));
+    c.set(key, o);
+  };
+  ext_block("degraded_mode", {{"trigger_ticks", 3}, {"redundancy_threshold", 0.5}, {"exit_fill", 0.5},
+                              {"dual_copy_fraction", 1.0 / 3.0}});
+  ext_block("inter_pair_leveling", {{"link_fraction", 0.10}});
+  {
+    const double tp = in.find("policy_timer_s") ? req_num(*in.find("policy_timer_s"), "policy_timer_s") : 1.0;
+    if (!(tp > 0)) throw ConfigError("policy_timer_s must be > 0");
+    c.set("policy_timer_s", jl::Value::number(tp));
+  }
+  {
+    const double tt = c.find("degraded_mode")->find("trigger_ticks")->num;
+    if (tt != std::floor(tt)) throw ConfigError("degraded_mode.trigger_ticks must be an integer");
   }
   c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
                                                ? in.find("emit_records")->b
@@ -438,6 +482,15 @@ kvsim_point_desc base_point(const jl::Value& c, const jl::Value& dev) {
   const jl::Value& d = *c.find("duration_s");
   p.duration_s = d.is_str() ? INFINITY : d.num;
   p.warmup_s = c.find("warmup_s")->num;
+  const jl::Value& dm = *c.find("degraded_mode");
+  const jl::Value& lv = *c.find("inter_pair_leveling");
+  p.accellm_flags = (dm.find("enabled")->b ? KVSIM_ACCELLM_DEGRADED : 0) | (lv.find("enabled")->b ? KVSIM_ACCELLM_LEVELING : 0);
+  p.degraded_trigger_ticks = (int32_t)dm.find("trigger_ticks")->num;
+  p.degraded_redundancy = dm.find("redundancy_threshold")->num;
+  p.degraded_exit_fill = dm.find("exit_fill")->num;
+  p.dual_copy_fraction = dm.find("dual_copy_fraction")->num;
+  p.leveling_link_fraction = lv.find("link_fraction")->num;
+  p.policy_timer_s = c.find("policy_timer_s")->num;
   return p;
 }
 
@@ -570,7 +623,8 @@ jl::Value summary_json(const kvsim_point_summary& s) {
   I("n_events", s.n_events); I("n_steps", s.n_steps); I("n_prefills", s.n_prefills);
   I("n_moves", s.n_moves); I("n_preemptions", s.n_preemptions); I("n_evictions", s.n_evictions);
   I("peak_kv_tokens", s.peak_kv_tokens); I("link_prefill_tokens", s.link_prefill_tokens);
-  I("link_mirror_tokens", s.link_mirror_tokens);
+  I("link_mirror_tokens", s.link_mirror_tokens); I("link_leveling_tokens", s.link_leveling_tokens);
+  I("n_timer_ticks", s.n_timer_ticks); I("n_mode_switches", s.n_mode_switches);
   D("makespan_s", s.makespan_s);
   D("ttft_mean", s.ttft_mean); D("ttft_p50", s.ttft_p50); D("ttft_p95", s.ttft_p95); D("ttft_max", s.ttft_max);
   D("tbt_mean", s.tbt_mean); D("tbt_max", s.tbt_max);

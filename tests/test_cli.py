@@ -51,7 +51,10 @@ def test_validate_echoes_defaults(kvsim, tmp_path):
                  "link_bandwidth": 1e9}}, "model does not fit in instance memory"),
     ({"workload": {"prompt_range": [10, 5], "decode_range": [1, 2]}}, "1 <= min <= max"),
     ({"policy": "fcfs"}, "unknown policy"),
-    ({"degraded_mode": True}, "not modelled"),
+    ({"splitwise_cobatch": True}, "not modelled"),
+    ({"degraded_mode": {"trigger_tick": 2}}, "unknown degraded_mode key: trigger_tick"),
+    ({"inter_pair_leveling": 3}, "must be a boolean or an object"),
+    ({"policy_timer_s": 0}, "policy_timer_s must be > 0"),
 ])
 def test_config_errors(kvsim, tmp_path, cfg, msg):
     r = run(kvsim, "validate-config", "--config", write(tmp_path, "c.json", cfg))
@@ -190,3 +193,36 @@ def test_sweep_compare_table(kvsim, tmp_path):
     for g in cmp:
         assert g["ratios_vs_accellm"]["accellm"]["cost_eff"] == 1.0
         assert len(g["trace_fingerprint"]) == 16
+
+
+def test_accellm_extension_keys_resolve(kvsim, tmp_path):
+    # every tie-break/threshold is a named key and defaults are echoed
+    r = run(kvsim, "validate-config", "--config",
+            write(tmp_path, "e.json", {"degraded_mode": {"trigger_ticks": 2}, "inter_pair_leveling": True}))
+    assert r.returncode == 0, r.stderr
+    c = json.loads(r.stdout)
+    assert c["degraded_mode"] == {"enabled": True, "trigger_ticks": 2, "redundancy_threshold": 0.5,
+                                  "exit_fill": 0.5, "dual_copy_fraction": 1.0 / 3.0}
+    assert c["inter_pair_leveling"] == {"enabled": True, "link_fraction": 0.1}
+    assert c["policy_timer_s"] == 1.0
+    r = run(kvsim, "validate-config", "--config", write(tmp_path, "f.json", {"num_requests": 3}))
+    c = json.loads(r.stdout)
+    assert c["degraded_mode"]["enabled"] is False and c["inter_pair_leveling"]["enabled"] is False
+
+
+@pytest.mark.gpu
+def test_run_accellm_extensions_match_oracle(kvsim, tmp_path):
+    # degraded mode + leveling through the drop-in entry point (SEMANTICS §6b)
+    cfg = {"policy": "accellm", "instances": 8, "rate": 30.0, "num_requests": 1500, "workload": "heavy",
+           "memory_reserve_fraction": 0.5, "seed": 4, "policy_timer_s": 0.1,
+           "degraded_mode": {"trigger_ticks": 1}, "inter_pair_leveling": True}
+    out = tmp_path / "o"
+    r = run(kvsim, "run", "--config", write(tmp_path, "c.json", cfg), "--out", str(out))
+    assert r.returncode == 0, r.stderr
+    got = json.load(open(out / "report.json"))["points"][0]["summary"]
+    p = make_point(policy="accellm", instances=8, rate=30.0, num_requests=1500, workload="heavy", reserve=0.5,
+                   seed=4, timer_s=0.1, degraded=True, trigger_ticks=1, leveling=True)
+    ref = run_oracle(p, ev_cap=0, recs=False).summary
+    assert got["n_mode_switches"] == ref.n_mode_switches > 0
+    assert got["link_leveling_tokens"] == ref.link_leveling_tokens
+    assert got["jct_mean"] == ref.jct_mean and got["n_events"] == ref.n_events
