@@ -208,6 +208,10 @@ int kvsim_gpu_reserve(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
                       char* err, size_t err_len);
 /* Kernel launches issued by the last run (for the bench's gpu_launches). */
 int64_t kvsim_gpu_last_launches(const kvsim_gpu_ctx* ctx);
+/* Profiling hook (no reference counterpart): when the context was opened with
+ * KVSIM_POINT_TIMES set, copies {start_ns, end_ns, warp slot} per point of the
+ * last kvsim_gpu_run into out (up to cap values); returns values copied. */
+int64_t kvsim_gpu_point_times(kvsim_gpu_ctx* ctx, uint64_t* out, int64_t cap);
 
 /* Bulk perfmodel evaluation on the device (K1). For each i:
  *   op[i]==0 prefill_latency(s1[i]=sum L, s2[i]=sum L^2)

@@ -54,6 +54,8 @@ def load_library() -> C.CDLL:
     L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]
     L.kvsim_gpu_last_launches.argtypes = [C.c_void_p]
     L.kvsim_gpu_last_launches.restype = C.c_int64
+    L.kvsim_gpu_point_times.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
+    L.kvsim_gpu_point_times.restype = C.c_int64
     L.kvsim_gpu_perf_batch.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                        C.POINTER(C.c_double), C.c_size_t, C.c_char_p, C.c_size_t]
@@ -132,6 +134,13 @@ class KvSim:
 
     def last_launches(self) -> int:
         return int(self.lib.kvsim_gpu_last_launches(self.h))
+
+    def point_times(self, n: int):
+        """Profiling: [(start_ns, end_ns, slot)] per point of the last run
+        (context opened with KVSIM_POINT_TIMES set), else []."""
+        buf = (C.c_uint64 * (3 * n))()
+        k = int(self.lib.kvsim_gpu_point_times(self.h, buf, 3 * n))
+        return [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(max(k, 0) // 3)]
 
     def perf_batch(self, points, pidx, ops, s1, s2):
         n = len(pidx)

@@ -92,6 +92,8 @@ struct SweepArgs {
   kvsim_event_record* ev;
   int64_t ev_cap;
   int64_t* ev_count;
+  // optional profiling: per point {start ns, end ns, slot} (globaltimer)
+  unsigned long long* ptime;
   // arena geometry
   int64_t Ncap, Bcap, Jcap;
   int32_t Imax, slots;
@@ -2519,6 +2521,13 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
     const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
     const int32_t pol = a.pts[pt].policy;
     const bool ext = pol == KVSIM_POLICY_ACCELLM && (a.pts[pt].accellm_flags & 3) != 0;
+#if !defined(KVSIM_EMU)
+    if (a.ptime != nullptr && lane == 0) {  // stored at once: no register live across the point
+      unsigned long long t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      a.ptime[3 * pt] = t0;
+    }
+#endif
     if (ext) {
       if (a.ev != nullptr) run_point<KVSIM_POLICY_ACCELLM, true, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_ACCELLM, false, true>(ap, w, slot, pt);
@@ -2531,6 +2540,14 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
       else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, false>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_UNIFIED, false>(ap, w, slot, pt);
     }
+#if !defined(KVSIM_EMU)
+    if (a.ptime != nullptr && lane == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      a.ptime[3 * pt + 1] = t1;
+      a.ptime[3 * pt + 2] = (unsigned long long)slot;
+    }
+#endif
   }
 }
 

@@ -122,7 +122,9 @@ struct kvsim_gpu_ctx {
   int sms = 0;
   int blocks_per_sm = 1;
   cudaStream_t stream = nullptr;
-  DevBuf arena, pts, order, out, recs, rec_off, ev, ev_count, tr_arr, tr_pl, tr_dl, tr_off, tr_n, tr_dmax, counter;
+  DevBuf arena, pts, order, out, recs, rec_off, ev, ev_count, tr_arr, tr_pl, tr_dl, tr_off, tr_n, tr_dmax, counter, ptime;
+  bool point_times = false;  // KVSIM_POINT_TIMES: record per-point start/end (profiling)
+  int64_t ptime_n = 0;
   kvsim_host::ArenaGeom geom;
   int32_t slots = 0;
   SweepArgs reserved_args{};
@@ -257,6 +259,7 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   c->minb = kDefaultMinBlocks;
   if (const char* e = std::getenv("KVSIM_MINB")) c->minb = std::atoi(e);
   c->kernel = sweep_variant(c->minb);
+  c->point_times = std::getenv("KVSIM_POINT_TIMES") != nullptr;
   KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
   int bps = 1;
   KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
@@ -275,7 +278,7 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
 void kvsim_gpu_close(kvsim_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  for (DevBuf* b : {&c->arena, &c->pts, &c->order, &c->out, &c->recs, &c->rec_off, &c->ev, &c->ev_count, &c->tr_arr,
+  for (DevBuf* b : {&c->arena, &c->pts, &c->order, &c->out, &c->recs, &c->rec_off, &c->ev, &c->ev_count, &c->ptime, &c->tr_arr,
                     &c->tr_pl, &c->tr_dl, &c->tr_off, &c->tr_n, &c->tr_dmax, &c->counter})
     b->release();
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -283,6 +286,13 @@ void kvsim_gpu_close(kvsim_gpu_ctx* c) {
 }
 
 int64_t kvsim_gpu_last_launches(const kvsim_gpu_ctx* c) { return c ? c->last_launches : 0; }
+
+int64_t kvsim_gpu_point_times(kvsim_gpu_ctx* c, uint64_t* out, int64_t cap) {
+  if (!c || !c->point_times || c->ptime_n == 0) return 0;
+  const int64_t n = std::min<int64_t>(cap, 3 * c->ptime_n);
+  if (cudaMemcpy(out, c->ptime.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return n;
+}
 
 int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const kvsim_trace_view* traces,
                   size_t n_traces, kvsim_point_summary* out, kvsim_request_record* recs, kvsim_event_record* ev,
@@ -373,6 +383,11 @@ int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const
   a.ev_cap = (int64_t)ev_cap;
   a.ev_count = (ev && ev_cap) ? (int64_t*)c->ev_count.p : nullptr;
   a.next_point = (unsigned long long*)c->counter.p;
+  if (c->point_times) {
+    KV_CUDA(c->ptime.ensure(sizeof(unsigned long long) * 3 * n));
+    a.ptime = (unsigned long long*)c->ptime.p;
+    c->ptime_n = (int64_t)n;
+  }
   rc = launch_sweep(c, a, s, err, err_len);
   if (rc) return rc;
   KV_CUDA(cudaMemcpyAsync(out, c->out.p, sizeof(kvsim_point_summary) * n, cudaMemcpyDeviceToHost, s));
