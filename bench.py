@@ -57,6 +57,16 @@ def algorithmic_bytes(summaries):
     return 40 * n + 8 * (tok - n)
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the config-4 sweep kernel from the committed ncu
+    capture (profiles/r1_ncu_bench_kernel.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r1_ncu_bench_kernel.json")
+    try:
+        return float(json.load(open(p))["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -156,6 +166,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     n_cpu = os.cpu_count() or 1
     metric = "simulated requests/sec (sweep, 1-8 B200) vs ref CPU; HBM GB/s fraction"
+    workload_is_config4 = args.rates == 833 and args.requests == 10000
     workload = (f"BASELINE config 4: 3 policies x instances {{4,8,12,16}} x {args.rates} rates in (0,3N] req/s, "
                 f"{args.requests} requests/point, mixed, Llama-2-70B on simulated H100")
 
@@ -282,7 +293,10 @@ def main():
             "events_per_step_per_gpu": events,
             "failed_points": bad,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"),
-                         "unit": "GB/s", "frac": achieved / peaks.get("hbm_gbs"), "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peaks.get("hbm_gbs"),
+                         "traffic": ncu_traffic() if workload_is_config4 else None,
+                         "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                         "profiles/r1_ncu_bench_kernel.json)",
                          "peak_source": src,
                          "algorithmic_bytes_per_launch": bytes_alg,
                          "note": "algorithmic bytes per SURVEY §8d (40 B/request + 8 B/decode iteration); "

@@ -37,9 +37,10 @@ def load_library() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise KvSimError(f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
-    L = C.CDLL(LIB_PATH)
+    path = os.environ.get("KVSIM_LIB", LIB_PATH)  # build-variant experiments (tools/)
+    if not os.path.exists(path):
+        raise KvSimError(f"CUDA library not built: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
     L.kvsim_gpu_abi_version.restype = C.c_int
     L.kvsim_gpu_device_count.restype = C.c_int
     L.kvsim_gpu_open.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]

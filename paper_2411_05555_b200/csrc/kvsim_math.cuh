@@ -39,9 +39,15 @@ KV_HD double kmul(double a, double b) {
   return a * b;
 #endif
 }
+#if defined(__CUDACC__)
+// One out-of-line copy of the IEEE division: inlined, __ddiv_rn's ~40-instruction
+// sequence was replicated at ~100 call sites and the hot loop's code no longer
+// fit the SM instruction cache (ncu: sm__icc_request_hit_rate 63%).
+__device__ __noinline__ inline double kdiv_ool(double a, double b) { return __ddiv_rn(a, b); }
+#endif
 KV_HD double kdiv(double a, double b) {
 #if defined(__CUDA_ARCH__)
-  return __ddiv_rn(a, b);
+  return kdiv_ool(a, b);
 #else
   return a / b;
 #endif

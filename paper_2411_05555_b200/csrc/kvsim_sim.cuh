@@ -1021,7 +1021,12 @@ struct Sim {
       {
         const int32_t pj = simt::shfl(L_job, pl), pp = simt::shfl(L_pend, pl);
         const int32_t qn = simt::shfl(Q_n, (lane >> 1) & 31);
-        const bool cand = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qn == 0 &&
+        const int32_t pr = simt::shfl(L_role, pl);
+        // a queued prompt only matters at a boundary while neither member
+        // prefills (ensure_prefill); with one member in the prefill role the
+        // other's boundaries ignore the queue and its prefill end bounds the chain
+        const bool qok = qn == 0 || L_role == ROLE_PREFILL || pr == ROLE_PREFILL;
+        const bool cand = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qok &&
                           !L_pend && !pp && (L_job == JOB_STEP || pj == JOB_STEP);
         if (simt::ballot(cand) == 0) return;
       }
@@ -1045,7 +1050,8 @@ struct Sim {
       const double bcomp = simt::shfl(L_comp, pl);
       b.mr = b.ni > 0 ? bmr : kInf;
       b.tw = 0; b.steps = 0;
-      const bool drv = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qn_pair == 0 &&
+      const bool drv = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) &&
+                       (qn_pair == 0 || L_role == ROLE_PREFILL || b.role == ROLE_PREFILL) &&
                        !L_pend && !bpend && (L_job == JOB_STEP || b.stepping);
       MemberChain a;
       a.stepping = L_job == JOB_STEP;
@@ -1118,7 +1124,18 @@ struct Sim {
         L_copy_tok = bct;
       }
     }
-    if (steps > 0) {  // divergent: only lanes that advanced touch the counters
+    const unsigned am = simt::ballot(steps > 0);
+    if (am != 0 && (am & (am - 1)) == 0) {  // one chain advanced (the common case): plain adds
+      if (steps > 0) {
+        Counters& ct = ws()->ct;
+        ct.adv_events += steps;
+        ct.n_steps += steps;
+        ct.tok_total += tok;
+        ct.tok_window += tw;
+        ct.mir_tokens += mir;
+        if (tmax > L_tlast) L_tlast = tmax;
+      }
+    } else if (steps > 0) {  // divergent: only lanes that advanced touch the counters
       simt::atomic_add_smem(&ws()->ct.adv_events, steps);
       simt::atomic_add_smem(&ws()->ct.n_steps, steps);
       simt::atomic_add_smem(&ws()->ct.tok_total, tok);

@@ -131,13 +131,13 @@ struct kvsim_gpu_ctx {
   bool reserved = false;
   int64_t last_launches = 0;
   void (*kernel)(SweepArgs) = nullptr;
-  int minb = 2;
+  int minb = 3;
 };
 
 namespace {
 
 using SweepFn = void (*)(SweepArgs);
-constexpr int kDefaultMinBlocks = 2;
+constexpr int kDefaultMinBlocks = 3;
 SweepFn sweep_variant(int minb) {
   // occupancy is not the limiter (instruction fetch is):
   // 1-6 blocks/SM measured within 10% of each other, so two variants ship
