@@ -933,6 +933,45 @@ int cmd_main(const Args& a) {
     write_file(a.out + "/resource_sweep.csv", rc);
     report.set("knees", resource_knees(meta, r.sum));
   }
+  if (ev_cap) {
+    // queue-depth time series (SPEC.md:358 MetricsReport diagnostics), rebuilt
+    // from the event log: +1 per arrival and per preemption (the request
+    // re-enters its queue), minus the prompts a prefill job (unified: a
+    // co-batched iteration) takes. One row per timestamp with the depth after
+    // all of that timestamp's events; report.json gets max and time average.
+    std::string qd = "point,t,depth\n";
+    jl::Value& pl = *const_cast<jl::Value*>(report.find("points"));
+    for (size_t i = 0; i < pts.size(); ++i) {
+      const int64_t k = std::min<int64_t>(r.ev_cnt[i], (int64_t)ev_cap);
+      std::vector<std::pair<double, int64_t>> dv;
+      for (int64_t j = 0; j < k; ++j) {
+        const kvsim_event_record& e = r.ev[i * ev_cap + j];
+        if (e.kind == KVSIM_EV_ARRIVE || e.kind == KVSIM_EV_PREEMPT) dv.push_back({e.t, 1});
+        else if (e.kind == KVSIM_EV_PREFILL_START) dv.push_back({e.t, -(int64_t)e.a});
+        else if (e.kind == KVSIM_EV_STEP_START && pts[i].policy == KVSIM_POLICY_UNIFIED && e.b > 0)
+          dv.push_back({e.t, -(int64_t)e.b});
+      }
+      std::stable_sort(dv.begin(), dv.end(), [](auto& x, auto& y) { return x.first < y.first; });
+      int64_t depth = 0, dmax = 0;
+      double area = 0, tprev = 0;
+      for (size_t j = 0; j < dv.size();) {
+        const double t = dv[j].first;
+        area += (double)depth * (t - tprev);
+        tprev = t;
+        for (; j < dv.size() && dv[j].first == t; ++j) depth += dv[j].second;
+        dmax = std::max(dmax, depth);
+        qd += std::to_string(i) + "," + num(t) + "," + std::to_string(depth) + "\n";
+      }
+      const double span = r.sum[i].makespan_s;
+      if (span > tprev) area += (double)depth * (span - tprev);
+      jl::Value q = jl::Value::object();
+      q.set("max", jl::Value::number((double)dmax));
+      q.set("time_avg", span > 0 ? jl::Value::number(area / span) : jl::Value());
+      q.set("truncated", jl::Value::boolean(r.ev_cnt[i] > (int64_t)ev_cap));
+      pl.arr[i].set("queue_depth", q);
+    }
+    write_file(a.out + "/queue_depth.csv", qd);
+  }
   write_file(a.out + "/report.json", jl::dump(report) + "\n");
   write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
   if (ev_cap) {

@@ -226,3 +226,54 @@ def test_run_accellm_extensions_match_oracle(kvsim, tmp_path):
     assert got["n_mode_switches"] == ref.n_mode_switches > 0
     assert got["link_leveling_tokens"] == ref.link_leveling_tokens
     assert got["jct_mean"] == ref.jct_mean and got["n_events"] == ref.n_events
+
+
+def _queue_series(events, unified):
+    """Reference restatement of the CLI's queue-depth rule over an event log."""
+    dv = {}
+    for e in events:
+        d = 0
+        if e.kind in (1, 8):          # ARRIVE, PREEMPT
+            d = 1
+        elif e.kind == 2:             # PREFILL_START: a prompts admitted
+            d = -e.a
+        elif e.kind == 4 and unified and e.b > 0:  # co-batched prompts
+            d = -e.b
+        if d:
+            dv[e.t] = dv.get(e.t, 0) + d
+    out, depth = [], 0
+    for t in sorted(dv):
+        depth += dv[t]
+        out.append((t, depth))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["accellm", "splitwise", "unified"])
+def test_queue_depth_series(kvsim, tmp_path, policy):
+    cfg = {"model": "llama2-70b", "device": "h100", "instances": 4, "policy": policy, "rate": 6.0,
+           "num_requests": 400, "workload": "light", "seed": 5, "warmup_s": 0}
+    out = tmp_path / "q"
+    r = run(kvsim, "run", "--config", write(tmp_path, "c.json", cfg), "--out", str(out), "--emit-events")
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.DictReader(open(out / "queue_depth.csv")))
+    got = [(float(x["t"]), int(x["depth"])) for x in rows]
+    p = make_point(model="llama2-70b", device="h100", policy=policy, instances=4, rate=6.0, num_requests=400,
+                   workload="light", seed=5, warmup_s=0.0)
+    ref = run_oracle(p, ev_cap=1 << 18)
+    want = _queue_series(ref.events, policy == "unified")
+    assert got == want
+    assert all(d >= 0 for _, d in got) and got[-1][1] == 0
+    q = json.load(open(out / "report.json"))["points"][0]["queue_depth"]
+    assert q["max"] == max(d for _, d in got) and not q["truncated"]
+
+
+@pytest.mark.parametrize("policy", ["accellm", "splitwise", "unified"])
+def test_queue_depth_rule_on_oracle(policy):
+    # the queue-depth rule balances: never negative, empty once every request ran
+    p = make_point(model="llama2-70b", device="h100", policy=policy, instances=4, rate=8.0, num_requests=300,
+                   workload="light", seed=9, warmup_s=0.0)
+    ref = run_oracle(p, ev_cap=1 << 18)
+    s = _queue_series(ref.events, policy == "unified")
+    assert s and all(d >= 0 for _, d in s) and s[-1][1] == 0
+    assert max(d for _, d in s) > 0
