@@ -900,24 +900,12 @@ struct Sim {
     double Wb, kvb, mden, mrcp, warmup;
     int64_t cap;
   };
-  KV_DEV bool pair_step(MemberChain& c, MemberChain& o, int cid, const double ht, const int32_t hk,
-                        const ChainK& K, int64_t& budget) {
-    const int64_t cap = K.cap;
-    const double warmup = K.warmup;
-    if (!(c.e < ht || (c.e == ht && 3 * 64 + cid < hk))) return false;
-    if (c.minrem < 2 || c.e >= c.mr || budget <= 0) return false;
-    if (o.role == ROLE_DECODE && c.kvmin != INT64_MAX) {  // rebalance_pair at cid's next boundary
-      const int64_t cz = (int64_t)c.B + c.ni - o.B - o.ni;
-      if (cz >= 1) {
-        const int64_t dz = (c.skv + c.skv_in + c.B) - (o.skv + o.skv_in);
-        const int64_t lim = cz >= 2 ? dz : dz - 1;
-        if (c.kvmin + 1 <= lim) return false;
-      }
-    }
-    if (c.used + c.B > cap || o.used + c.m > cap) return false;
+  // one virtual step end of a chained pair member (bookkeeping only; the
+  // caller has evaluated the stop tests)
+  KV_DEV void lean_step(MemberChain& c, const ChainK& K, int cid) {
     const double e = c.e;
-    if (c.js >= warmup) c.busy = kadd(c.busy, ksub(e, c.js));
-    if (e >= warmup) c.tw += c.B;
+    if (c.js >= K.warmup) c.busy = kadd(c.busy, ksub(e, c.js));
+    if (e >= K.warmup) c.tw += c.B;
     if (c.dj == 0) { c.de1 = e; c.dpe = c.prev; }
     else { const double g = ksub(e, c.prev); if (g > c.dG) c.dG = g; }
     if (c.m > 0) {
@@ -928,23 +916,13 @@ struct Sim {
     }
     if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, cid, c.B, 0, 0);
     c.skv += c.B;
-    c.used += c.B;
-    if (c.used > c.peak) c.peak = c.used;
-    o.used += c.m;
-    o.copy_tok += c.m;
-    if (o.used > o.peak) o.peak = o.used;
     if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv);
     c.prev = e;
     c.js = e;
     c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul((double)c.skv, K.kvb)), K.mden, K.mrcp), c.comp));
     c.dj += 1;
-    c.minrem -= 1;
-    if (c.kvmin != INT64_MAX) c.kvmin += 1;
     c.steps += 1;
-    budget -= 1;
-    return true;
   }
-
   // drive: bitmask of lanes allowed to advance (instances; AcceLLM: any lane
   // of a pair selects the pair)
   KV_DEV_NOINLINE void advance(unsigned drive) {
@@ -1086,12 +1064,53 @@ struct Sim {
         b.mlat = transfer_latency(PC.f, kmul((double)b.m, PC.f.kvb));
         if (!a.stepping) a.B = 0;
         const ChainK K{PC.f.W, PC.f.kvb, PC.f.mem_den, PC.f.mem_rcp, warmup, cap};
+        // Incremental form of pair_step's stop tests: remaining-token and
+        // event budgets as counters, KV slack per member (own steps take B,
+        // the partner's steps take its mirror lines m), and the rebalance
+        // test as a gap G = lim - (kvmin + 1) that grows by B - 1 per own
+        // step and shrinks by the partner's B per partner step (stop at
+        // G >= 0). The KV ledgers are applied once after the loop (they only
+        // grow during a chain, so the peaks are the final values).
+        constexpr int64_t kOff = INT64_MIN / 4;  // rebalance test disabled
+        int64_t GA = kOff, GB = kOff;
+        {
+          const int64_t cza = (int64_t)a.B + a.ni - b.B - b.ni, czb = (int64_t)b.B + b.ni - a.B - a.ni;
+          const int64_t dza = (a.skv + a.skv_in + a.B) - (b.skv + b.skv_in);
+          const int64_t dzb = (b.skv + b.skv_in + b.B) - (a.skv + a.skv_in);
+          if (b.role == ROLE_DECODE && a.kvmin != INT64_MAX && cza >= 1) GA = (cza >= 2 ? dza : dza - 1) - (a.kvmin + 1);
+          if (a.role == ROLE_DECODE && b.kvmin != INT64_MAX && czb >= 1) GB = (czb >= 2 ? dzb : dzb - 1) - (b.kvmin + 1);
+        }
+        int64_t SA = cap - a.used, SB = cap - b.used;
+        int32_t rA = a.minrem - 1, rB = b.minrem - 1;
+        const int32_t kA = 3 * 64 + lane, kB = kA + 1;
         for (;;) {
-          const bool pickA = a.stepping && (!b.stepping || !(b.e < a.e));  // ties: lower id (even lane)
-          bool ok;
-          if (pickA) ok = pair_step(a, b, lane, pht, phk, K, budget);
-          else ok = b.stepping && pair_step(b, a, lane + 1, pht, phk, K, budget);
-          if (!ok) break;
+          if (a.stepping && (!b.stepping || !(b.e < a.e))) {  // ties: lower id (even lane)
+            const double e = a.e;
+            if (!(e < pht || (e == pht && kA < phk)) || e >= a.mr || rA <= 0 || budget <= 0 || GA >= 0 ||
+                SA < a.B || SB < a.m)
+              break;
+            lean_step(a, K, lane);
+            rA -= 1; SA -= a.B; SB -= a.m; GA += a.B - 1; GB -= a.B;
+          } else {
+            const double e = b.e;
+            if (!b.stepping || !(e < pht || (e == pht && kB < phk)) || e >= b.mr || rB <= 0 || budget <= 0 ||
+                GB >= 0 || SB < b.B || SA < b.m)
+              break;
+            lean_step(b, K, lane + 1);
+            rB -= 1; SB -= b.B; SA -= b.m; GB += b.B - 1; GA -= b.B;
+          }
+          budget -= 1;
+        }
+        {
+          const int64_t ua = (int64_t)a.steps * a.B + (int64_t)b.steps * b.m;
+          const int64_t ub = (int64_t)b.steps * b.B + (int64_t)a.steps * a.m;
+          a.used += ua; b.used += ub;
+          a.copy_tok += (int64_t)b.steps * b.m; b.copy_tok += (int64_t)a.steps * a.m;
+          if (a.used > a.peak) a.peak = a.used;
+          if (b.used > b.peak) b.peak = b.used;
+          a.minrem -= a.steps; b.minrem -= b.steps;
+          if (a.kvmin != INT64_MAX) a.kvmin += a.steps;
+          if (b.kvmin != INT64_MAX) b.kvmin += b.steps;
         }
         if (!a.stepping) a.B = L_nb;
         steps = a.steps + b.steps;
