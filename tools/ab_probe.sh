@@ -1,0 +1,2 @@
+# A/B of variants/*.so on one box: config-4 sweep wall time, alternating, 2 rounds
+for r in 1 2; do for f in variants/*.so; do KVSIM_LIB=$f python tools/occupancy_probe.py 2>&1 | sed "s#^#$(basename $f) #" >> gpurun_out/ab.log; done; done

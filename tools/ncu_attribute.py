@@ -12,11 +12,14 @@ import collections, csv, re, sys
 
 
 def main(sass_csv, dis_txt, sim_cuh):
+    rows = list(csv.reader(open(sass_csv)))
+    minb = re.search(r"kvsim_sweep_kernel<\(int\)(\d+)>", rows[0][1]).group(1)
+    tag = f"ILi{minb}EE"
     dis = open(dis_txt).read().split("\n")
-    start = [i for i, l in enumerate(dis) if l.startswith(".text._Z18kvsim_sweep_kernelILi2EE")][0]
+    start = [i for i, l in enumerate(dis) if l.startswith(".text._Z18kvsim_sweep_kernel" + tag)][0]
     off2src, cur = {}, None
     for l in dis[start:]:
-        if l.startswith("//----") and "ILi2" not in l:
+        if l.startswith("//----") and tag not in l:
             break
         m = re.match(r'\s*//## File "(.*)", line (\d+)', l)
         if m:
@@ -45,7 +48,6 @@ def main(sass_csv, dis_txt, sim_cuh):
                 break
         return name
 
-    rows = list(csv.reader(open(sass_csv)))
     hdr = rows[1]
     ia, ie = hdr.index("Address"), hdr.index("Instructions Executed")
     iss, ino = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("stall_no_inst")

@@ -28,3 +28,7 @@ print("busy by (policy,N)", {k: round(v / busy, 3) for k, v in sorted(byn.items(
 durs = sorted(((b - a) / 1e9, i) for i, (a, b, c) in enumerate(pt))
 print("longest points", [(round(d, 3), pts[i].policy, pts[i].num_instances, round(pts[i].rate, 2)) for d, i in durs[-8:]])
 print("point time quantiles", [round(durs[int(q*(len(durs)-1))][0], 4) for q in (0.1, 0.5, 0.9, 0.99)])
+if len(sys.argv) > 2:
+    import json
+    json.dump([{"policy": p.policy, "n": p.num_instances, "rate": p.rate, "start": (a - T0) / 1e9, "dur": (b - a) / 1e9,
+                "slot": c} for p, (a, b, c) in zip(pts, pt)], open(sys.argv[2], "w"))
