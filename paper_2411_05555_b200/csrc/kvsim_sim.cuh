@@ -447,6 +447,10 @@ struct Sim {
     StepOut o;
     const int32_t nb = get(L_nb, x);
     const double prev = get(L_prev_end, x);
+    // chained steps not yet applied (advance/flush) are applied in the same
+    // pass: remaining tokens -dj, TBT max with the deferred gaps
+    const int32_t dj = get(L_dj, x);
+    const double e1 = get(L_de1, x), pe = get(L_dpe, x), G = get(L_dG, x);
     int32_t* rid_a = b_rid(x);
     int32_t* rem_a = b_rem(x);
     int32_t* kvb_a = b_kvb(x);
@@ -462,22 +466,28 @@ struct Sim {
         rf = rem_a[j];
         tb = tbt_a[j];
       }
-      const int32_t rem = (rf & kRemMask) - 1;
-      const bool joiner = (rf & kJoin) != 0;
+      const int32_t rem = (rf & kRemMask) - dj - 1;
+      const bool was_joiner = (rf & kJoin) != 0;
+      const bool joiner = was_joiner && dj == 0;  // no step since joining
       const bool hasc = (rf & kCopy) != 0;
       const bool done = act && rem == 0;
       const bool surv = act && rem != 0;
       const unsigned sm = simt::ballot(surv);
       const int32_t dst = wpos + simt::popc(sm & simt::lanemask_lt());
       const bool moved = surv && dst != j;
-      if (act && (joiner || done || moved)) rid = rid_a[j];
+      if (act && (was_joiner || done || moved)) rid = rid_a[j];
       double gap = 0.0;
       bool upd = false;
       if (act) {
+        if (dj > 0) {
+          const double last0 = was_joiner ? c_last()[rid] : pe;
+          double g1 = ksub(e1, last0);
+          if (G > g1) g1 = G;
+          if (g1 > tb) { tb = g1; upd = true; }
+        }
         const double last = joiner ? c_last()[rid] : prev;
         gap = ksub(t, last);
-        upd = gap > tb;
-        if (upd) tb = gap;
+        if (gap > tb) { tb = gap; upd = true; }
       }
       if (done || moved) kvb = kvb_a[j];
       m += simt::popc(simt::ballot(act && hasc));
@@ -519,6 +529,7 @@ struct Sim {
     o.minrem = simt::warp_min_i32(minrem);
     o.kvmin = simt::warp_min_i64(kvmin);
     simt::sync();
+    if (own(x) && dj > 0) { L_dj = 0; L_dG = 0.0; }
     return o;
   }
 
@@ -812,8 +823,7 @@ struct Sim {
     EMU_COUNT(3);
     account_job(x, t);
     if (lane == 0) ws()->ct.n_steps += 1;
-    flush(x);
-    const StepOut o = step_loop(x, t);
+    const StepOut o = step_loop(x, t);  // applies the deferred chained steps too
     const int32_t surv = o.nb_old - o.completed;
     if (own(x)) {
       L_job = JOB_NONE;
@@ -1222,8 +1232,7 @@ struct Sim {
     EMU_COUNT(18);
     account_job(x, t);
     if (lane == 0) ws()->ct.n_steps += 1;
-    flush(x);
-    const StepOut o = step_loop(x, t);
+    const StepOut o = step_loop(x, t);  // applies the deferred chained steps too
     int32_t nb = o.nb_old - o.completed;
     int64_t skv = get(L_skv, x) - o.kv_done + nb;
     int64_t freed = o.kv_done + o.completed;
