@@ -24,6 +24,7 @@
  *                             transfer_latency / kv_capacity_tokens
  *                             (perfmodel.hpp:84-106) evaluated in bulk
  *   kvsim_gpu_gen_trace   <- generate_trace
+ *   kvsim_gpu_host_alloc  <- load_trace's buffers, pinned
  *
  * Errors: every entry point returns 0 on success or a negative KVSIM_E_* code
  * with a message in `err` (SPEC.md:69,78,96,416 messages are preserved).
@@ -228,6 +229,16 @@ int kvsim_gpu_perf_batch(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t
 int kvsim_gpu_gen_trace(kvsim_gpu_ctx* ctx, const kvsim_point_desc* p, double* arrival_s,
                         int32_t* prompt_len, int32_t* decode_len, int64_t* n_out,
                         char* err, size_t err_len);
+
+/* Page-locked host memory for bulk trace ingestion (load_trace,
+ * SPEC.md:164-172). A caller that parses a large external
+ * trace straight into these buffers gets DMA-speed, asynchronous host-to-device
+ * copies of traces[] inside kvsim_gpu_run instead of staged pageable copies.
+ * Returns NULL when page-locked memory is unavailable (no CUDA device, or the
+ * allocation failed); the caller then uses ordinary memory. Free with
+ * kvsim_gpu_host_free (NULL is a no-op). */
+void* kvsim_gpu_host_alloc(size_t bytes);
+void kvsim_gpu_host_free(void* p);
 
 #ifdef __cplusplus
 }

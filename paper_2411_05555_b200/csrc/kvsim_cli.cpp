@@ -16,6 +16,7 @@
 // {"error": ...} line on stderr.
 #include <algorithm>
 #include <atomic>
+#include <charconv>
 #include <cerrno>
 #include <cstdarg>
 #include <cmath>
@@ -396,41 +397,211 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
 }
 
 // ------------------------------------------------------------------ traces
-struct Trace {
-  std::vector<double> arr;
-  std::vector<int32_t> pl, dl;
-};
-Trace load_trace(const std::string& path) {
-  // header `#kvsim-trace v1`, rows id,arrival_s,prompt_len,decode_len
-  std::ifstream f(path);
-  if (!f) throw ConfigError("cannot open trace " + path);
-  std::string line;
-  size_t ln = 0;
-  Trace t;
-  if (!std::getline(f, line) || line.rfind("#kvsim-trace v1", 0) != 0)
-    throw ConfigError(path + ":1: missing '#kvsim-trace v1' header");
-  ln = 1;
-  double prev = -INFINITY;
-  while (std::getline(f, line)) {
-    ++ln;
-    if (!line.empty() && line.back() == '\r') line.pop_back();
-    if (line.empty() || line[0] == '#') continue;
-    if (line.rfind("id,", 0) == 0) continue;  // optional column header
-    long long id;
-    double a;
-    long long p, d;
-    char tail;
-    if (std::sscanf(line.c_str(), "%lld,%lf,%lld,%lld%c", &id, &a, &p, &d, &tail) != 4)
-      throw ConfigError(path + ":" + std::to_string(ln) + ": parse error");
-    if ((size_t)id != t.arr.size()) throw ConfigError(path + ":" + std::to_string(ln) + ": ids must be 0..n-1 in order");
-    if (a < prev) throw ConfigError(path + ":" + std::to_string(ln) + ": arrival_s decreases");
-    if (p < 1 || d < 1 || p > (1 << 30) || d > (1 << 28))
-      throw ConfigError(path + ":" + std::to_string(ln) + ": lengths out of range");
-    prev = a;
-    t.arr.push_back(a);
-    t.pl.push_back((int32_t)p);
-    t.dl.push_back((int32_t)d);
+// Host array in page-locked memory when the library can provide it
+// (kvsim_gpu_host_alloc), else ordinary memory: traces parsed straight into
+// it are DMA'd to the device inside kvsim_gpu_run without a staging copy.
+template <class T>
+class HostArray {
+ public:
+  HostArray() = default;
+  HostArray(const HostArray&) = delete;
+  HostArray& operator=(const HostArray&) = delete;
+  HostArray(HostArray&& o) noexcept { swap(o); }
+  HostArray& operator=(HostArray&& o) noexcept { swap(o); return *this; }
+  ~HostArray() { release(); }
+  size_t size() const { return n_; }
+  bool empty() const { return n_ == 0; }
+  T* data() { return p_; }
+  const T* data() const { return p_; }
+  T& operator[](size_t i) { return p_[i]; }
+  const T& operator[](size_t i) const { return p_[i]; }
+  bool pinned() const { return pinned_; }
+  void resize(size_t n) {  // keeps the first min(n, size()) elements
+    if (n <= cap_) { n_ = n; return; }
+    HostArray t;
+    t.alloc(n);
+    if (n_) std::memcpy(t.p_, p_, n_ * sizeof(T));
+    t.n_ = n;
+    swap(t);
   }
+
+ private:
+  void alloc(size_t n) {
+    p_ = static_cast<T*>(kvsim_gpu_host_alloc(n * sizeof(T)));
+    pinned_ = p_ != nullptr;
+    if (!p_) p_ = static_cast<T*>(std::malloc(n * sizeof(T)));
+    if (!p_) throw std::bad_alloc();
+    cap_ = n;
+  }
+  void release() {
+    if (p_) { if (pinned_) kvsim_gpu_host_free(p_); else std::free(p_); }
+    p_ = nullptr; n_ = cap_ = 0; pinned_ = false;
+  }
+  void swap(HostArray& o) {
+    std::swap(p_, o.p_); std::swap(n_, o.n_); std::swap(cap_, o.cap_); std::swap(pinned_, o.pinned_);
+  }
+  T* p_ = nullptr;
+  size_t n_ = 0, cap_ = 0;
+  bool pinned_ = false;
+};
+
+struct Trace {
+  HostArray<double> arr;
+  HostArray<int32_t> pl, dl;
+};
+
+namespace trace_io {
+// One row `id,arrival_s,prompt_len,decode_len`. Numbers may
+// be preceded by blanks or '+', as the scanf-based reader accepted; doubles go
+// through std::from_chars, which rounds correctly like strtod.
+inline const char* skip_blank(const char* p, const char* e) {
+  while (p < e && (*p == ' ' || *p == '\t')) ++p;
+  return p;
+}
+inline bool int_field(const char*& p, const char* e, long long& v) {
+  p = skip_blank(p, e);
+  if (p < e && *p == '+') ++p;
+  auto r = std::from_chars(p, e, v);
+  if (r.ec != std::errc()) return false;
+  p = r.ptr;
+  return true;
+}
+inline bool row(const char* p, const char* e, long long& id, double& a, long long& pl, long long& dl) {
+  if (!int_field(p, e, id) || p >= e || *p++ != ',') return false;
+  p = skip_blank(p, e);
+  if (p < e && *p == '+') ++p;
+  auto r = std::from_chars(p, e, a);
+  if (r.ec != std::errc()) return false;
+  p = r.ptr;
+  if (p >= e || *p++ != ',' || !int_field(p, e, pl) || p >= e || *p++ != ',' || !int_field(p, e, dl)) return false;
+  return p == e;
+}
+struct Chunk {
+  const char* b;
+  const char* e;
+  size_t first_line = 0, lines = 0, first_row = 0, rows = 0;
+  size_t err_line = 0;  // 0 = none
+  std::string err;
+  size_t first_row_line = 0;  // line of the first data row
+  bool first_ok = false;      // ... and it parsed and passed the local checks
+  double first_a = 0, last_a = 0;
+};
+// is this line a data row? (comments, blank lines and an optional column header are not)
+inline bool is_row(const char* p, const char* e) {
+  if (p < e && e[-1] == '\r') --e;
+  return !(p == e || *p == '#' || (e - p >= 3 && std::memcmp(p, "id,", 3) == 0));
+}
+}  // namespace trace_io
+
+Trace load_trace(const std::string& path) {
+  // header `#kvsim-trace v1`, rows id,arrival_s,prompt_len,decode_len;
+  // errors name the line. Bulk ingestion: the file is read
+  // once, split at line boundaries and parsed by all host threads straight into
+  // page-locked arrays; the first error in file order is reported.
+  using namespace trace_io;
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw ConfigError("cannot open trace " + path);
+  std::string buf;
+  {
+    char tmp[1 << 16];
+    size_t k;
+    while ((k = std::fread(tmp, 1, sizeof tmp, f)) > 0) buf.append(tmp, k);
+    std::fclose(f);
+  }
+  const char* B = buf.data();
+  const char* E = B + buf.size();
+  const char* nl = static_cast<const char*>(std::memchr(B, '\n', buf.size()));
+  const char* body = nl ? nl + 1 : E;
+  if (buf.rfind("#kvsim-trace v1", 0) != 0) throw ConfigError(path + ":1: missing '#kvsim-trace v1' header");
+  const size_t bytes = (size_t)(E - body);
+  size_t nt = std::max(1u, std::thread::hardware_concurrency());
+  nt = std::min<size_t>({nt, 64, bytes / (1 << 20) + 1});  // ~1 MB or more per thread
+  std::vector<Chunk> ch(nt);
+  const char* cur = body;
+  for (size_t k = 0; k < nt; ++k) {
+    const char* stop = k + 1 == nt ? E : body + bytes * (k + 1) / nt;
+    if (stop < cur) stop = cur;
+    if (k + 1 < nt) {  // extend to the end of the line
+      const char* q = static_cast<const char*>(std::memchr(stop, '\n', (size_t)(E - stop)));
+      stop = q ? q + 1 : E;
+    }
+    ch[k].b = cur;
+    ch[k].e = stop;
+    cur = stop;
+  }
+  auto for_lines = [](const Chunk& c, auto&& fn) {
+    const char* p = c.b;
+    while (p < c.e) {
+      const char* q = static_cast<const char*>(std::memchr(p, '\n', (size_t)(c.e - p)));
+      const char* le = q ? q : c.e;
+      if (!fn(p, le)) return;
+      p = q ? q + 1 : c.e;
+    }
+  };
+  auto parallel = [&](auto&& fn) {
+    std::vector<std::thread> th;
+    for (size_t k = 1; k < nt; ++k) th.emplace_back(fn, k);
+    fn(0);
+    for (auto& t : th) t.join();
+  };
+  // pass 1: lines and data rows per chunk
+  parallel([&](size_t k) {
+    for_lines(ch[k], [&](const char* p, const char* e) {
+      ch[k].lines++;
+      ch[k].rows += is_row(p, e);
+      return true;
+    });
+  });
+  size_t line0 = 2, row0 = 0;
+  for (auto& c : ch) { c.first_line = line0; c.first_row = row0; line0 += c.lines; row0 += c.rows; }
+  Trace t;
+  t.arr.resize(row0);
+  t.pl.resize(row0);
+  t.dl.resize(row0);
+  // pass 2: parse and check each chunk (row ids and arrival order are local
+  // given the chunk's first row index; chunk seams are checked after the join)
+  parallel([&](size_t k) {
+    Chunk& c = ch[k];
+    size_t ln = c.first_line, r = c.first_row;
+    double prev = -INFINITY;
+    auto fail = [&](const char* m) { c.err_line = ln; c.err = m; return false; };
+    for_lines(c, [&](const char* p, const char* e) {
+      if (e > p && e[-1] == '\r') --e;
+      if (is_row(p, e)) {
+        long long id, pl, dl;
+        double a;
+        if (!row(p, e, id, a, pl, dl)) return fail("parse error");
+        if (id < 0 || (size_t)id != r) return fail("ids must be 0..n-1 in order");
+        if (!std::isfinite(a)) return fail("arrival_s must be finite");
+        if (a < prev) return fail("arrival_s decreases");
+        if (pl < 1 || dl < 1 || pl > (1 << 30) || dl > (1 << 28)) return fail("lengths out of range");
+        if (r == c.first_row) { c.first_a = a; c.first_ok = true; c.first_row_line = ln; }
+        prev = a;
+        c.last_a = a;
+        t.arr[r] = a;
+        t.pl[r] = (int32_t)pl;
+        t.dl[r] = (int32_t)dl;
+        ++r;
+      }
+      ++ln;
+      return true;
+    });
+  });
+  // first error in file order: a chunk's own error, or a seam where the
+  // chunk's first arrival is below the last arrival before it
+  size_t bad = 0;
+  std::string msg;
+  double last = -INFINITY;
+  for (auto& c : ch) {
+    if (c.first_ok && c.first_a < last) {  // precedes any later error in the chunk
+      bad = c.first_row_line;
+      msg = "arrival_s decreases";
+      break;
+    }
+    if (c.err_line) { bad = c.err_line; msg = c.err; break; }
+    if (c.rows) last = c.last_a;
+  }
+  if (bad) throw ConfigError(path + ":" + std::to_string(bad) + ": " + msg);
   return t;
 }
 std::string trace_csv(const Trace& t) {
@@ -787,6 +958,26 @@ int cmd_main(const Args& a) {
     }
   }
   if (a.cmd == "validate-config") {
+    if (has_trace) {  // what load_trace ingested: row count, length sums, FNV-1a of the arrival bits
+      uint64_t h = 1469598103934665603ull;
+      int64_t ps = 0, ds = 0;
+      for (size_t i = 0; i < trace.arr.size(); ++i) {
+        uint64_t b;
+        std::memcpy(&b, &trace.arr[i], 8);
+        for (int k = 0; k < 8; ++k) { h ^= (b >> (8 * k)) & 255u; h *= 1099511628211ull; }
+        ps += trace.pl[i];
+        ds += trace.dl[i];
+      }
+      char hx[32];
+      std::snprintf(hx, sizeof hx, "%016llx", (unsigned long long)h);
+      jl::Value ts = jl::Value::object();
+      ts.obj.push_back({"rows", jl::Value::number((double)trace.arr.size())});
+      ts.obj.push_back({"prompt_tokens", jl::Value::number((double)ps)});
+      ts.obj.push_back({"decode_tokens", jl::Value::number((double)ds)});
+      ts.obj.push_back({"arrival_fnv1a", jl::Value::string(hx)});
+      ts.obj.push_back({"pinned", jl::Value::boolean(trace.arr.pinned())});
+      cfg.obj.push_back({"trace_summary", ts});
+    }
     std::printf("%s\n", jl::dump(cfg).c_str());
     return 0;
   }

@@ -499,4 +499,23 @@ int kvsim_gpu_gen_trace(kvsim_gpu_ctx* c, const kvsim_point_desc* p, double* arr
   return KVSIM_OK;
 }
 
+void* kvsim_gpu_host_alloc(size_t bytes) {
+  int n = 0;
+  if (bytes == 0 || cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  void* p = nullptr;
+  // portable: usable by every device context (the CLI's one thread per GPU)
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void kvsim_gpu_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 }  // extern "C"

@@ -71,3 +71,22 @@ def test_no_cpu_fallback(lib):
     assert lib.kvsim_gpu_device_count() == 0
     with pytest.raises(pkg.KvSimError):
         pkg.KvSim(0)
+
+
+def test_pinned_host_buffers(lib):
+    # kvsim_gpu_host_alloc: page-locked memory for bulk trace ingestion, NULL
+    # without a device (callers then use ordinary memory); free(NULL) is a no-op
+    import ctypes as C
+    import torch
+    lib.kvsim_gpu_host_alloc.restype = C.c_void_p
+    lib.kvsim_gpu_host_alloc.argtypes = [C.c_size_t]
+    lib.kvsim_gpu_host_free.argtypes = [C.c_void_p]
+    lib.kvsim_gpu_host_free(None)
+    assert lib.kvsim_gpu_host_alloc(0) is None
+    p = lib.kvsim_gpu_host_alloc(1 << 20)
+    if not torch.cuda.is_available():
+        assert p is None
+    else:
+        assert p is not None
+        C.memset(p, 7, 1 << 20)
+        lib.kvsim_gpu_host_free(p)

@@ -11,7 +11,7 @@ import os
 import pytest
 
 from harness import Result, diff_results, oracle, run_oracle
-from paper_2411_05555_b200.abi import PointDesc, PointSummary, make_point
+from paper_2411_05555_b200.abi import PointDesc, PointSummary, TraceView, make_point
 
 pytestmark = pytest.mark.gpu
 
@@ -99,3 +99,42 @@ def test_device_resident_entry_matches_host_entry(sim):
     sz = C.sizeof(PointSummary)
     for i in range(n):
         assert raw[i * sz:(i + 1) * sz] == bytes(host[i]), i
+
+
+def test_external_trace_full_size(sim):
+    # a 100k-request user trace (load_trace path) shared by
+    # the three policies: GPU (trace uploaded from page-locked memory, as the
+    # CLI's bulk loader provides it) vs the oracle on the same rows
+    import random
+    n = 100_000
+    lib = sim.lib
+    lib.kvsim_gpu_host_alloc.restype = C.c_void_p
+    lib.kvsim_gpu_host_alloc.argtypes = [C.c_size_t]
+    lib.kvsim_gpu_host_free.argtypes = [C.c_void_p]
+    bufs = [lib.kvsim_gpu_host_alloc(n * w) for w in (8, 4, 4)]
+    assert all(bufs)
+    try:
+        arr = C.cast(bufs[0], C.POINTER(C.c_double))
+        pl = C.cast(bufs[1], C.POINTER(C.c_int32))
+        dl = C.cast(bufs[2], C.POINTER(C.c_int32))
+        r = random.Random(11)
+        t = 0.0
+        for i in range(n):  # bursty conversation-shaped arrivals, long-tailed lengths
+            t += r.expovariate(14.0 if (i // 500) % 2 else 6.0)
+            arr[i] = t
+            pl[i] = min(8000, int(r.paretovariate(1.3) * 200))
+            dl[i] = r.randint(2, 1500)
+        tv = TraceView(arr, pl, dl, n)
+        pts = []
+        for pol in ("unified", "splitwise", "accellm"):
+            p = make_point(policy=pol, instances=8, num_requests=n, workload="mixed", seed=0)
+            p.trace_index = 0
+            pts.append(p)
+        out = sim.run(pts, traces=[tv])
+        for p, s in zip(pts, out):
+            assert s.status == 0 and s.n_requests == n
+            ref = run_oracle(p, trace=tv, ev_cap=0, recs=False)
+            assert not diff_results(ref, Result(s, None, None), events=False), p.policy
+    finally:
+        for b in bufs:
+            lib.kvsim_gpu_host_free(b)
