@@ -244,7 +244,11 @@ def main():
     summ = (PointSummary * n).from_buffer_copy(host_out)
     bad = sum(1 for s in summ if s.status != 0)
     reqs = sum(s.n_requests for s in summ)
-    total_reqs = reqs * world
+    total_reqs = reqs
+    if dist:  # requests all ranks simulated (each rank runs its own grid)
+        t = torch.tensor([reqs], dtype=torch.int64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_reqs = int(t.item())
     value = total_reqs * args.steps / t_total
     kernel_s = t_total / args.steps
     bytes_alg = algorithmic_bytes(summ)
