@@ -2,7 +2,8 @@
 in the same process, a full config-4 warm-up sweep each, then R rounds of
 alternating timed sweeps. Less noisy than one process per variant (clock and
 power state are shared). Usage: python tools/ab_inproc.py [R] [lib[:MINB] ...]
-(MINB = KVSIM_MINB for that context: resident blocks per SM)."""
+(MINB = KVSIM_MINB for that context: resident blocks per SM; lib:MINB:CARVE
+also sets KVSIM_CARVEOUT, the shared-memory carveout percent)."""
 import glob, os, statistics, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_05555_b200 as pkg
@@ -13,7 +14,12 @@ libs = sys.argv[2:] or sorted(glob.glob("variants/*.so"))
 pts = config4_points(0, 833, 10000)
 sims = {}
 for spec in libs:
-    lib, _, minb = spec.partition(":")
+    lib, _, rest = spec.partition(":")
+    minb, _, carve = rest.partition(":")
+    if carve:
+        os.environ["KVSIM_CARVEOUT"] = carve
+    else:
+        os.environ.pop("KVSIM_CARVEOUT", None)
     os.environ["KVSIM_LIB"] = lib
     if minb:
         os.environ["KVSIM_MINB"] = minb
