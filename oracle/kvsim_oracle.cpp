@@ -145,6 +145,7 @@ struct Req {
   int32_t qlen = 0;           // length of the pending (re)prefill
   int primary = -1, copy = -1;
   bool stepping = false;      // member of its primary's in-flight step (+1 reserved)
+  bool settling = false;      // joined from the incoming list, no decode step here yet (§6: not movable)
   double fresh_at = 0;        // copy is complete at this time
   double last_t = 0, first_t = kNaN, done_t = kNaN, tbt_max = 0;
   int32_t n_moves = 0, n_preempt = 0;
@@ -344,7 +345,7 @@ struct Sim {
     int cnt = 0;
     std::vector<Incoming> keep;
     for (auto& in : X.incoming) {
-      if (in.ready <= t) { X.batch.push_back(in.rid); ++cnt; }
+      if (in.ready <= t) { X.batch.push_back(in.rid); R[in.rid].settling = true; ++cnt; }
       else keep.push_back(in);
     }
     X.incoming.swap(keep);
@@ -403,6 +404,7 @@ struct Sim {
       Req& r = R[rid];
       emit(r, t);
       r.stepping = false;
+      r.settling = false;
       if (r.emitted == r.decode) {
         // held after the step == kv() with the new emitted count
         I[x].used -= r.kv();
@@ -656,7 +658,7 @@ struct Sim {
                 (int64_t)Y.incoming.size();
     int64_t d = load_of(x) - load_of(y);
     std::vector<int> cand;
-    for (int rid : X.batch) if (R[rid].copy == y) cand.push_back(rid);
+    for (int rid : X.batch) if (R[rid].copy == y && !R[rid].settling) cand.push_back(rid);
     std::sort(cand.begin(), cand.end(), [&](int a, int b) {
       if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
       return a < b;
@@ -816,7 +818,7 @@ struct Sim {
                 (int64_t)D.incoming.size();
     int64_t dd = load_of(x) - load_of(d);
     std::vector<int> cand;
-    for (int rid : X.batch) if (R[rid].copy == d) cand.push_back(rid);
+    for (int rid : X.batch) if (R[rid].copy == d && !R[rid].settling) cand.push_back(rid);
     std::sort(cand.begin(), cand.end(), [&](int a, int b) {
       if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
       return a < b;
@@ -916,7 +918,8 @@ struct Sim {
     Inst& Y = I[y];
     if (Y.role != DECODE || Y.switch_pending || degraded_pair(x / 2) || degraded_pair(y / 2)) return;
     int64_t d = pair_load(x / 2) - pair_load(y / 2);
-    std::vector<int> cand(X.batch.begin(), X.batch.end());
+    std::vector<int> cand;
+    for (int rid : X.batch) if (!R[rid].settling) cand.push_back(rid);
     std::sort(cand.begin(), cand.end(), [&](int a, int b) {
       if (R[a].kv() != R[b].kv()) return R[a].kv() > R[b].kv();
       return a < b;

@@ -36,9 +36,12 @@ inline long long emu_prof[32];
 #endif
 
 constexpr int kMaxInst = 32;
-constexpr int32_t kRemMask = 0x1fffffff;
+constexpr int32_t kRemMask = 0x0fffffff;
 constexpr int32_t kJoin = 0x40000000;  // no decode step since joining the batch
 constexpr int32_t kCopy = 0x20000000;  // holds a redundant copy on the partner
+// joined from the incoming list (moved / handed off / leveled) and not yet
+// decoded a step here: not a rebalance candidate (SEMANTICS §6, "settling")
+constexpr int32_t kSettle = 0x10000000;
 enum { ROLE_DECODE = 0, ROLE_PREFILL = 1 };
 enum { JOB_NONE = 0, JOB_PREFILL = 1, JOB_STEP = 2 };
 
@@ -572,7 +575,7 @@ struct Sim {
         const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
         const bool hasc = c_cpy()[rid] >= 0;
         b_rid(x)[k] = rid;
-        b_rem(x)[k] = (dl - em) | kJoin | (hasc ? kCopy : 0);
+        b_rem(x)[k] = (dl - em) | kJoin | kSettle | (hasc ? kCopy : 0);
         b_kvb(x)[k] = pl + dl - 1;
         b_tbt(x)[k] = c_tbt()[rid];
         kvsum += (int64_t)pl + em - 1;
@@ -1653,7 +1656,7 @@ struct Sim {
       int32_t bidx = -1;
       for (int32_t j = lane; j < nb; j += 32) {
         const int32_t rf = b_rem(x)[j];
-        if (rf & kCopy) {
+        if ((rf & (kCopy | kSettle)) == kCopy) {
           const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
           if (kv <= lim) {
             const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
@@ -2018,7 +2021,7 @@ struct Sim {
       int32_t bidx = -1;
       for (int32_t j = lane; j < nb; j += 32) {
         const int32_t rf = b_rem(x)[j];
-        if (rf & kCopy) {
+        if ((rf & (kCopy | kSettle)) == kCopy) {
           const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
           if (kv <= lim) {
             const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
@@ -2148,7 +2151,7 @@ struct Sim {
       for (int32_t j = lane; j < nb; j += 32) {
         const int32_t rf = b_rem(x)[j];
         const int64_t kv = (int64_t)b_kvb(x)[j] - (rf & kRemMask);
-        if (kv <= lim) {
+        if (kv <= lim && !(rf & kSettle)) {
           const uint64_t kk = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - b_rid(x)[j]);
           if (kk > best) { best = kk; bidx = j; }
         }
