@@ -123,30 +123,39 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
-def cpu_reference(points, budget_s, threads):
-    """Time the CPU oracle (restated reference simulator) on a bounded,
-    deterministic subsample of the points (every k-th), all host threads."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sweep(points, threads):
+    """Run the CPU oracle (restated reference simulator, test infrastructure)
+    on `points`, one point per host thread. Returns
+    (summaries, seconds)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from harness import oracle  # test infrastructure: the checker / CPU baseline only
+    from harness import oracle  # the checker / CPU baseline only
     L = oracle()
-    # calibrate on a tiny slice, then choose a stride so the run takes ~budget_s
-    probe = points[:: max(1, len(points) // 48)][:48]
-    P = (PointDesc * len(probe))(*probe)
-    S = (PointSummary * len(probe))()
+    P = (PointDesc * len(points))(*points)
+    S = (PointSummary * len(points))()
     t0 = time.perf_counter()
-    L.kvo_run_sweep(P, len(probe), threads, S)
-    dt = max(time.perf_counter() - t0, 1e-6)
-    per_pt = dt / len(probe)
-    n_take = max(threads, min(len(points), int(budget_s / per_pt)))
-    stride = max(1, len(points) // n_take)
-    sample = points[::stride]
-    P = (PointDesc * len(sample))(*sample)
-    S = (PointSummary * len(sample))()
-    t0 = time.perf_counter()
-    L.kvo_run_sweep(P, len(sample), threads, S)
-    dt = time.perf_counter() - t0
-    reqs = sum(s.n_requests for s in S)
-    return reqs / dt, len(sample), stride, dt
+    L.kvo_run_sweep(P, len(points), threads, S)
+    return S, time.perf_counter() - t0
+
+
+def parity_check(gpu, cpu):
+    """Bitwise comparison of every summary field (GPU == oracle)."""
+    def key(x):
+        y = PointSummary.from_buffer_copy(bytes(x))
+        y.reserved[0] = 0  # kernel-only diagnostic (event-loop iterations)
+        return bytes(y)
+    bad = [i for i, (a, b) in enumerate(zip(gpu, cpu)) if key(a) != key(b)]
+    return {"checked": len(cpu), "mismatches": len(bad), "first_mismatch": bad[0] if bad else None,
+            "fields": "all kvsim_point_summary fields, bit for bit"}
 
 
 def main():
@@ -159,6 +168,7 @@ def main():
     ap.add_argument("--requests", type=int, default=10000)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the full-size CPU oracle baseline / parity check")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -171,27 +181,33 @@ def main():
                 f"{args.requests} requests/point, mixed, Llama-2-70B on simulated H100")
 
     if args.impl == "reference":
+        # The reference's own CPU path does not exist; its restated
+        # simulator (the oracle) runs on every host thread. The K timed steps
+        # together cover the whole config-4 grid exactly once: step s runs
+        # points s, s+K, s+2K, ... (each a bounded, interleaved 1/K sample).
         if rank != 0:
             return
         pts = config4_points(0, args.rates, args.requests)
-        vals = []
-        for _ in range(args.warmup):
-            cpu_reference(pts, min(3.0, args.cpu_budget / 4), n_cpu)
-        info = None
-        for _ in range(args.steps):
-            v, ns, stride, dt = cpu_reference(pts, args.cpu_budget / max(args.steps, 1), n_cpu)
-            vals.append(v)
-            info = (ns, stride, dt)
-        v = statistics.median(vals)
+        for w in range(args.warmup):
+            oracle_sweep(pts[w::max(1, len(pts) // 64)], n_cpu)
+        K = max(args.steps, 1)
+        times, reqs = [], 0
+        for st in range(K):
+            S, dt = oracle_sweep(pts[st::K], n_cpu)
+            times.append(dt)
+            reqs += sum(x.n_requests for x in S if x.status == 0)
+        v = reqs / sum(times)
         line = {"metric": metric, "value": v, "unit": "simulated requests/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": info[2] * 1e3,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / K * 1e3,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (device-RNG-equivalent traces from the seeded generator)",
+                "data": "synthetic (the seeded generator of SEMANTICS §2, same traces as the GPU arm)",
                 "impl": "reference",
-                "config": {"workload": workload, "parallelism": f"{n_cpu} host threads"},
+                "config": {"workload": workload, "parallelism": f"{n_cpu} host threads, one point per thread"},
                 "cpu_baseline": {"value": v, "unit": "simulated requests/s", "cores": n_cpu, "kind": "port",
-                                 "sample": f"every {info[1]}th point of the sweep ({info[0]} points x "
-                                           f"{args.requests} requests) per step"},
+                                 "cpu_model": cpu_model(),
+                                 "sample": f"all {len(pts)} points x {args.requests} requests, split into {K} "
+                                           f"interleaved steps (step s = points s, s+{K}, ...); "
+                                           f"{sum(times):.1f} s in total"},
                 "e2e": {"value": v, "unit": "simulated requests/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -243,7 +259,9 @@ def main():
     host_out = d_out.cpu().numpy().tobytes()
     summ = (PointSummary * n).from_buffer_copy(host_out)
     bad = sum(1 for s in summ if s.status != 0)
-    reqs = sum(s.n_requests for s in summ)
+    # failed points (e.g. an exceeded event budget) did not simulate all of
+    # their requests: they do not count towards the throughput
+    reqs = sum(s.n_requests for s in summ if s.status == 0)
     total_reqs = reqs
     if dist:  # requests all ranks simulated (each rank runs its own grid)
         t = torch.tensor([reqs], dtype=torch.int64, device=f"cuda:{dev}")
@@ -277,12 +295,16 @@ def main():
         e2e = {"value": total_reqs * len(tt) / te, "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
-    cpu = None
-    if rank == 0 and world == 1:
-        v, ns, stride, dt = cpu_reference(pts, args.cpu_budget, n_cpu)
-        cpu = {"value": v, "unit": "simulated requests/s", "cores": n_cpu, "kind": "port",
-               "sample": f"every {stride}th point of this sweep ({ns} points x {args.requests} requests), "
-                         f"{dt:.1f} s on {n_cpu} host threads (CPU oracle, one point per thread)"}
+    cpu, parity = None, None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the full sweep on the CPU oracle (all host threads): both the
+        # cpu_baseline and a bitwise check of every GPU summary
+        S_cpu, dt = oracle_sweep(pts, n_cpu)
+        v = sum(x.n_requests for x in S_cpu if x.status == 0) / dt
+        cpu = {"value": v, "unit": "simulated requests/s", "cores": n_cpu, "kind": "port", "cpu_model": cpu_model(),
+               "sample": f"the full sweep ({n} points x {args.requests} requests), {dt:.1f} s on {n_cpu} host "
+                         f"threads (CPU oracle, one point per thread)"}
+        parity = parity_check(summ, S_cpu)
 
     if rank == 0:
         line = {
@@ -308,6 +330,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     sim.close()

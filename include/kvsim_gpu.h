@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define KVSIM_ABI_VERSION 1
+#define KVSIM_ABI_VERSION 2
 #define KVSIM_MAX_INSTANCES 32
 
 enum kvsim_policy { KVSIM_POLICY_UNIFIED = 0, KVSIM_POLICY_SPLITWISE = 1, KVSIM_POLICY_ACCELLM = 2 };
@@ -134,6 +134,16 @@ typedef struct kvsim_point_summary {
   int64_t link_leveling_tokens; /* KV moved by inter-pair leveling */
   int64_t n_timer_ticks;        /* policy timer events */
   int64_t n_mode_switches;      /* degraded-mode entries + exits */
+  /* v2: the rest of the MetricsReport */
+  double ttft_queue_mean;       /* mean (first prefill start - arrival): the queue-wait part of TTFT */
+  double tbt_p50, tbt_p95;      /* nearest rank over the pooled TBT samples of measured requests;
+                                   detail runs only (kvsim_run_opts.detail), NaN otherwise */
+  double idle_runnable_s;       /* sum over instances of time in the window with no job in
+                                   flight while >= 1 request is live anywhere */
+  double queue_depth_avg;       /* time average over [0, makespan] of the requests waiting in
+                                   prefill queues (SPEC.md:358 queue-depth series) */
+  int64_t queue_depth_max;
+  int64_t n_tbt_samples;        /* sum over measured requests of (decode_len - 1) */
   int64_t reserved[1];
 } kvsim_point_summary;
 
@@ -143,7 +153,19 @@ typedef struct kvsim_request_record {
   double arrival_s, first_token_s, completion_s, tbt_max_s;
   int32_t prompt_len, decode_len;
   int32_t n_moves, n_preemptions;
+  double prefill_start_s;       /* v2: start of the job that produced the first token (queue wait
+                                   = prefill_start_s - arrival_s) */
 } kvsim_request_record;
+
+/* v2: per-instance record ("idle_fraction per instance;
+ * peak_kv_bytes per instance"). idle fraction = 1 - busy_s / window. */
+typedef struct kvsim_instance_record {
+  double busy_s;                /* job time of jobs starting in the window */
+  double idle_runnable_s;       /* see kvsim_point_summary.idle_runnable_s */
+  int64_t peak_kv_tokens;       /* peak ledger (primaries + copies + reservations) */
+  int32_t initial_role;         /* 0 decode, 1 prefill (splitwise prefill instances) */
+  int32_t reserved;
+} kvsim_instance_record;
 
 /* Decision / event log entry (--emit-events). */
 enum kvsim_event_kind {
@@ -195,6 +217,23 @@ int kvsim_gpu_run(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
                   kvsim_point_summary* out, kvsim_request_record* recs,
                   kvsim_event_record* ev, size_t ev_cap, int64_t* ev_count,
                   char* err, size_t err_len);
+
+/* v2: optional outputs and modes of a run (all fields zero = kvsim_gpu_run
+ * without records / events). */
+typedef struct kvsim_run_opts {
+  int32_t detail;               /* 1: pooled TBT percentiles (tbt_p50/p95). Runs the plain event
+                                   loop (no step chaining) and keeps one (gap, count) entry per
+                                   step in HBM: for reports, not for throughput sweeps */
+  int32_t reserved_i[3];
+  kvsim_request_record* recs;   /* as in kvsim_gpu_run */
+  kvsim_event_record* ev;       /* as in kvsim_gpu_run */
+  size_t ev_cap;
+  int64_t* ev_count;
+  kvsim_instance_record* inst;  /* nullable; point i's records at i * KVSIM_MAX_INSTANCES */
+} kvsim_run_opts;
+int kvsim_gpu_run_ex(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
+                     const kvsim_trace_view* traces, size_t n_traces, kvsim_point_summary* out,
+                     const kvsim_run_opts* opts, char* err, size_t err_len);
 
 /* Device-resident variant: d_pts / d_out are device pointers, generated traces
  * only, no records; launched on `stream` (a cudaStream_t; NULL selects the

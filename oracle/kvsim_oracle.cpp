@@ -148,6 +148,7 @@ struct Req {
   bool settling = false;      // joined from the incoming list, no decode step here yet (§6: not movable)
   double fresh_at = 0;        // copy is complete at this time
   double last_t = 0, first_t = kNaN, done_t = kNaN, tbt_max = 0;
+  double pf_start = kNaN;     // start of the job that produced the first token (queue wait)
   int32_t n_moves = 0, n_preempt = 0;
   bool done = false;
   int64_t kv() const { return (int64_t)prompt + emitted - 1; }
@@ -167,6 +168,10 @@ struct Inst {
   int64_t used = 0, peak = 0;
   double busy_time = 0;
   bool switch_pending = false;
+  // idle-while-runnable: the current idle period began at
+  // idle_t (last job end) when the cluster's zero-live measure was idle_z
+  double idle_t = 0, idle_z = 0, idle_rb = 0;
+  int role0 = DECODE;
 };
 
 struct Sim {
@@ -187,6 +192,15 @@ struct Sim {
   int64_t n_events = 0, n_steps = 0, n_prefills = 0, n_moves = 0, n_preempt = 0, n_evict = 0;
   int64_t tokens_total = 0, tokens_window = 0, prefill_tokens = 0, mirror_tokens = 0;
   double now = 0;
+  // live requests (arrived, not complete) and Z(t) = time in [warmup, t] with
+  // none live; queue depth (requests waiting in prefill queues) series stats
+  int64_t live = 0;
+  double zero_since = 0, z_acc = 0;
+  int64_t qdepth = 0, qd_max = 0;
+  double qd_area = 0, qd_tprev = 0;
+  // detail runs: every TBT sample of a measured request (pooled percentiles)
+  bool detail = false;
+  std::vector<double> tbt_samples;
   // AcceLLM timer-driven extensions (SEMANTICS §6b): degraded mode
   // and inter-pair leveling (
   // PAPER.md:309). partner[x] = holder of the copies of x's primaries
@@ -213,7 +227,7 @@ struct Sim {
     else if (policy == KVSIM_POLICY_SPLITWISE) {
       Q.resize(1);
       n_prefill = p.num_prefill_instances > 0 ? p.num_prefill_instances : (n + 2) / 4;
-      for (int i = 0; i < n_prefill; ++i) I[i].role = PREFILL;
+      for (int i = 0; i < n_prefill; ++i) I[i].role = I[i].role0 = PREFILL;
     } else Q.resize(n / 2);
     qtokens.assign(Q.size(), 0);
     if (policy == KVSIM_POLICY_ACCELLM && (p.accellm_flags & 3)) {
@@ -251,9 +265,35 @@ struct Sim {
   int queue_of(int i) const {
     return policy == KVSIM_POLICY_UNIFIED ? i : policy == KVSIM_POLICY_SPLITWISE ? 0 : qid(i / 2);
   }
-  void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; }
-  void push_front(int q, int rid) { Q[q].push_front(rid); qtokens[q] += R[rid].qlen; }
-  int pop_front(int q) { int r = Q[q].front(); Q[q].pop_front(); qtokens[q] -= R[r].qlen; return r; }
+  // queue depth: area += depth * (now - previous change), then the change
+  void qd_change(int64_t delta) {
+    qd_area = qd_area + (double)qdepth * (now - qd_tprev);
+    qd_tprev = now;
+    qdepth += delta;
+    if (qdepth > qd_max) qd_max = qdepth;
+  }
+  void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; qd_change(1); }
+  void push_front(int q, int rid) { Q[q].push_front(rid); qtokens[q] += R[rid].qlen; qd_change(1); }
+  int pop_front(int q) { int r = Q[q].front(); Q[q].pop_front(); qtokens[q] -= R[r].qlen; qd_change(-1); return r; }
+  // degraded-mode queue merge: the request stays queued (no depth change)
+  int move_front(int q) { int r = Q[q].front(); Q[q].pop_front(); qtokens[q] -= R[r].qlen; return r; }
+  void append_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; }
+
+  // ---- idle while runnable
+  double clip(double t) const { return t > P.warmup_s ? t : P.warmup_s; }
+  // Z(t): measure of [warmup, t] with no live request (t >= every change so far)
+  double zeta(double t) const { return live == 0 ? z_acc + (clip(t) - clip(zero_since)) : z_acc; }
+  void live_add(int64_t k, double t) {
+    if (live == 0 && k > 0) z_acc = z_acc + (clip(t) - clip(zero_since));
+    live += k;
+    if (live == 0) zero_since = t;
+  }
+  // a job starts on x at t: close x's idle period
+  void job_begin(Inst& X, double t) {
+    const double a = clip(t) - clip(X.idle_t);
+    const double b = zeta(t) - X.idle_z;
+    X.idle_rb = X.idle_rb + (a - b);
+  }
 
   // token emission at time t (first token, recompute token or decode token)
   void emit(Req& r, double t) {
@@ -262,16 +302,23 @@ struct Sim {
       status = KVSIM_E_INTERNAL;  // token_times strictly increasing
     }
     if (r.emitted == 0) r.first_t = t;
-    else { double gap = t - r.last_t; if (gap > r.tbt_max) r.tbt_max = gap; }
+    else {
+      double gap = t - r.last_t;
+      if (gap > r.tbt_max) r.tbt_max = gap;
+      if (detail && r.arrival >= P.warmup_s) tbt_samples.push_back(gap);
+    }
     r.last_t = t;
     r.emitted += 1;
     ++tokens_total;
     if (t >= P.warmup_s) ++tokens_window;
   }
-  void finish_req(Req& r, double t) { r.done = true; r.done_t = t; }
+  void finish_req(Req& r, double t) { r.done = true; r.done_t = t; live_add(-1, t); }
 
+  // a job ends on x at t: busy time, and x's idle period (if any) starts here
   void account_job(Inst& x, double t) {
     if (x.job_start >= P.warmup_s) x.busy_time += t - x.job_start;
+    x.idle_t = t;
+    x.idle_z = zeta(t);
   }
 
   // ---- memory helpers (§5)
@@ -381,6 +428,7 @@ struct Sim {
     int64_t B = (int64_t)X.batch.size(), K = 0;
     for (int rid : X.batch) { K += R[rid].kv(); R[rid].stepping = true; }
     bump(x, B);
+    job_begin(X, t);
     X.job = JOB_STEP;
     X.job_start = t;
     X.busy_until = t + decode_lat(f, B, K);
@@ -444,12 +492,14 @@ struct Sim {
       if (X.used + len > f.cap) break;
       pop_front(x);
       bump(x, len);
+      if (R[head].emitted == 0) R[head].pf_start = t;
       X.job_reqs.push_back(head);
       s1 += len;
       s2 += len * len;
     }
     if (B == 0 && X.job_reqs.empty()) return;
     double lat = (X.job_reqs.empty() ? 0.0 : prefill_lat(f, s1, s2)) + (B ? decode_lat(f, B, K) : 0.0);
+    job_begin(X, t);
     X.job = JOB_STEP;
     X.job_start = t;
     X.busy_until = t + lat;
@@ -504,6 +554,7 @@ struct Sim {
         pop_front(0);
         bump(d, len);
         R[head].primary = d;
+        if (R[head].emitted == 0) R[head].pf_start = t;
         X.job_reqs.push_back(head);
         s1 += len;
         s2 += len * len;
@@ -511,6 +562,7 @@ struct Sim {
       if (X.job_reqs.empty()) continue;
       X.job_s1 = s1;
       bump(p, s1);
+      job_begin(X, t);
       X.job = JOB_PREFILL;
       X.job_start = t;
       X.busy_until = t + prefill_lat(f, s1, s2);
@@ -613,11 +665,13 @@ struct Sim {
       pop_front(q);
       bump(x, len);
       R[head].primary = x;
+      if (R[head].emitted == 0) R[head].pf_start = t;
       X.job_reqs.push_back(head);
       s1 += len;
       s2 += len * len;
     }
     X.job_s1 = s1;
+    job_begin(X, t);
     X.job = JOB_PREFILL;
     X.job_start = t;
     X.busy_until = t + prefill_lat(f, s1, s2);
@@ -874,7 +928,7 @@ struct Sim {
     for (int h = a + 1; h <= a + 3; ++h) partner[h] = a;
     gmode[g] = 1;
     ++n_modes;
-    while (!Q[2 * g + 1].empty()) push_back(2 * g, pop_front(2 * g + 1));
+    while (!Q[2 * g + 1].empty()) append_back(2 * g, move_front(2 * g + 1));
     log(KVSIM_EV_MODE, g, 1, 0, 0);
     ensure_prefill(2 * g, t);
   }
@@ -1061,6 +1115,7 @@ struct Sim {
       switch (bk) {
         case 0:
           ++next_arrival;
+          live_add(1, t);
           arrive(bid, t);
           break;
         case 1:
@@ -1161,9 +1216,16 @@ int64_t gen_trace(const kvsim_point_desc& p, double* arr, int32_t* pr, int32_t* 
 
 int64_t nearest_rank(int64_t n, int pct) { return (pct * n + 99) / 100 - 1; }
 
-void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
+void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs, kvsim_instance_record* inst) {
   const kvsim_point_desc& p = S.P;
   std::memset(out, 0, sizeof(*out));
+  // instances idle at the end: their idle period runs to the makespan
+  for (auto& x : S.I)
+    if (x.job == NONE) S.job_begin(x, S.now);
+  if (inst) {
+    for (int i = 0; i < S.n; ++i)
+      inst[i] = kvsim_instance_record{S.I[i].busy_time, S.I[i].idle_rb, S.I[i].peak, S.I[i].role0, 0};
+  }
   out->status = S.status;
   out->num_instances = S.n;
   out->user_tag = p.user_tag;
@@ -1191,13 +1253,13 @@ void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
   out->link_prefill_gb = (double)S.prefill_tokens * S.f.kvb / 1e9;
   out->link_mirror_gb = (double)S.mirror_tokens * S.f.kvb / 1e9;
   std::vector<double> ttft, jct;
-  double s_ttft = 0, s_jct = 0, s_tbt = 0, tbt_max = 0;
+  double s_ttft = 0, s_jct = 0, s_tbt = 0, tbt_max = 0, s_qw = 0;
   int64_t n_tbt = 0, completed = 0;
   for (int64_t i = 0; i < S.N; ++i) {
     const Req& r = S.R[i];
     if (recs) {
       recs[i] = kvsim_request_record{r.arrival, r.first_t, r.done_t, r.tbt_max, r.prompt, r.decode,
-                                     r.n_moves, r.n_preempt};
+                                     r.n_moves, r.n_preempt, r.pf_start};
     }
     if (!r.done) continue;
     ++completed;
@@ -1207,6 +1269,7 @@ void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
     jct.push_back(b);
     s_ttft += a;
     s_jct += b;
+    s_qw += r.pf_start - r.arrival;
     if (r.decode > 1) {
       s_tbt += r.done_t - r.first_t;
       n_tbt += r.decode - 1;
@@ -1233,6 +1296,24 @@ void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs) {
   }
   out->tbt_mean = n_tbt > 0 ? s_tbt / (double)n_tbt : kNaN;
   out->tbt_max = n_tbt > 0 ? tbt_max : kNaN;
+  out->n_tbt_samples = n_tbt;
+  out->ttft_queue_mean = m > 0 ? s_qw / (double)m : kNaN;
+  out->tbt_p50 = out->tbt_p95 = kNaN;
+  if (S.detail && n_tbt > 0 && (int64_t)S.tbt_samples.size() == n_tbt) {
+    std::vector<double>& v = S.tbt_samples;
+    std::nth_element(v.begin(), v.begin() + nearest_rank(n_tbt, 50), v.end());
+    out->tbt_p50 = v[nearest_rank(n_tbt, 50)];
+    std::nth_element(v.begin(), v.begin() + nearest_rank(n_tbt, 95), v.end());
+    out->tbt_p95 = v[nearest_rank(n_tbt, 95)];
+  }
+  double irb = 0;
+  for (auto& x : S.I) irb += x.idle_rb;
+  out->idle_runnable_s = irb;
+  out->queue_depth_max = S.qd_max;
+  {
+    double area = S.qd_area + (double)S.qdepth * (S.now - S.qd_tprev);
+    out->queue_depth_avg = S.now > 0 ? area / S.now : kNaN;
+  }
   double window = S.now - p.warmup_s;
   if (window > 0) {
     out->cost_eff = (double)S.tokens_window / (window * (double)S.n);
@@ -1269,8 +1350,9 @@ int64_t kvo_gen_trace(const kvsim_point_desc* p, double* a, int32_t* pr, int32_t
   return gen_trace(*p, a, pr, de, cap);
 }
 
-int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsim_point_summary* out,
-                  kvsim_request_record* recs, kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count) {
+int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsim_point_summary* out,
+                     kvsim_request_record* recs, kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count,
+                     kvsim_instance_record* inst, int detail) {
   int st = check_point(*p);
   if (st != KVSIM_OK) {
     std::memset(out, 0, sizeof(*out));
@@ -1280,6 +1362,7 @@ int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsi
     return st;
   }
   Sim S(*p, ev, ev_cap);
+  S.detail = detail != 0;
   int64_t N;
   std::vector<double> arr;
   std::vector<int32_t> pr, de;
@@ -1302,9 +1385,14 @@ int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsi
     S.R[i].decode = de[i];
   }
   S.run();
-  summarize(S, out, recs);
+  summarize(S, out, recs, inst);
   if (ev_count) *ev_count = S.ev_n;
   return S.status;
+}
+
+int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsim_point_summary* out,
+                  kvsim_request_record* recs, kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count) {
+  return kvo_run_point_ex(p, trace, out, recs, ev, ev_cap, ev_count, nullptr, 0);
 }
 
 int kvo_run_sweep(const kvsim_point_desc* pts, int64_t n, int threads, kvsim_point_summary* out) {

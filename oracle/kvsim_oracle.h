@@ -44,6 +44,13 @@ int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace,
                   kvsim_point_summary* out, kvsim_request_record* recs,
                   kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count);
 
+/* v2: also per-instance records (n_instances entries, nullable) and detail
+ * metrics (pooled TBT percentiles) when detail != 0. */
+int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace,
+                     kvsim_point_summary* out, kvsim_request_record* recs,
+                     kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count,
+                     kvsim_instance_record* inst, int detail);
+
 /* Sweep over n points on `threads` host threads (one point per thread at a
  * time). Generated traces only. */
 int kvo_run_sweep(const kvsim_point_desc* pts, int64_t n, int threads,

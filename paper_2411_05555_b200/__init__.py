@@ -17,7 +17,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .abi import (EventRecord, PointDesc, PointSummary, RequestRecord, TraceView,  # noqa: F401
+from .abi import (EventRecord, InstanceRecord, PointDesc, PointSummary, RequestRecord, RunOpts,  # noqa: F401
+                  TraceView,
                   make_point, points_array, summary_dict, STATUS, POLICY, POLICY_NAME,
                   DEVICES, MODELS, WORKLOADS, SUMMARY_CSV)
 
@@ -50,6 +51,8 @@ def load_library() -> C.CDLL:
     L.kvsim_gpu_run.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(TraceView), C.c_size_t,
                                 C.POINTER(PointSummary), C.POINTER(RequestRecord), C.POINTER(EventRecord),
                                 C.c_size_t, C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_run_ex.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(TraceView), C.c_size_t,
+                                   C.POINTER(PointSummary), C.POINTER(RunOpts), C.c_char_p, C.c_size_t]
     L.kvsim_gpu_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                        C.c_char_p, C.c_size_t]
     L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]
@@ -95,9 +98,12 @@ class KvSim:
         if rc != 0:
             raise KvSimError(f"{what} failed [{rc}]: {self.err.value.decode()}")
 
-    def run(self, points, traces=None, records: bool = False, events: int = 0):
+    def run(self, points, traces=None, records: bool = False, events: int = 0, detail: bool = False,
+            instances: bool = False):
         """Run points (list of PointDesc). Returns summaries, or (summaries,
-        records per point, events per point) when records/events requested."""
+        records per point, events per point) when records/events requested.
+        detail: pooled TBT percentiles (kvsim_run_opts.detail); instances:
+        per-instance records, afterwards in self.last_instances."""
         n = len(points)
         P = (PointDesc * n)(*points)
         S = (PointSummary * n)()
@@ -105,14 +111,27 @@ class KvSim:
         R = (RequestRecord * max(tot, 1))() if records else None
         E = (EventRecord * max(events * n, 1))() if events else None
         cnt = (C.c_int64 * n)() if events else None
+        I = (InstanceRecord * (32 * n))() if instances else None
         T, nt = None, 0
         if traces:
             nt = len(traces)
             T = (TraceView * nt)(*traces)
-        rc = self.lib.kvsim_gpu_run(self.h, P, n, T, nt, S, R, E, events, cnt, self.err, 512)
+        if detail or instances:
+            o = RunOpts()
+            o.detail = 1 if detail else 0
+            o.recs = R
+            o.ev = C.cast(E, C.c_void_p) if E is not None else None
+            o.ev_cap = events
+            o.ev_count = cnt
+            o.inst = I
+            rc = self.lib.kvsim_gpu_run_ex(self.h, P, n, T, nt, S, C.byref(o), self.err, 512)
+        else:
+            rc = self.lib.kvsim_gpu_run(self.h, P, n, T, nt, S, R, E, events, cnt, self.err, 512)
         self._check(rc, "kvsim_gpu_run")
         summaries = list(S)
         self.last_event_counts = list(cnt) if events else None
+        self.last_instances = ([list(I[32 * i:32 * i + points[i].num_instances]) for i in range(n)]
+                               if instances else None)
         if not records and not events:
             return summaries
         recs_out, ev_out, off = [], [], 0

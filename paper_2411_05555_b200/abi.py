@@ -80,6 +80,10 @@ class PointSummary(C.Structure):
         ("user_tag", C.c_uint64),
         ("link_leveling_tokens", C.c_int64), ("n_timer_ticks", C.c_int64),
         ("n_mode_switches", C.c_int64),
+        # ABI v2 (kvsim_gpu.h): the rest of the MetricsReport
+        ("ttft_queue_mean", C.c_double), ("tbt_p50", C.c_double), ("tbt_p95", C.c_double),
+        ("idle_runnable_s", C.c_double), ("queue_depth_avg", C.c_double),
+        ("queue_depth_max", C.c_int64), ("n_tbt_samples", C.c_int64),
         ("reserved", C.c_int64 * 1),
     ]
 
@@ -90,6 +94,23 @@ class RequestRecord(C.Structure):
         ("completion_s", C.c_double), ("tbt_max_s", C.c_double),
         ("prompt_len", C.c_int32), ("decode_len", C.c_int32),
         ("n_moves", C.c_int32), ("n_preemptions", C.c_int32),
+        ("prefill_start_s", C.c_double),
+    ]
+
+
+class InstanceRecord(C.Structure):
+    _fields_ = [
+        ("busy_s", C.c_double), ("idle_runnable_s", C.c_double),
+        ("peak_kv_tokens", C.c_int64), ("initial_role", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class RunOpts(C.Structure):
+    _fields_ = [
+        ("detail", C.c_int32), ("reserved_i", C.c_int32 * 3),
+        ("recs", C.POINTER(RequestRecord)),
+        ("ev", C.c_void_p), ("ev_cap", C.c_size_t), ("ev_count", C.POINTER(C.c_int64)),
+        ("inst", C.POINTER(InstanceRecord)),
     ]
 
 

@@ -24,9 +24,11 @@ namespace kvsim_host {
 struct ArenaGeom {
   int64_t Ncap = 1, Bcap = 1, Jcap = 1;
   int32_t Imax = 1;
+  int64_t Tcap = 0;  // detail runs: TBT (gap, count) entries per slot
   // bytes per slot
   size_t per_slot() const {
-    const size_t cold = (size_t)Ncap * (6 * sizeof(double) + 7 * sizeof(int32_t));
+    const size_t cold = (size_t)Ncap * (7 * sizeof(double) + 7 * sizeof(int32_t)) +
+                        (size_t)Tcap * (sizeof(double) + sizeof(int32_t));
     const size_t ring = (size_t)Imax * Ncap * sizeof(int32_t);
     const size_t batch = (size_t)Imax * Bcap * (3 * sizeof(int32_t) + sizeof(double));
     const size_t inc = (size_t)Imax * Bcap * (sizeof(int32_t) + sizeof(double));
@@ -36,17 +38,21 @@ struct ArenaGeom {
   }
 };
 
-// trace_min_prompt: per trace index, the minimum prompt (or empty)
+// trace_min_prompt: per trace index, the minimum prompt (or empty);
+// trace_max_decode likewise (detail runs size the TBT entries from it)
 inline ArenaGeom size_arena(const kvsim_point_desc* pts, size_t n, const std::vector<int64_t>& trace_n,
-                            const std::vector<int32_t>& trace_min_prompt) {
+                            const std::vector<int32_t>& trace_min_prompt, bool detail = false,
+                            const std::vector<int32_t>& trace_max_decode = {}) {
   ArenaGeom g;
   for (size_t i = 0; i < n; ++i) {
     const kvsim_point_desc& p = pts[i];
     int64_t N = p.num_requests > 0 ? p.num_requests : 0;
     int32_t pmin = p.prompt_min;
+    int64_t dmax = p.decode_max;
     if (p.trace_index >= 0 && (size_t)p.trace_index < trace_n.size()) {
       N = std::min<int64_t>(N, trace_n[p.trace_index]);
       pmin = trace_min_prompt[p.trace_index];
+      dmax = (size_t)p.trace_index < trace_max_decode.size() ? trace_max_decode[p.trace_index] : 1;
     }
     if (pmin < 1) pmin = 1;
     const kvsim_math::Perf f = kvsim_math::make_perf(p);
@@ -56,6 +62,8 @@ inline ArenaGeom size_arena(const kvsim_point_desc* pts, size_t n, const std::ve
     g.Bcap = std::max<int64_t>(g.Bcap, std::min<int64_t>(N, cap / pmin + 2));
     g.Jcap = std::max<int64_t>(g.Jcap, std::min<int64_t>(N, budget / pmin + 1));
     g.Imax = std::max<int32_t>(g.Imax, std::min<int32_t>(std::max(p.num_instances, 1), KVSIM_MAX_INSTANCES));
+    // entries <= decode steps + individual gaps, each <= the TBT samples N (dmax - 1)
+    if (detail) g.Tcap = std::max<int64_t>(g.Tcap, 2 * N * std::max<int64_t>(dmax - 1, 0) + 64);
   }
   return g;
 }
@@ -75,7 +83,7 @@ inline size_t carve(Args& a, char* base, const ArenaGeom& g, int32_t slots) {
   const size_t S = (size_t)slots;
   const size_t cold = S * (size_t)g.Ncap;
   take(a.c_arr, cold); take(a.c_last, cold); take(a.c_tbt, cold); take(a.c_fresh, cold);
-  take(a.c_first, cold); take(a.c_done, cold);
+  take(a.c_first, cold); take(a.c_done, cold); take(a.c_qs, cold);
   take(a.c_pl, cold); take(a.c_dl, cold); take(a.c_qlen, cold); take(a.c_em, cold);
   take(a.c_cpy, cold); take(a.c_nmv, cold); take(a.c_npre, cold);
   take(a.q_rid, S * g.Imax * (size_t)g.Ncap);
@@ -85,6 +93,9 @@ inline size_t carve(Args& a, char* base, const ArenaGeom& g, int32_t slots) {
   const size_t jj = S * g.Imax * (size_t)g.Jcap;
   take(a.j_rid, jj); take(a.j_dst, jj);
   take(a.link, S * g.Imax * (size_t)g.Imax);
+  take(a.t_val, S * (size_t)g.Tcap);
+  take(a.t_cnt, S * (size_t)g.Tcap);
+  a.Tcap = g.Tcap;
   a.Ncap = g.Ncap;
   a.Bcap = g.Bcap;
   a.Jcap = g.Jcap;

@@ -99,7 +99,7 @@ const char* const kKeys[] = {"model", "device", "num_devices", "memory_reserve_f
                              "arrival_process", "rate", "rates", "duration_s", "num_requests", "warmup_s", "seed",
                              "seeds", "efficiency", "link_aggregation", "trace", "sweep_instances",
                              "sweep_devices", "curves", "emit_records", "splitwise_cobatch", "degraded_mode",
-                             "inter_pair_leveling", "policy_timer_s", "output", "resource"};
+                             "inter_pair_leveling", "policy_timer_s", "output", "resource", "detail_metrics"};
 
 struct Resolved {
   jl::Value cfg;  // resolved config (defaults filled)
@@ -393,6 +393,11 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
   c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
                                                ? in.find("emit_records")->b
                                                : cmd == "run"));
+  // detail metrics (pooled TBT p50/p95: plain event loop + per-step gap
+  // entries in HBM) default on for `run`, off for sweeps
+  if (const jl::Value* v = in.find("detail_metrics"))
+    if (v->kind != jl::Value::Bool) throw ConfigError("detail_metrics must be a boolean");
+  c.set("detail_metrics", jl::Value::boolean(in.find("detail_metrics") ? in.find("detail_metrics")->b : cmd == "run"));
   return c;
 }
 
@@ -722,32 +727,36 @@ struct RunOut {
   std::vector<kvsim_point_summary> sum;
   std::vector<kvsim_request_record> recs;
   std::vector<int64_t> rec_off;
-  std::vector<kvsim_event_record> ev;
-  std::vector<int64_t> ev_cnt;
-  size_t ev_cap = 0;
+  std::vector<kvsim_instance_record> inst;       // point i at i * KVSIM_MAX_INSTANCES
+  std::vector<std::vector<kvsim_event_record>> ev;  // complete per-point event logs
 };
+
+// Event logs: each chunk runs with a bounded per-point buffer (so host and
+// device memory stay bounded whatever the sweep size); a point whose log
+// overflowed it is re-run alone with a buffer of its exact event count
+// (the simulation is deterministic), so every written log is complete.
+constexpr size_t kEvBytesPerChunk = size_t(256) << 20;
+constexpr size_t kEvCapStart = size_t(1) << 16;
 
 // One host thread per GPU pulling chunks of points from a shared counter;
 // results land at their point index, so the merge is deterministic and
 // independent of the GPU count.
-void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, int gpus, bool records, size_t ev_cap,
-                RunOut& out) {
+void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, int gpus, bool records, bool events,
+                bool detail, RunOut& out) {
   const size_t n = pts.size();
   out.sum.assign(n, kvsim_point_summary{});
   out.rec_off.assign(n + 1, 0);
   for (size_t i = 0; i < n; ++i) out.rec_off[i + 1] = out.rec_off[i] + pts[i].num_requests;
   if (records) out.recs.assign((size_t)out.rec_off[n], kvsim_request_record{});
-  out.ev_cap = ev_cap;
-  if (ev_cap) {
-    out.ev.assign(n * ev_cap, kvsim_event_record{});
-    out.ev_cnt.assign(n, 0);
-  }
+  out.inst.assign(n * KVSIM_MAX_INSTANCES, kvsim_instance_record{});
+  if (events) out.ev.assign(n, {});
   kvsim_trace_view tv{};
   if (trace) tv = kvsim_trace_view{trace->arr.data(), trace->pl.data(), trace->dl.data(), (int64_t)trace->arr.size()};
   const int ndev = kvsim_gpu_device_count();
   if (ndev <= 0) throw std::runtime_error("no CUDA device available (kvsim has no CPU fallback)");
   if (gpus <= 0 || gpus > ndev) gpus = ndev < 1 ? 1 : (gpus <= 0 ? 1 : ndev);
-  const size_t chunk = std::max<size_t>(1, std::min<size_t>(65536, (n + 4 * gpus - 1) / (4 * gpus)));
+  size_t chunk = std::max<size_t>(1, std::min<size_t>(65536, (n + 4 * gpus - 1) / (4 * gpus)));
+  if (events) chunk = std::min(chunk, std::max<size_t>(1, kEvBytesPerChunk / (kEvCapStart * sizeof(kvsim_event_record))));
   std::atomic<size_t> next{0};
   std::vector<std::string> errors(gpus);
   std::vector<std::thread> th;
@@ -756,16 +765,48 @@ void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, in
       char err[512] = {0};
       kvsim_gpu_ctx* ctx = nullptr;
       if (kvsim_gpu_open(g, &ctx, err, sizeof err) != 0) { errors[g] = err; return; }
+      std::vector<kvsim_event_record> evbuf;
+      std::vector<int64_t> evcnt;
       for (;;) {
         const size_t a = next.fetch_add(chunk);
         if (a >= n) break;
         const size_t b = std::min(n, a + chunk);
-        // records of a chunk are contiguous: rec_off[a..b)
-        int rc = kvsim_gpu_run(ctx, pts.data() + a, b - a, trace ? &tv : nullptr, trace ? 1 : 0, out.sum.data() + a,
-                               records ? out.recs.data() + out.rec_off[a] : nullptr,
-                               ev_cap ? out.ev.data() + a * ev_cap : nullptr, ev_cap,
-                               ev_cap ? out.ev_cnt.data() + a : nullptr, err, sizeof err);
+        kvsim_run_opts o{};
+        o.detail = detail ? 1 : 0;
+        o.recs = records ? out.recs.data() + out.rec_off[a] : nullptr;  // records of a chunk are contiguous
+        o.inst = out.inst.data() + a * KVSIM_MAX_INSTANCES;
+        if (events) {
+          evbuf.assign((b - a) * kEvCapStart, kvsim_event_record{});
+          evcnt.assign(b - a, 0);
+          o.ev = evbuf.data();
+          o.ev_cap = kEvCapStart;
+          o.ev_count = evcnt.data();
+        }
+        int rc = kvsim_gpu_run_ex(ctx, pts.data() + a, b - a, trace ? &tv : nullptr, trace ? 1 : 0, out.sum.data() + a,
+                                  &o, err, sizeof err);
         if (rc != 0) { errors[g] = err; break; }
+        if (!events) continue;
+        for (size_t i = a; i < b; ++i) {
+          const int64_t k = evcnt[i - a];
+          if (k <= (int64_t)kEvCapStart) {
+            out.ev[i].assign(evbuf.begin() + (i - a) * kEvCapStart, evbuf.begin() + (i - a) * kEvCapStart + k);
+            continue;
+          }
+          // overflowed: rerun this point alone with an exact-size log
+          std::vector<kvsim_event_record> big((size_t)k);
+          int64_t k2 = 0;
+          kvsim_point_summary s2{};
+          kvsim_run_opts o2{};
+          o2.detail = detail ? 1 : 0;
+          o2.ev = big.data();
+          o2.ev_cap = (size_t)k;
+          o2.ev_count = &k2;
+          rc = kvsim_gpu_run_ex(ctx, &pts[i], 1, trace ? &tv : nullptr, trace ? 1 : 0, &s2, &o2, err, sizeof err);
+          if (rc != 0) { errors[g] = err; break; }
+          if (k2 != k) { errors[g] = "event count changed on rerun (non-deterministic run)"; break; }
+          out.ev[i].swap(big);
+        }
+        if (!errors[g].empty()) break;
       }
       kvsim_gpu_close(ctx);
     });
@@ -803,13 +844,18 @@ jl::Value summary_json(const kvsim_point_summary& s) {
   D("cost_eff", s.cost_eff); D("idle_frac", s.idle_frac); D("peak_kv_gb", s.peak_kv_gb);
   D("link_prefill_gb", s.link_prefill_gb); D("link_mirror_gb", s.link_mirror_gb);
   D("busy_s_total", s.busy_s_total);
+  D("ttft_queue_mean", s.ttft_queue_mean);
+  D("tbt_p50", s.tbt_p50); D("tbt_p95", s.tbt_p95);
+  D("idle_runnable_s", s.idle_runnable_s);
+  I("n_tbt_samples", s.n_tbt_samples);
   return o;
 }
 
 const char* ev_name(int k) {
-  static const char* names[] = {"?", "arrive", "prefill_start", "prefill_done", "step_start", "step_end", "move",
-                                "evict", "preempt", "role", "transfer", "wake", "join", "copy"};
-  return (k >= 0 && k <= 13) ? names[k] : "?";
+  static const char* names[] = {"?",    "arrive", "prefill_start", "prefill_done", "step_start", "step_end",
+                                "move", "evict",  "preempt",       "role",         "transfer",   "wake",
+                                "join", "copy",   "timer",         "level",        "mode"};
+  return (k >= 0 && k <= 16) ? names[k] : "?";
 }
 
 jl::Value meta_json(const jl::Value& cfg, const std::string& cmd) {
@@ -1033,10 +1079,10 @@ int cmd_main(const Args& a) {
   }
   if (a.cmd != "run" && a.cmd != "sweep" && a.cmd != "resource-sweep") usage();
   const bool records = cfg.find("emit_records")->b;
-  const size_t ev_cap = a.emit_events ? (size_t)1 << 20 : 0;
+  const bool detail = cfg.find("detail_metrics")->b;
   RunOut r;
   logf(1, "%s: %zu point(s) on %d GPU(s)", a.cmd.c_str(), pts.size(), a.gpus);
-  run_points(pts, has_trace ? &trace : nullptr, a.gpus, records, ev_cap, r);
+  run_points(pts, has_trace ? &trace : nullptr, a.gpus, records, a.emit_events, detail, r);
   // summary.csv (stable 13 columns) + sweep axes
   std::string csv = std::string(kSummaryCols) + ",instances,device,seed,status\n";
   for (size_t i = 0; i < pts.size(); ++i)
@@ -1054,6 +1100,29 @@ int cmd_main(const Args& a) {
     e.set("device", jl::Value::string(meta[i].device));
     e.set("seed", jl::Value::number((double)meta[i].seed));
     e.set("summary", summary_json(r.sum[i]));
+    {
+      // per-instance idle fraction and peak KV
+      const kvsim_point_summary& su = r.sum[i];
+      const double window = su.makespan_s - pts[i].warmup_s;
+      const double kvb = 2.0 * pts[i].num_layers * pts[i].num_kv_heads * pts[i].head_dim * pts[i].bytes_per_value;
+      jl::Value ia = jl::Value::array();
+      for (int x = 0; x < su.num_instances; ++x) {
+        const kvsim_instance_record& q = r.inst[i * KVSIM_MAX_INSTANCES + x];
+        jl::Value o = jl::Value::object();
+        o.set("instance", jl::Value::number(x));
+        o.set("initial_role", jl::Value::string(q.initial_role ? "prefill" : "decode"));
+        o.set("busy_s", jl::Value::number(q.busy_s));
+        o.set("idle_frac", window > 0 ? jl::Value::number(1.0 - q.busy_s / window) : jl::Value());
+        o.set("idle_runnable_s", jl::Value::number(q.idle_runnable_s));
+        o.set("peak_kv_gb", jl::Value::number((double)q.peak_kv_tokens * kvb / 1e9));
+        ia.push(o);
+      }
+      e.set("instances_detail", ia);
+      jl::Value q = jl::Value::object();
+      q.set("max", jl::Value::number((double)su.queue_depth_max));
+      q.set("time_avg", std::isnan(su.queue_depth_avg) ? jl::Value() : jl::Value::number(su.queue_depth_avg));
+      e.set("queue_depth", q);
+    }
     if (records && a.cmd == "run") {
       jl::Value rq = jl::Value::array();
       for (int64_t k = 0; k < r.sum[i].n_requests; ++k) {
@@ -1065,6 +1134,7 @@ int cmd_main(const Args& a) {
         x.set("jct_s", jl::Value::number(q.completion_s - q.arrival_s));
         x.set("tbt_max_s", jl::Value::number(q.tbt_max_s));
         x.set("tbt_mean_s", q.decode_len > 1 ? jl::Value::number((q.completion_s - q.first_token_s) / (q.decode_len - 1)) : jl::Value());
+        x.set("queue_wait_s", jl::Value::number(q.prefill_start_s - q.arrival_s));
         x.set("prompt_len", jl::Value::number(q.prompt_len));
         x.set("decode_len", jl::Value::number(q.decode_len));
         rq.push(x);
@@ -1124,60 +1194,40 @@ int cmd_main(const Args& a) {
     write_file(a.out + "/resource_sweep.csv", rc);
     report.set("knees", resource_knees(meta, r.sum));
   }
-  if (ev_cap) {
+  write_file(a.out + "/report.json", jl::dump(report) + "\n");
+  write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
+  if (a.emit_events) {
     // queue-depth time series (SPEC.md:358 MetricsReport diagnostics), rebuilt
-    // from the event log: +1 per arrival and per preemption (the request
-    // re-enters its queue), minus the prompts a prefill job (unified: a
-    // co-batched iteration) takes. One row per timestamp with the depth after
-    // all of that timestamp's events; report.json gets max and time average.
-    std::string qd = "point,t,depth\n";
-    jl::Value& pl = *const_cast<jl::Value*>(report.find("points"));
+    // from the (complete) event logs: +1 per arrival and per preemption (the
+    // request re-enters its queue), minus the prompts a prefill job (unified:
+    // a co-batched iteration) takes; one row per timestamp with the depth
+    // after that timestamp's events. Its max / time average are the device's
+    // queue_depth_* summary fields (report.json).
+    FILE* qf = std::fopen((a.out + "/queue_depth.csv").c_str(), "w");
+    FILE* ef = std::fopen((a.out + "/events.jsonl").c_str(), "w");
+    if (!qf || !ef) throw std::runtime_error("cannot write event outputs in " + a.out);
+    std::fputs("point,t,depth\n", qf);
     for (size_t i = 0; i < pts.size(); ++i) {
-      const int64_t k = std::min<int64_t>(r.ev_cnt[i], (int64_t)ev_cap);
       std::vector<std::pair<double, int64_t>> dv;
-      for (int64_t j = 0; j < k; ++j) {
-        const kvsim_event_record& e = r.ev[i * ev_cap + j];
+      for (const kvsim_event_record& e : r.ev[i]) {
         if (e.kind == KVSIM_EV_ARRIVE || e.kind == KVSIM_EV_PREEMPT) dv.push_back({e.t, 1});
         else if (e.kind == KVSIM_EV_PREFILL_START) dv.push_back({e.t, -(int64_t)e.a});
         else if (e.kind == KVSIM_EV_STEP_START && pts[i].policy == KVSIM_POLICY_UNIFIED && e.b > 0)
           dv.push_back({e.t, -(int64_t)e.b});
       }
       std::stable_sort(dv.begin(), dv.end(), [](auto& x, auto& y) { return x.first < y.first; });
-      int64_t depth = 0, dmax = 0;
-      double area = 0, tprev = 0;
+      int64_t depth = 0;
       for (size_t j = 0; j < dv.size();) {
         const double t = dv[j].first;
-        area += (double)depth * (t - tprev);
-        tprev = t;
         for (; j < dv.size() && dv[j].first == t; ++j) depth += dv[j].second;
-        dmax = std::max(dmax, depth);
-        qd += std::to_string(i) + "," + num(t) + "," + std::to_string(depth) + "\n";
+        std::fprintf(qf, "%zu,%s,%lld\n", i, num(t).c_str(), (long long)depth);
       }
-      const double span = r.sum[i].makespan_s;
-      if (span > tprev) area += (double)depth * (span - tprev);
-      jl::Value q = jl::Value::object();
-      q.set("max", jl::Value::number((double)dmax));
-      q.set("time_avg", span > 0 ? jl::Value::number(area / span) : jl::Value());
-      q.set("truncated", jl::Value::boolean(r.ev_cnt[i] > (int64_t)ev_cap));
-      pl.arr[i].set("queue_depth", q);
+      for (const kvsim_event_record& e : r.ev[i])
+        std::fprintf(ef, "{\"point\":%zu,\"t\":%s,\"kind\":\"%s\",\"inst\":%d,\"a\":%d,\"b\":%d,\"c\":%lld}\n", i,
+                     num(e.t).c_str(), ev_name(e.kind), e.inst, e.a, e.b, (long long)e.c);
     }
-    write_file(a.out + "/queue_depth.csv", qd);
-  }
-  write_file(a.out + "/report.json", jl::dump(report) + "\n");
-  write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
-  if (ev_cap) {
-    std::string ej;
-    for (size_t i = 0; i < pts.size(); ++i) {
-      const int64_t k = std::min<int64_t>(r.ev_cnt[i], (int64_t)ev_cap);
-      for (int64_t j = 0; j < k; ++j) {
-        const kvsim_event_record& e = r.ev[i * ev_cap + j];
-        ej += "{\"point\":" + std::to_string(i) + ",\"t\":" + num(e.t) + ",\"kind\":\"" + ev_name(e.kind) +
-              "\",\"inst\":" + std::to_string(e.inst) + ",\"a\":" + std::to_string(e.a) + ",\"b\":" +
-              std::to_string(e.b) + ",\"c\":" + std::to_string(e.c) + "}\n";
-      }
-      if (r.ev_cnt[i] > (int64_t)ev_cap) logf(1, "point %zu: event log truncated at %zu", i, ev_cap);
-    }
-    write_file(a.out + "/events.jsonl", ej);
+    std::fclose(qf);
+    std::fclose(ef);
   }
   int bad = 0;
   for (auto& s : r.sum) bad += s.status != 0;

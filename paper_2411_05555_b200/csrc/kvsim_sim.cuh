@@ -66,6 +66,7 @@ struct Counters {
   int64_t ev_n;  // event-log cursor (atomic; lanes log concurrently)
   int64_t adv_events;  // virtual step ends processed by advance() (lane atomics)
   int64_t lvl_tokens, n_ticks, n_modes;
+  int64_t t_n;   // detail runs: TBT (gap, count) entries written (atomic cursor)
 };
 struct WarpScratch {
   PointConst pc;  // written by lane 0 at point start, read (broadcast) by all
@@ -97,11 +98,19 @@ struct SweepArgs {
   int64_t* ev_count;
   // optional profiling: per point {start ns, end ns, slot} (globaltimer)
   unsigned long long* ptime;
+  // optional per-instance records (point i at i * KVSIM_MAX_INSTANCES)
+  kvsim_instance_record* inst;
+  // detail runs (pooled TBT percentiles): plain event loop, one (gap, count)
+  // entry per step / individual gap in [slot][Tcap]
+  int32_t detail;
+  int64_t Tcap;
+  double* t_val;
+  int32_t* t_cnt;
   // arena geometry
   int64_t Ncap, Bcap, Jcap;
   int32_t Imax, slots;
   // cold per-request arrays [slot][Ncap]
-  double *c_arr, *c_last, *c_tbt, *c_fresh, *c_first, *c_done;
+  double *c_arr, *c_last, *c_tbt, *c_fresh, *c_first, *c_done, *c_qs;
   int32_t *c_pl, *c_dl, *c_qlen, *c_em, *c_cpy, *c_nmv, *c_npre;
   int32_t* q_rid;  // [slot][Imax][Ncap] queue rings
   int32_t *b_rid, *b_rem, *b_kvb;
@@ -120,7 +129,8 @@ struct SweepArgs {
 // SEMANTICS §6b): copies live on the instance partner[x] names (x^1, or the
 // dual instance of a degraded group), all links use the directed-link matrix,
 // and step chaining is off (plain event loop).
-template <int POL, bool LOG, bool EXT = false>
+// DET: detail run (pooled TBT percentiles); implies the plain event loop.
+template <int POL, bool LOG, bool EXT = false, bool DET = false>
 struct Sim {
   const SweepArgs* A;  // kernel parameters (param space; __grid_constant__)
   WarpScratch* W;      // per-warp shared scratch: point constants, counters
@@ -137,7 +147,7 @@ struct Sim {
   int64_t n_events;
   double now;     // time of the event being processed (event-log timestamps)
   double t_last;  // latest event time processed (makespan)
-  static constexpr bool chain_steps = !EXT;  // exact step chaining (advance); off = plain event loop
+  static constexpr bool chain_steps = !EXT && !DET;  // exact step chaining (advance); off = plain event loop
   static constexpr bool logging = LOG;  // event log compiled in (parity runs) or out (sweeps)
   int32_t status;
   // lane-owned instance state (lane x <-> instance x)
@@ -160,6 +170,12 @@ struct Sim {
   int64_t L_lvl_bud;
   int32_t G_mode, G_cnt;
   int64_t tick;
+  // idle while runnable: this lane's instance has been idle
+  // since L_idle_t, when the zero-live measure was L_idle_z
+  double L_idle_t, L_idle_z, L_idle_rb;
+  // uniform: live requests, zero-live measure Z (since the warm-up), queue depth
+  int64_t live, qdepth, qd_max;
+  double zero_since, z_acc, qd_area, qd_tprev;
 
   // per-slot arena offsets, computed once (the accessors below run on every
   // arena access; recomputing slot * capacity from the parameter block each
@@ -199,6 +215,7 @@ struct Sim {
   KV_DEV double* c_fresh() const { return gp(A->c_fresh + o_c); }
   KV_DEV double* c_first() const { return gp(A->c_first + o_c); }
   KV_DEV double* c_done() const { return gp(A->c_done + o_c); }
+  KV_DEV double* c_qs() const { return gp(A->c_qs + o_c); }
   KV_DEV int32_t* c_pl() const { return gp(A->c_pl + o_c); }
   KV_DEV int32_t* c_dl() const { return gp(A->c_dl + o_c); }
   KV_DEV int32_t* c_qlen() const { return gp(A->c_qlen + o_c); }
@@ -276,6 +293,13 @@ struct Sim {
   }
 
   // ------------------------------------------------------------- queues
+  // queue depth series: area += depth * (now - previous change)
+  KV_DEV void qd_change(int64_t delta) {
+    qd_area = kadd(qd_area, kmul((double)qdepth, ksub(now, qd_tprev)));
+    qd_tprev = now;
+    qdepth += delta;
+    if (qdepth > qd_max) qd_max = qdepth;
+  }
   KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q), c = get(Q_n, q);
     int64_t idx = (int64_t)h + c;
@@ -283,6 +307,7 @@ struct Sim {
     if (lane == 0) ring(q)[idx] = rid;
     simt::sync();
     if (own(q)) { Q_n += 1; Q_tok += len; }
+    qd_change(1);
   }
   KV_DEV void q_push_front(int q, int32_t rid, int64_t len) {
     int32_t h = get(Q_head, q);
@@ -290,6 +315,7 @@ struct Sim {
     if (lane == 0) ring(q)[nh] = rid;
     simt::sync();
     if (own(q)) { Q_head = nh; Q_n += 1; Q_tok += len; }
+    qd_change(1);
   }
   KV_DEV int32_t q_at(int q, int32_t h, int64_t k) {
     int64_t idx = (int64_t)h + k;
@@ -297,6 +323,7 @@ struct Sim {
     return ring(q)[idx];
   }
   KV_DEV void q_pop(int q, int32_t k, int64_t tokens) {
+    if (k > 0) qd_change(-(int64_t)k);
     if (own(q)) {
       int64_t nh = (int64_t)Q_head + k;
       if (nh >= Ncap_) nh -= Ncap_;
@@ -351,6 +378,7 @@ struct Sim {
     pc.event_budget = 4 * pc.n_limit * ((int64_t)(evd > 1 ? evd : 1) + 2) + 4096;
     // validity (perfmodel validate())
     if (n < 1 || n > kMaxInst || n > A->Imax || d.policy != POL) status = KVSIM_E_INVALID;
+    else if (!geometry_fits(d)) status = KVSIM_E_INVALID;
     else if (policy == KVSIM_POLICY_ACCELLM && (n & 1)) status = KVSIM_E_ODD_INSTANCES;
     else if (policy == KVSIM_POLICY_SPLITWISE && (n < 2 || n_prefill >= n)) status = KVSIM_E_INVALID;
     else if (!pc.f.fits) status = KVSIM_E_MODEL_FIT;
@@ -381,6 +409,9 @@ struct Sim {
     L_lvl_bud = 0;
     G_mode = G_cnt = 0;
     tick = 1;
+    L_idle_t = L_idle_z = L_idle_rb = 0.0;
+    live = qdepth = qd_max = 0;
+    zero_since = z_acc = qd_area = qd_tprev = 0.0;
     // directed links (splitwise; AcceLLM EXT)
     if (policy == KVSIM_POLICY_SPLITWISE || EXT)
       for (int i = lane; i < n * n; i += 32) link_()[i] = 0.0;
@@ -390,6 +421,22 @@ struct Sim {
     if (status == KVSIM_OK) gen_next();
     simt::sync();
     return status == KVSIM_OK;
+  }
+
+  // the point must fit the arena geometry the launch was sized for
+  // (kvsim_arena.hpp size_arena); a device-resident caller could pass points
+  // that differ from its reservation, so this is re-checked per point
+  KV_DEV_NOINLINE bool geometry_fits(const kvsim_point_desc& d) const {
+    if (d.num_requests < 0 || d.num_requests > A->Ncap) return false;
+    if (d.trace_index >= 0) return A->tr_off != nullptr;  // traces: sized by the host from the trace itself
+    if (d.decode_max > kRemMask || d.prompt_max > kRemMask) return false;
+    const int64_t N = d.num_requests;
+    const int64_t pmin = d.prompt_min > 0 ? d.prompt_min : 1;
+    const Perf f = make_perf(d);
+    const int64_t cap = f.fits ? f.cap : 0;
+    const int64_t budget = d.prefill_token_budget > 0 ? d.prefill_token_budget : 8192;
+    const int64_t nb = cap / pmin + 2, nj = budget / pmin + 1;
+    return (N < nb ? N : nb) <= A->Bcap && (N < nj ? N : nj) <= A->Jcap;
   }
 
   // arrival generator (SEMANTICS §2); uniform across lanes
@@ -421,6 +468,7 @@ struct Sim {
     } else {
       double gap = ksub(t, c_last()[rid]);
       if (gap > c_tbt()[rid]) c_tbt()[rid] = gap;
+      if constexpr (DET) if (c_arr()[rid] >= PC.warmup) tbt_entry(gap, 1);
     }
     c_last()[rid] = t;
     em += 1;
@@ -431,9 +479,42 @@ struct Sim {
     if (lane == 0) ws()->ct.tok_total += k;
     if (t >= PC.warmup) if (lane == 0) ws()->ct.tok_window += k;
   }
+  // detail runs: one TBT entry (gap shared by cnt samples); divergent-safe
+  KV_DEV void tbt_entry(double gap, int32_t cnt) {
+    const int64_t k = simt::atomic_add_smem(&ws()->ct.t_n, (int64_t)1);
+    if (k < A->Tcap) {
+      gp(A->t_val + (int64_t)slot * A->Tcap)[k] = gap;
+      gp(A->t_cnt + (int64_t)slot * A->Tcap)[k] = cnt;
+    }
+  }
+  // ---- idle while runnable (SEMANTICS §7)
+  KV_DEV double clip(double t) const { return t > PC.warmup ? t : PC.warmup; }
+  // Z(t): measure of [warm-up, t] with no live request
+  KV_DEV double zeta(double t) const { return live == 0 ? kadd(z_acc, ksub(clip(t), clip(zero_since))) : z_acc; }
+  // uniform: k requests arrive (k > 0) or complete (k < 0) at t
+  KV_DEV void live_add(int64_t k, double t) {
+    if (live == 0 && k > 0) z_acc = kadd(z_acc, ksub(clip(t), clip(zero_since)));
+    live += k;
+    if (live == 0) zero_since = t;
+  }
+  // a job starts on x at t: close x's idle period
+  KV_DEV void job_begin(int x, double t) {
+    const double z = zeta(t);
+    if (own(x)) {
+      const double a = ksub(clip(t), clip(L_idle_t));
+      const double b = ksub(z, L_idle_z);
+      L_idle_rb = kadd(L_idle_rb, ksub(a, b));
+    }
+  }
+  // a job ends on x at t: busy time; x's idle period (if any) starts here
   KV_DEV void account_job(int x, double t) {
     double js = get(L_job_start, x);
-    if (own(x) && js >= PC.warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
+    const double z = zeta(t);
+    if (own(x)) {
+      if (js >= PC.warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
+      L_idle_t = t;
+      L_idle_z = z;
+    }
   }
 
   // ------------------------------------------------------- hot decode loop
@@ -459,6 +540,7 @@ struct Sim {
     int32_t* kvb_a = b_kvb(x);
     double* tbt_a = b_tbt(x);
     int32_t wpos = 0, completed = 0, m = 0, copy_done = 0, minrem = 0x7fffffff;
+    int32_t ncont = 0;  // detail runs: measured members sharing the gap t - prev
     int64_t kv_done = 0, copy_free = 0, kvmin = INT64_MAX;  // per-lane partials
     for (int32_t j0 = 0; j0 < nb; j0 += 32) {
       const int32_t j = j0 + lane;
@@ -478,7 +560,7 @@ struct Sim {
       const unsigned sm = simt::ballot(surv);
       const int32_t dst = wpos + simt::popc(sm & simt::lanemask_lt());
       const bool moved = surv && dst != j;
-      if (act && (was_joiner || done || moved)) rid = rid_a[j];
+      if (act && (DET || was_joiner || done || moved)) rid = rid_a[j];
       double gap = 0.0;
       bool upd = false;
       if (act) {
@@ -491,6 +573,11 @@ struct Sim {
         const double last = joiner ? c_last()[rid] : prev;
         gap = ksub(t, last);
         if (gap > tb) { tb = gap; upd = true; }
+      }
+      if constexpr (DET) {
+        const bool inc = act && c_arr()[rid] >= PC.warmup;
+        if (inc && joiner) tbt_entry(gap, 1);
+        ncont += simt::popc(simt::ballot(inc && !joiner));
       }
       if (done || moved) kvb = kvb_a[j];
       m += simt::popc(simt::ballot(act && hasc));
@@ -522,6 +609,9 @@ struct Sim {
       completed += simt::popc(dm);
       copy_done += simt::popc(simt::ballot(done && hasc));
       wpos += simt::popc(sm);
+    }
+    if constexpr (DET) {
+      if (ncont > 0 && lane == 0) tbt_entry(ksub(t, prev), ncont);
     }
     o.nb_old = nb;
     o.completed = completed;
@@ -812,6 +902,7 @@ struct Sim {
     const int64_t K = get(L_skv, x);
     add_used(x, nb);
     const double lat = decode_latency(PC.f, nb, K);
+    job_begin(x, t);
     if (own(x)) {
       L_job = JOB_STEP;
       L_job_start = t;
@@ -839,6 +930,7 @@ struct Sim {
       L_final -= o.kv_done + o.completed;
     }
     count_tokens(o.nb_old, t);
+    if (o.completed) live_add(-(int64_t)o.completed, t);
     if (policy == KVSIM_POLICY_ACCELLM) {
       const int y = partner_of(x);
       if (own(y)) { L_used -= o.copy_free; L_copy_tok -= o.copy_free; }
@@ -1204,7 +1296,10 @@ struct Sim {
       const unsigned fail = simt::ballot(valid && !(okb && okm));
       const int32_t nvalid = simt::popc(simt::ballot(valid));
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
-      if (lane < take) j_rid(x)[k + lane] = rid;
+      if (lane < take) {
+        j_rid(x)[k + lane] = rid;
+        if (c_em()[rid] == 0) c_qs()[rid] = t;
+      }
       const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
       const int64_t tsq = simt::warp_sum_nn(lane < take ? len * len : (int64_t)0);
       s1 += tsum;
@@ -1220,6 +1315,7 @@ struct Sim {
     }
     if (nb == 0 && k == 0) return;
     const double lat = kadd(k ? prefill_latency(PC.f, s1, s2) : 0.0, nb ? decode_latency(PC.f, nb, K) : 0.0);
+    job_begin(x, t);
     if (own(x)) {
       L_job = JOB_STEP;
       L_job_start = t;
@@ -1275,6 +1371,7 @@ struct Sim {
     minrem = simt::warp_min_i32(minrem);
     simt::sync();
     count_tokens(k, t);
+    if (completed) live_add(-(int64_t)completed, t);
     if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
@@ -1317,7 +1414,11 @@ struct Sim {
           const int d = simt::ffs(simt::ballot(fr == best)) - 1;
           if (best < len) { stop = true; break; }
           add_used(d, len);
-          if (lane == 0) { j_rid(p)[k] = rid; j_dst(p)[k] = d; }
+          if (lane == 0) {
+            j_rid(p)[k] = rid;
+            j_dst(p)[k] = d;
+            if (c_em()[rid] == 0) c_qs()[rid] = t;
+          }
           s1 += len;
           s2 += len * len;
           k += 1;
@@ -1328,6 +1429,7 @@ struct Sim {
       q_pop(0, k, s1);
       add_used(p, s1);
       const double lat = prefill_latency(PC.f, s1, s2);
+      job_begin(p, t);
       if (own(p)) {
         L_job = JOB_PREFILL;
         L_job_start = t;
@@ -1373,6 +1475,7 @@ struct Sim {
     }
     simt::sync();
     count_tokens(k, t);
+    if (completed) live_add(-(int64_t)completed, t);
     log(KVSIM_EV_PREFILL_DONE, p, k, completed, 0);
     // one transfer per destination, ascending id; lane d keeps the finish time
     double fin_mine = 0.0;
@@ -1560,7 +1663,10 @@ struct Sim {
       const unsigned fail = simt::ballot(valid && !(okb && okm));
       const int32_t nvalid = simt::popc(simt::ballot(valid));
       const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
-      if (lane < take) j_rid(x)[k + lane] = rid;
+      if (lane < take) {
+        j_rid(x)[k + lane] = rid;
+        if (c_em()[rid] == 0) c_qs()[rid] = t;
+      }
       const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
       const int64_t tsq = simt::warp_sum_nn(lane < take ? len * len : (int64_t)0);
       s1 += tsum;
@@ -1583,6 +1689,7 @@ struct Sim {
     simt::sync();
     q_pop(q, k, s1);
     const double lat = prefill_latency(PC.f, s1, s2);
+    job_begin(x, t);
     if (own(x)) {
       L_job = JOB_PREFILL;
       L_job_start = t;
@@ -1752,6 +1859,7 @@ struct Sim {
     simt::sync();
     if (own(x)) L_used -= kvfree;
     count_tokens(k, t);
+    if (completed) live_add(-(int64_t)completed, t);
     log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
     if constexpr (EXT) {
       if (is_dual(x)) {
@@ -2239,6 +2347,7 @@ struct Sim {
   // -------------------------------------------------------------- arrival
   KV_DEV_NOINLINE void arrive(double t) {
     EMU_COUNT(16);
+    live_add(1, t);
     const int64_t rid64 = next_rid;
     const int32_t rid = (int32_t)rid64;
     int32_t pl, dl;
@@ -2261,6 +2370,7 @@ struct Sim {
       c_fresh()[rid] = 0.0;
       c_first()[rid] = 0.0;
       c_done()[rid] = 0.0;
+      c_qs()[rid] = 0.0;
       c_nmv()[rid] = 0;
       c_npre()[rid] = 0;
     }
@@ -2397,6 +2507,38 @@ struct Sim {
     r1 = pre1;
     r2 = pre2;
   }
+  // the same over weighted entries (detail runs: (gap, count) TBT entries)
+  KV_DEV_NOINLINE void radix_select2_w(const double* arr, const int32_t* w, int64_t nn, int64_t k1, int64_t k2,
+                                       uint64_t& r1, uint64_t& r2) {
+    uint64_t pre1 = 0, pre2 = 0, mask = 0;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int b = lane; b < 256; b += 32) { ws()->hist[0][b] = 0; ws()->hist[1][b] = 0; }
+      simt::sync();
+      for (int64_t i = lane; i < nn; i += 32) {
+        const uint64_t kk = as_u64(arr[i]);
+        const uint32_t dg = (uint32_t)((kk >> shift) & 255u);
+        const uint32_t c = (uint32_t)w[i];
+        if ((kk & mask) == pre1) simt::atomic_add_smem(&ws()->hist[0][dg], c);
+        if ((kk & mask) == pre2) simt::atomic_add_smem(&ws()->hist[1][dg], c);
+      }
+      simt::sync();
+      int64_t acc1 = 0, acc2 = 0;
+      int b1 = -1, b2 = -1;
+      for (int b = 0; b < 256; ++b) {
+        const int64_t h1 = ws()->hist[0][b], h2 = ws()->hist[1][b];
+        if (b1 < 0 && acc1 + h1 > k1) b1 = b; else if (b1 < 0) acc1 += h1;
+        if (b2 < 0 && acc2 + h2 > k2) b2 = b; else if (b2 < 0) acc2 += h2;
+      }
+      k1 -= acc1;
+      k2 -= acc2;
+      pre1 |= (uint64_t)b1 << shift;
+      pre2 |= (uint64_t)b2 << shift;
+      mask |= (uint64_t)255u << shift;
+      simt::sync();
+    }
+    r1 = pre1;
+    r2 = pre2;
+  }
 
   KV_DEV_NOINLINE void finalize() {
     kvsim_point_summary s;
@@ -2430,8 +2572,29 @@ struct Sim {
       s.n_timer_ticks = ct.n_ticks;
       s.n_mode_switches = ct.n_modes;
       const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
-      double busy = 0.0;
-      for (int x = 0; x < n; ++x) busy = kadd(busy, get(L_busy_time, x));
+      // instances idle at the end: their idle period runs to the makespan
+      for (int x = 0; x < n; ++x)
+        if (get(L_job, x) == JOB_NONE) job_begin(x, t_last);
+      double busy = 0.0, irb = 0.0;
+      for (int x = 0; x < n; ++x) {
+        busy = kadd(busy, get(L_busy_time, x));
+        irb = kadd(irb, get(L_idle_rb, x));
+      }
+      s.idle_runnable_s = irb;
+      s.queue_depth_max = qd_max;
+      {
+        const double area = kadd(qd_area, kmul((double)qdepth, ksub(t_last, qd_tprev)));
+        s.queue_depth_avg = t_last > 0.0 ? kdiv(area, t_last) : kNaN;
+      }
+      if (A->inst != nullptr && lane < n) {
+        kvsim_instance_record ir;
+        ir.busy_s = L_busy_time;
+        ir.idle_runnable_s = L_idle_rb;
+        ir.peak_kv_tokens = L_peak;
+        ir.initial_role = (policy == KVSIM_POLICY_SPLITWISE && lane < n_prefill) ? ROLE_PREFILL : ROLE_DECODE;
+        ir.reserved = 0;
+        A->inst[point * KVSIM_MAX_INSTANCES + lane] = ir;
+      }
       s.peak_kv_tokens = peak;
       s.busy_s_total = busy;
       s.peak_kv_gb = kdiv(kmul((double)peak, PC.f.kvb), 1e9);
@@ -2451,18 +2614,19 @@ struct Sim {
           r.decode_len = c_dl()[i];
           r.n_moves = c_nmv()[i];
           r.n_preemptions = c_npre()[i];
+          r.prefill_start_s = c_em()[i] > 0 ? c_qs()[i] : kNaN;
           R[i] = r;
         }
       }
       simt::sync();
       // sequential (rid-order) sums, maxima; keys for selection
-      double s_ttft = 0.0, s_jct = 0.0, s_tbt = 0.0, tmax = 0.0;
+      double s_ttft = 0.0, s_jct = 0.0, s_tbt = 0.0, tmax = 0.0, s_qw = 0.0;
       int64_t n_tbt = 0, m = 0, completed = 0;
       double mx_ttft = 0.0, mx_jct = 0.0;
       for (int64_t i0 = 0; i0 < N; i0 += 32) {
         const int64_t i = i0 + lane;
         const bool act = i < N;
-        double a = 0.0, b = 0.0, tb = 0.0, ts = 0.0;
+        double a = 0.0, b = 0.0, tb = 0.0, ts = 0.0, qw = 0.0;
         bool inc = false, dn = false;
         int32_t dl = 0;
         if (act) {
@@ -2475,6 +2639,7 @@ struct Sim {
             b = ksub(c_done()[i], arr);
             ts = ksub(c_done()[i], c_first()[i]);
             tb = c_tbt()[i];
+            qw = ksub(c_qs()[i], arr);
           }
         }
         simt::sync();
@@ -2490,11 +2655,13 @@ struct Sim {
           const bool il = simt::shfl((int32_t)inc, l) != 0;
           const double al = simt::shfl(a, l), bl = simt::shfl(b, l), tsl = simt::shfl(ts, l);
           const double tbl = simt::shfl(tb, l);
+          const double qwl = simt::shfl(qw, l);
           const int32_t dll = simt::shfl(dl, l);
           if (il) {
             m += 1;
             s_ttft = kadd(s_ttft, al);
             s_jct = kadd(s_jct, bl);
+            s_qw = kadd(s_qw, qwl);
             if (al > mx_ttft) mx_ttft = al;
             if (bl > mx_jct) mx_jct = bl;
             if (dll > 1) {
@@ -2527,6 +2694,26 @@ struct Sim {
       }
       s.tbt_mean = n_tbt > 0 ? kdiv(s_tbt, (double)n_tbt) : kNaN;
       s.tbt_max = n_tbt > 0 ? tmax : kNaN;
+      s.n_tbt_samples = n_tbt;
+      s.ttft_queue_mean = m > 0 ? kdiv(s_qw, (double)m) : kNaN;
+      s.tbt_p50 = s.tbt_p95 = kNaN;
+      if constexpr (DET) {
+        const int64_t ne = ws()->ct.t_n;
+        if (n_tbt > 0 && ne <= A->Tcap && n_tbt < (int64_t)0xffffffffll) {
+          const double* tv = gp(A->t_val + (int64_t)slot * A->Tcap);
+          const int32_t* tc = gp(A->t_cnt + (int64_t)slot * A->Tcap);
+          int64_t wsum = 0;
+          for (int64_t i = lane; i < ne; i += 32) wsum += tc[i];
+          wsum = simt::warp_sum_nn(wsum);
+          if (wsum == n_tbt) {
+            const int64_t k50 = (50 * n_tbt + 99) / 100 - 1, k95 = (95 * n_tbt + 99) / 100 - 1;
+            uint64_t r1, r2;
+            radix_select2_w(tv, tc, ne, k50, k95, r1, r2);
+            s.tbt_p50 = as_f64(r1);
+            s.tbt_p95 = as_f64(r2);
+          }
+        }
+      }
       const double window = ksub(t_last, PC.warmup);
       if (window > 0.0) {
         s.cost_eff = kdiv((double)ct.tok_window, kmul(window, (double)n));
@@ -2545,9 +2732,9 @@ struct Sim {
 };
 
 // One point, simulated by the policy-specialised core.
-template <int P, bool LOG, bool EXT = false>
+template <int P, bool LOG, bool EXT = false, bool DET = false>
 KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot, int64_t pt) {
-  Sim<P, LOG, EXT> sim(ap, w, slot);
+  Sim<P, LOG, EXT, DET> sim(ap, w, slot);
   if (sim.init_point(pt)) sim.run();
   sim.finalize();
 }
@@ -2576,7 +2763,12 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
       a.ptime[3 * pt] = t0;
     }
 #endif
-    if (ext) {
+    if (a.detail) {  // reports: plain event loop, pooled TBT percentiles
+      if (ext) run_point<KVSIM_POLICY_ACCELLM, true, true, true>(ap, w, slot, pt);
+      else if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE, true, false, true>(ap, w, slot, pt);
+      else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, true, false, true>(ap, w, slot, pt);
+      else run_point<KVSIM_POLICY_UNIFIED, true, false, true>(ap, w, slot, pt);
+    } else if (ext) {
       if (a.ev != nullptr) run_point<KVSIM_POLICY_ACCELLM, true, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_ACCELLM, false, true>(ap, w, slot, pt);
     } else if (a.ev != nullptr) {

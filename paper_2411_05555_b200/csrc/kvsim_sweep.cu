@@ -122,7 +122,8 @@ struct kvsim_gpu_ctx {
   int sms = 0;
   int blocks_per_sm = 1;
   cudaStream_t stream = nullptr;
-  DevBuf arena, pts, order, out, recs, rec_off, ev, ev_count, tr_arr, tr_pl, tr_dl, tr_off, tr_n, tr_dmax, counter, ptime;
+  DevBuf arena, pts, order, out, recs, rec_off, ev, ev_count, tr_arr, tr_pl, tr_dl, tr_off, tr_n, tr_dmax, counter, ptime,
+      inst;
   bool point_times = false;  // KVSIM_POINT_TIMES: record per-point start/end (profiling)
   int64_t ptime_n = 0;
   kvsim_host::ArenaGeom geom;
@@ -246,41 +247,58 @@ int kvsim_point_validate(const kvsim_point_desc* p, char* err, size_t err_len) {
 int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   *out = nullptr;
   int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
     return set_err(err, err_len, KVSIM_E_NO_DEVICE, "no CUDA device available (kvsim has no CPU fallback)");
+  }
   if (device < 0 || device >= n) return set_err(err, err_len, KVSIM_E_INVALID, "device index out of range");
   KV_CUDA(cudaSetDevice(device));
   cudaDeviceProp prop;
   KV_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
-    return set_err(err, err_len, KVSIM_E_NO_DEVICE, "kvsim kernels are built for sm_100a (Blackwell) only");
-  auto* c = new kvsim_gpu_ctx();
-  c->device = device;
-  c->sms = prop.multiProcessorCount;
-  c->minb = kDefaultMinBlocks;
-  if (const char* e = std::getenv("KVSIM_MINB")) c->minb = std::atoi(e);
-  c->kernel = sweep_variant(c->minb);
-  c->point_times = std::getenv("KVSIM_POINT_TIMES") != nullptr;
-  KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
-  // L1/shared split (percent of the unified array given to shared memory):
-  // the per-warp Sim object (local memory) and arena lines are served from
-  // L1, so keep shared memory near what 3 blocks need. Config-4 sweep,
-  // in-process A/B: driver default 5.39 s, 25% 5.31 s, 16% 5.30 s, 50% 5.52 s,
-  // 8% 6.00 s
-  int carve = kDefaultCarveout;
-  if (const char* e = std::getenv("KVSIM_CARVEOUT")) carve = std::atoi(e);
-  if (carve >= 0)
-    KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-  int bps = 1;
-  KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
-  c->blocks_per_sm = bps > 0 ? bps : 1;
-  // resident blocks per SM actually used (<= the occupancy limit): fewer
-  // co-resident warps thrash the instruction cache less
-  if (const char* e = std::getenv("KVSIM_BLOCKS_PER_SM")) {
-    const int want = std::atoi(e);
-    if (want >= 1 && want < c->blocks_per_sm) c->blocks_per_sm = want;
+  // the library carries sm_100a SASS only (no PTX): anything but compute
+  // capability 10.0 (sm_103, sm_12x, older parts) cannot load the kernels
+  if (prop.major != 10 || prop.minor != 0)
+    return set_err(err, err_len, KVSIM_E_NO_DEVICE,
+                   "kvsim kernels are built for sm_100a (B200) only; device is sm_" + std::to_string(prop.major) +
+                       std::to_string(prop.minor));
+  int minb = kDefaultMinBlocks;
+  if (const char* e = std::getenv("KVSIM_MINB")) {
+    minb = std::atoi(e);
+    if (minb != 2 && minb != 3)
+      return set_err(err, err_len, KVSIM_E_INVALID, "KVSIM_MINB must be 2 or 3 (the shipped kernel variants)");
   }
-  KV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  auto* c = new kvsim_gpu_ctx();
+  const int rc = [&]() -> int {
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    c->minb = minb;
+    c->kernel = sweep_variant(c->minb);
+    c->point_times = std::getenv("KVSIM_POINT_TIMES") != nullptr;
+    // the kernel image must actually load on this device
+    cudaFuncAttributes fa;
+    KV_CUDA(cudaFuncGetAttributes(&fa, c->kernel));
+    KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+    // L1/shared split (percent of the unified array given to shared memory),
+    // KVSIM_CARVEOUT overrides; -1 leaves the driver default
+    int carve = kDefaultCarveout;
+    if (const char* e = std::getenv("KVSIM_CARVEOUT")) carve = std::atoi(e);
+    if (carve >= 0)
+      KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    int bps = 1;
+    KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
+    c->blocks_per_sm = bps > 0 ? bps : 1;
+    // resident blocks per SM actually used (<= the occupancy limit)
+    if (const char* e = std::getenv("KVSIM_BLOCKS_PER_SM")) {
+      const int want = std::atoi(e);
+      if (want >= 1 && want < c->blocks_per_sm) c->blocks_per_sm = want;
+    }
+    KV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    return KVSIM_OK;
+  }();
+  if (rc != KVSIM_OK) {
+    kvsim_gpu_close(c);
+    return rc;
+  }
   *out = c;
   return KVSIM_OK;
 }
@@ -289,7 +307,7 @@ void kvsim_gpu_close(kvsim_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (DevBuf* b : {&c->arena, &c->pts, &c->order, &c->out, &c->recs, &c->rec_off, &c->ev, &c->ev_count, &c->ptime, &c->tr_arr,
-                    &c->tr_pl, &c->tr_dl, &c->tr_off, &c->tr_n, &c->tr_dmax, &c->counter})
+                    &c->tr_pl, &c->tr_dl, &c->tr_off, &c->tr_n, &c->tr_dmax, &c->counter, &c->inst})
     b->release();
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -307,6 +325,22 @@ int64_t kvsim_gpu_point_times(kvsim_gpu_ctx* c, uint64_t* out, int64_t cap) {
 int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const kvsim_trace_view* traces,
                   size_t n_traces, kvsim_point_summary* out, kvsim_request_record* recs, kvsim_event_record* ev,
                   size_t ev_cap, int64_t* ev_count, char* err, size_t err_len) {
+  kvsim_run_opts o{};
+  o.recs = recs;
+  o.ev = ev;
+  o.ev_cap = ev_cap;
+  o.ev_count = ev_count;
+  return kvsim_gpu_run_ex(c, pts, n, traces, n_traces, out, &o, err, err_len);
+}
+
+int kvsim_gpu_run_ex(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const kvsim_trace_view* traces,
+                     size_t n_traces, kvsim_point_summary* out, const kvsim_run_opts* opts, char* err,
+                     size_t err_len) {
+  const kvsim_run_opts o = opts ? *opts : kvsim_run_opts{};
+  kvsim_request_record* recs = o.recs;
+  kvsim_event_record* ev = o.ev;
+  const size_t ev_cap = o.ev_cap;
+  int64_t* ev_count = o.ev_count;
   if (!c) return set_err(err, err_len, KVSIM_E_INVALID, "null context");
   if (n == 0) return KVSIM_OK;
   if (!pts || !out) return set_err(err, err_len, KVSIM_E_INVALID, "null points/out");
@@ -329,6 +363,7 @@ int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const
       mn = std::min(mn, traces[k].prompt_len[i]);
       dm = std::max(dm, traces[k].decode_len[i]);
     }
+    if (dm > 0x0fffffff) return set_err(err, err_len, KVSIM_E_INVALID, "trace decode_len must be < 2^28");
     tmin[k] = traces[k].n ? mn : 1;
     tdmax[k] = dm;
   }
@@ -354,7 +389,7 @@ int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const
     KV_CUDA(cudaMemcpyAsync(c->tr_dmax.p, tdmax.data(), sizeof(int32_t) * n_traces, cudaMemcpyHostToDevice, s));
   }
   // arena
-  const kvsim_host::ArenaGeom g = kvsim_host::size_arena(pts, n, tn, tmin);
+  const kvsim_host::ArenaGeom g = kvsim_host::size_arena(pts, n, tn, tmin, o.detail != 0, tdmax);
   int rc = prepare_arena(c, g, n, err, err_len);
   if (rc) return rc;
   c->reserved = false;
@@ -393,6 +428,12 @@ int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const
   a.ev_cap = (int64_t)ev_cap;
   a.ev_count = (ev && ev_cap) ? (int64_t*)c->ev_count.p : nullptr;
   a.next_point = (unsigned long long*)c->counter.p;
+  a.detail = o.detail != 0;
+  if (o.inst) {
+    KV_CUDA(c->inst.ensure(sizeof(kvsim_instance_record) * KVSIM_MAX_INSTANCES * n));
+    KV_CUDA(cudaMemsetAsync(c->inst.p, 0, sizeof(kvsim_instance_record) * KVSIM_MAX_INSTANCES * n, s));
+    a.inst = (kvsim_instance_record*)c->inst.p;
+  }
   if (c->point_times) {
     KV_CUDA(c->ptime.ensure(sizeof(unsigned long long) * 3 * n));
     a.ptime = (unsigned long long*)c->ptime.p;
@@ -407,6 +448,9 @@ int kvsim_gpu_run(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, const
     KV_CUDA(cudaMemcpyAsync(ev, c->ev.p, sizeof(kvsim_event_record) * ev_cap * n, cudaMemcpyDeviceToHost, s));
     if (ev_count) KV_CUDA(cudaMemcpyAsync(ev_count, c->ev_count.p, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
   }
+  if (o.inst)
+    KV_CUDA(cudaMemcpyAsync(o.inst, c->inst.p, sizeof(kvsim_instance_record) * KVSIM_MAX_INSTANCES * n,
+                            cudaMemcpyDeviceToHost, s));
   KV_CUDA(cudaStreamSynchronize(s));
   return KVSIM_OK;
 }
@@ -439,6 +483,11 @@ int kvsim_gpu_run_device(kvsim_gpu_ctx* c, const kvsim_point_desc* d_pts, size_t
   if (!c || !c->reserved) return set_err(err, err_len, KVSIM_E_INVALID, "call kvsim_gpu_reserve first");
   if ((int64_t)n != c->reserved_args.n_pts)
     return set_err(err, err_len, KVSIM_E_INVALID, "point count differs from the reservation");
+  if (!d_pts || !d_out) return set_err(err, err_len, KVSIM_E_INVALID, "null device points/out");
+  KV_CUDA(cudaSetDevice(c->device));
+  // d_pts must hold the points passed to kvsim_gpu_reserve; the kernel
+  // re-checks every point against the reserved arena geometry and reports
+  // KVSIM_E_INVALID in its summary instead of overrunning a slot
   SweepArgs a = c->reserved_args;
   a.pts = d_pts;
   a.out = d_out;

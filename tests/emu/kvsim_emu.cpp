@@ -13,7 +13,7 @@
 
 extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_trace_view* traces, int64_t n_traces,
                          kvsim_point_summary* out, kvsim_request_record* recs, kvsim_event_record* ev,
-                         int64_t ev_cap, int64_t* ev_count, int n_warps) {
+                         int64_t ev_cap, int64_t* ev_count, int n_warps, kvsim_instance_record* inst, int detail) {
   using namespace kvsim_dev;
   for (int64_t i = 0; i < n; ++i) {
     if (kvsim_host::validate_point(pts[i], nullptr, 0) == KVSIM_E_INVALID) {
@@ -38,7 +38,7 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
     tmin.push_back(traces[k].n ? mn : 1);
     tdmax.push_back(dm);
   }
-  kvsim_host::ArenaGeom g = kvsim_host::size_arena(pts, (size_t)n, tn, tmin);
+  kvsim_host::ArenaGeom g = kvsim_host::size_arena(pts, (size_t)n, tn, tmin, detail != 0, tdmax);
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   const int32_t slots = n_warps;
@@ -66,6 +66,8 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
   a.ev_cap = ev_cap;
   a.ev_count = ev_count;
   a.next_point = &counter;
+  a.inst = inst;
+  a.detail = detail;
   std::vector<WarpScratch> scratch((size_t)slots);
   struct Job { SweepArgs* a; WarpScratch* s; int64_t slot; };
   std::vector<Job> jobs;

@@ -7,7 +7,7 @@ import math
 import os
 import subprocess
 
-from paper_2411_05555_b200.abi import (EventRecord, PointDesc, PointSummary, RequestRecord,
+from paper_2411_05555_b200.abi import (EventRecord, InstanceRecord, PointDesc, PointSummary, RequestRecord,
                                        TraceView, SUMMARY_FLOAT_FIELDS, SUMMARY_INT_FIELDS)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -41,6 +41,9 @@ def oracle():
         L.kvo_run_point.argtypes = [C.POINTER(PointDesc), C.POINTER(TraceView), C.POINTER(PointSummary),
                                     C.POINTER(RequestRecord), C.POINTER(EventRecord), C.c_int64,
                                     C.POINTER(C.c_int64)]
+        L.kvo_run_point_ex.argtypes = [C.POINTER(PointDesc), C.POINTER(TraceView), C.POINTER(PointSummary),
+                                       C.POINTER(RequestRecord), C.POINTER(EventRecord), C.c_int64,
+                                       C.POINTER(C.c_int64), C.POINTER(InstanceRecord), C.c_int]
         L.kvo_run_sweep.argtypes = [C.POINTER(PointDesc), C.c_int64, C.c_int, C.POINTER(PointSummary)]
         for fn in ("kvo_prefill_latency", "kvo_decode_step_latency"):
             getattr(L, fn).restype = C.c_double
@@ -70,39 +73,45 @@ def emu():
         L = C.CDLL(EMU_SO)
         L.kvemu_run.argtypes = [C.POINTER(PointDesc), C.c_int64, C.POINTER(TraceView), C.c_int64,
                                 C.POINTER(PointSummary), C.POINTER(RequestRecord), C.POINTER(EventRecord),
-                                C.c_int64, C.POINTER(C.c_int64), C.c_int]
+                                C.c_int64, C.POINTER(C.c_int64), C.c_int, C.POINTER(InstanceRecord), C.c_int]
         _emu = L
     return _emu
 
 
 class Result:
-    def __init__(self, summary, recs, events, status=0, ev_total=None):
+    def __init__(self, summary, recs, events, status=0, ev_total=None, inst=None):
         self.summary = summary
         self.recs = recs
         self.events = events
         self.status = status
+        self.inst = inst
         # total events produced (may exceed the captured log)
         self.ev_total = ev_total if ev_total is not None else (len(events) if events is not None else None)
 
 
-def run_oracle(p: PointDesc, trace: TraceView | None = None, ev_cap: int = 0, recs: bool = True) -> Result:
+def run_oracle(p: PointDesc, trace: TraceView | None = None, ev_cap: int = 0, recs: bool = True,
+               detail: bool = False, inst: bool = True) -> Result:
     L = oracle()
     s = PointSummary()
     nrec = max(int(p.num_requests), 0)
     R = (RequestRecord * max(nrec, 1))() if recs else None
     E = (EventRecord * max(ev_cap, 1))() if ev_cap else None
+    I = (InstanceRecord * 32)() if inst else None
     cnt = C.c_int64(0)
-    st = L.kvo_run_point(C.byref(p), C.byref(trace) if trace is not None else None, C.byref(s), R, E, ev_cap,
-                         C.byref(cnt))
+    st = L.kvo_run_point_ex(C.byref(p), C.byref(trace) if trace is not None else None, C.byref(s), R, E, ev_cap,
+                            C.byref(cnt), I, 1 if detail else 0)
     n = s.n_requests
-    return Result(s, R[:n] if recs else None, E[:min(cnt.value, ev_cap)] if ev_cap else None, st, cnt.value)
+    return Result(s, R[:n] if recs else None, E[:min(cnt.value, ev_cap)] if ev_cap else None, st, cnt.value,
+                  list(I[:max(p.num_instances, 0)]) if inst and st == 0 else None)
 
 
-def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warps: int = 2):
+def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warps: int = 2, detail: bool = False,
+                   inst: bool = True):
     L = emu()
     n = len(points)
     P = (PointDesc * n)(*points)
     S = (PointSummary * n)()
+    I = (InstanceRecord * (32 * n))() if inst else None
     tot = sum(max(int(p.num_requests), 0) for p in points)
     R = (RequestRecord * max(tot, 1))() if recs else None
     E = (EventRecord * max(ev_cap * n, 1))() if ev_cap else None
@@ -112,7 +121,7 @@ def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warp
     if traces:
         nt = len(traces)
         T = (TraceView * nt)(*traces)
-    L.kvemu_run(P, n, T, nt, S, R, E, ev_cap, cnt, warps)
+    L.kvemu_run(P, n, T, nt, S, R, E, ev_cap, cnt, warps, I, 1 if detail else 0)
     out = []
     off = 0
     for i, p in enumerate(points):
@@ -121,7 +130,8 @@ def run_points_emu(points, traces=None, ev_cap: int = 0, recs: bool = True, warp
         rr = R[off:off + s.n_requests] if recs else None
         off += nr
         ee = E[i * ev_cap:i * ev_cap + min(cnt[i], ev_cap)] if ev_cap else None
-        out.append(Result(s, rr, ee, s.status, cnt[i]))
+        ii = list(I[32 * i:32 * i + p.num_instances]) if inst and s.status == 0 else None
+        out.append(Result(s, rr, ee, s.status, cnt[i], ii))
     return out
 
 
@@ -165,6 +175,13 @@ def diff_results(a: Result, b: Result, *, events: bool = True) -> list[str]:
                     break
             if len(errs) > 20:
                 break
+    if a.inst is not None and b.inst is not None:
+        for i, (ra, rb) in enumerate(zip(a.inst, b.inst)):
+            for f, _ in InstanceRecord._fields_:
+                va, vb = getattr(ra, f), getattr(rb, f)
+                ok = feq(va, vb) if isinstance(va, float) else va == vb
+                if not ok:
+                    errs.append(f"inst[{i}].{f}: {va!r} != {vb!r}")
     if events and a.events is not None and b.events is not None:
         if a.ev_total != b.ev_total:
             errs.append(f"event totals: {a.ev_total} != {b.ev_total}")

@@ -57,3 +57,23 @@ def test_accellm_extensions_random(chunk):
 def test_accellm_extensions_long():
     from configs import ext_long_points
     check(ext_long_points(n=400), ev=1 << 20)
+
+
+@pytest.mark.parametrize("chunk", range(2))
+def test_detail_metrics_random(chunk):
+    """Detail runs (pooled TBT p50/p95 from per-step (gap, count) entries,
+    plain event loop): kernel core == oracle bit for bit, including the
+    per-instance records and the new v2 summary fields."""
+    import math
+    pts = [random_small(i) for i in range(chunk * 25, chunk * 25 + 25)]
+    pts += [config1(seed=chunk, n=120), config2("accellm", 6.0, n=60), config2("unified", 6.0, n=60)]
+    got = run_points_emu(pts, ev_cap=EV, warps=4, detail=True)
+    bad = []
+    for p, g in zip(pts, got):
+        ref = run_oracle(p, ev_cap=EV, detail=True)
+        d = diff_results(ref, g)
+        if d:
+            bad.append((p.policy, p.num_instances, p.num_requests, d[:4]))
+        if g.status == 0 and g.summary.n_tbt_samples > 0:
+            assert not math.isnan(g.summary.tbt_p50) and g.summary.tbt_p50 <= g.summary.tbt_p95 <= g.summary.tbt_max
+    assert not bad, bad

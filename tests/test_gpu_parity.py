@@ -24,13 +24,15 @@ def sim():
     s.close()
 
 
-def check(sim, points, ev=EV, records=True):
-    summ, recs, evs = sim.run(points, records=records, events=ev)
+def check(sim, points, ev=EV, records=True, detail=False):
+    summ, recs, evs = sim.run(points, records=records, events=ev, detail=detail, instances=True)
     cnts = sim.last_event_counts
+    inst = sim.last_instances
     bad = []
     for i, p in enumerate(points):
-        ref = run_oracle(p, ev_cap=ev, recs=records)
-        d = diff_results(ref, Result(summ[i], recs[i], evs[i], ev_total=cnts[i]))
+        ref = run_oracle(p, ev_cap=ev, recs=records, detail=detail)
+        d = diff_results(ref, Result(summ[i], recs[i], evs[i], ev_total=cnts[i],
+                                     inst=inst[i] if summ[i].status == 0 else None))
         if d:
             bad.append((i, p.policy, p.num_requests, d[:4]))
     assert not bad, bad
@@ -166,3 +168,58 @@ def test_extensions_mixed_with_plain_points(sim):
         pts.append(random_ext(300 + i))
         pts.append(random_small(700 + i, max_req=120))
     check(sim, pts, ev=1 << 17)
+
+
+def test_detail_metrics(sim):
+    """Detail runs (kvsim_run_opts.detail): pooled TBT p50/p95 from the
+    per-step (gap, count) entries, plain event loop; bit-exact vs the oracle,
+    with per-instance records and event logs."""
+    pts = [random_small(2000 + i, max_req=150) for i in range(60)]
+    pts += [config1(seed=3, n=1000)]
+    pts += [config2(pol, 12.0, seed=1, n=1500) for pol in ("accellm", "splitwise", "unified")]
+    summ = check(sim, pts, ev=1 << 19, detail=True)
+    for s in summ:
+        if s.status == 0 and s.n_tbt_samples > 0:
+            assert s.tbt_p50 <= s.tbt_p95 <= s.tbt_max
+
+
+def _full_size(sim, pts):
+    """Summaries + per-request records bitwise (chained sweep kernel), then
+    the same points in a detail run (plain event loop, TBT percentiles)."""
+    summ, recs, _ = sim.run(pts, records=True)
+    det = sim.run(pts, detail=True, instances=True)
+    inst = sim.last_instances
+    bad = []
+    for i, p in enumerate(pts):
+        ref = run_oracle(p, ev_cap=0, recs=True, detail=True)
+        d = diff_results(ref, Result(summ[i], recs[i], None), events=False)
+        # the sweep run leaves tbt_p50/p95 NaN; compare those on the detail run
+        d = [x for x in d if not x.startswith(("summary.tbt_p50", "summary.tbt_p95"))]
+        d += diff_results(ref, Result(det[i], None, None, inst=inst[i]), events=False)
+        if d:
+            bad.append((i, p.policy, p.rate, p.seed, d[:4]))
+    assert not bad, bad
+    return summ
+
+
+def test_config2_full_size(sim):
+    """BASELINE config 2 at SURVEY §8(d)'s size: 10k requests, 3 policies x
+    rates {6, 12, 18} x seeds 0-2."""
+    pts = [config2(pol, rate, seed=sd, n=10000) for pol in ("accellm", "splitwise", "unified")
+           for rate in (6.0, 12.0, 18.0) for sd in (0, 1, 2)]
+    _full_size(sim, pts)
+
+
+def test_config3_full_size(sim):
+    """BASELINE config 3 at 10k requests: 3 policies x rates {1, 2, 3} x seeds 0-2."""
+    pts = [config3(pol, rate, seed=sd, n=10000) for pol in ("accellm", "splitwise", "unified")
+           for rate in (1.0, 2.0, 3.0) for sd in (0, 1, 2)]
+    _full_size(sim, pts)
+
+
+def test_config2_config3_event_logs_10k(sim):
+    """Full decision/event logs at 10k requests (seed 0, one rate per config)."""
+    pts = [config2(pol, 12.0, seed=0, n=10000) for pol in ("accellm", "splitwise", "unified")]
+    pts += [config3(pol, 2.0, seed=0, n=10000) for pol in ("accellm", "splitwise", "unified")]
+    for p in pts:
+        check(sim, [p], ev=1 << 23)
