@@ -139,7 +139,8 @@ typedef struct kvsim_point_summary {
   double tbt_p50, tbt_p95;      /* nearest rank over the pooled TBT samples of measured requests;
                                    detail runs only (kvsim_run_opts.detail), NaN otherwise */
   double idle_runnable_s;       /* sum over instances of time in the window with no job in
-                                   flight while >= 1 request is live anywhere */
+                                   flight while >= 1 request waits in a prefill queue, i.e.
+                                   runnable work exists that nobody runs */
   double queue_depth_avg;       /* time average over [0, makespan] of the requests waiting in
                                    prefill queues (SPEC.md:358 queue-depth series) */
   int64_t queue_depth_max;

@@ -192,9 +192,8 @@ struct Sim {
   int64_t n_events = 0, n_steps = 0, n_prefills = 0, n_moves = 0, n_preempt = 0, n_evict = 0;
   int64_t tokens_total = 0, tokens_window = 0, prefill_tokens = 0, mirror_tokens = 0;
   double now = 0;
-  // live requests (arrived, not complete) and Z(t) = time in [warmup, t] with
-  // none live; queue depth (requests waiting in prefill queues) series stats
-  int64_t live = 0;
+  // queue depth (requests waiting in prefill queues) and Z(t) = time in
+  // [warmup, t] with none waiting (idle-while-runnable, SEMANTICS §7)
   double zero_since = 0, z_acc = 0;
   int64_t qdepth = 0, qd_max = 0;
   double qd_area = 0, qd_tprev = 0;
@@ -269,7 +268,9 @@ struct Sim {
   void qd_change(int64_t delta) {
     qd_area = qd_area + (double)qdepth * (now - qd_tprev);
     qd_tprev = now;
+    if (qdepth == 0 && delta > 0) z_acc = z_acc + (clip(now) - clip(zero_since));
     qdepth += delta;
+    if (qdepth == 0) zero_since = now;
     if (qdepth > qd_max) qd_max = qdepth;
   }
   void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; qd_change(1); }
@@ -282,12 +283,7 @@ struct Sim {
   // ---- idle while runnable
   double clip(double t) const { return t > P.warmup_s ? t : P.warmup_s; }
   // Z(t): measure of [warmup, t] with no live request (t >= every change so far)
-  double zeta(double t) const { return live == 0 ? z_acc + (clip(t) - clip(zero_since)) : z_acc; }
-  void live_add(int64_t k, double t) {
-    if (live == 0 && k > 0) z_acc = z_acc + (clip(t) - clip(zero_since));
-    live += k;
-    if (live == 0) zero_since = t;
-  }
+  double zeta(double t) const { return qdepth == 0 ? z_acc + (clip(t) - clip(zero_since)) : z_acc; }
   // a job starts on x at t: close x's idle period
   void job_begin(Inst& X, double t) {
     const double a = clip(t) - clip(X.idle_t);
@@ -312,7 +308,7 @@ struct Sim {
     ++tokens_total;
     if (t >= P.warmup_s) ++tokens_window;
   }
-  void finish_req(Req& r, double t) { r.done = true; r.done_t = t; live_add(-1, t); }
+  void finish_req(Req& r, double t) { r.done = true; r.done_t = t; }
 
   // a job ends on x at t: busy time, and x's idle period (if any) starts here
   void account_job(Inst& x, double t) {
@@ -1115,7 +1111,6 @@ struct Sim {
       switch (bk) {
         case 0:
           ++next_arrival;
-          live_add(1, t);
           arrive(bid, t);
           break;
         case 1:
@@ -1393,6 +1388,24 @@ int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace, k
 int kvo_run_point(const kvsim_point_desc* p, const kvsim_trace_view* trace, kvsim_point_summary* out,
                   kvsim_request_record* recs, kvsim_event_record* ev, int64_t ev_cap, int64_t* ev_count) {
   return kvo_run_point_ex(p, trace, out, recs, ev, ev_cap, ev_count, nullptr, 0);
+}
+
+int kvo_run_sweep_ex(const kvsim_point_desc* pts, int64_t n, int threads, kvsim_point_summary* out,
+                     kvsim_instance_record* inst, int detail) {
+  if (threads < 1) threads = 1;
+  std::atomic<int64_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      kvo_run_point_ex(&pts[i], nullptr, &out[i], nullptr, nullptr, 0, nullptr,
+                       inst ? inst + i * KVSIM_MAX_INSTANCES : nullptr, detail);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int k = 0; k < threads; ++k) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  return KVSIM_OK;
 }
 
 int kvo_run_sweep(const kvsim_point_desc* pts, int64_t n, int threads, kvsim_point_summary* out) {

@@ -56,6 +56,11 @@ int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace,
 int kvo_run_sweep(const kvsim_point_desc* pts, int64_t n, int threads,
                   kvsim_point_summary* out);
 
+/* v2: sweep with per-instance records (point i at i * KVSIM_MAX_INSTANCES,
+ * nullable) and detail metrics */
+int kvo_run_sweep_ex(const kvsim_point_desc* pts, int64_t n, int threads,
+                     kvsim_point_summary* out, kvsim_instance_record* inst, int detail);
+
 #ifdef __cplusplus
 }
 #endif

@@ -171,10 +171,10 @@ struct Sim {
   int32_t G_mode, G_cnt;
   int64_t tick;
   // idle while runnable: this lane's instance has been idle
-  // since L_idle_t, when the zero-live measure was L_idle_z
+  // since L_idle_t, when the zero-queue measure was L_idle_z
   double L_idle_t, L_idle_z, L_idle_rb;
-  // uniform: live requests, zero-live measure Z (since the warm-up), queue depth
-  int64_t live, qdepth, qd_max;
+  // uniform: queue depth (waiting requests) and its zero measure Z since the warm-up
+  int64_t qdepth, qd_max;
   double zero_since, z_acc, qd_area, qd_tprev;
 
   // per-slot arena offsets, computed once (the accessors below run on every
@@ -294,10 +294,13 @@ struct Sim {
 
   // ------------------------------------------------------------- queues
   // queue depth series: area += depth * (now - previous change)
+  // (also the zero-queue measure Z used by idle_runnable, SEMANTICS §7)
   KV_DEV void qd_change(int64_t delta) {
     qd_area = kadd(qd_area, kmul((double)qdepth, ksub(now, qd_tprev)));
     qd_tprev = now;
+    if (qdepth == 0 && delta > 0) z_acc = kadd(z_acc, ksub(clip(now), clip(zero_since)));
     qdepth += delta;
+    if (qdepth == 0) zero_since = now;
     if (qdepth > qd_max) qd_max = qdepth;
   }
   KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
@@ -410,7 +413,7 @@ struct Sim {
     G_mode = G_cnt = 0;
     tick = 1;
     L_idle_t = L_idle_z = L_idle_rb = 0.0;
-    live = qdepth = qd_max = 0;
+    qdepth = qd_max = 0;
     zero_since = z_acc = qd_area = qd_tprev = 0.0;
     // directed links (splitwise; AcceLLM EXT)
     if (policy == KVSIM_POLICY_SPLITWISE || EXT)
@@ -489,14 +492,8 @@ struct Sim {
   }
   // ---- idle while runnable (SEMANTICS §7)
   KV_DEV double clip(double t) const { return t > PC.warmup ? t : PC.warmup; }
-  // Z(t): measure of [warm-up, t] with no live request
-  KV_DEV double zeta(double t) const { return live == 0 ? kadd(z_acc, ksub(clip(t), clip(zero_since))) : z_acc; }
-  // uniform: k requests arrive (k > 0) or complete (k < 0) at t
-  KV_DEV void live_add(int64_t k, double t) {
-    if (live == 0 && k > 0) z_acc = kadd(z_acc, ksub(clip(t), clip(zero_since)));
-    live += k;
-    if (live == 0) zero_since = t;
-  }
+  // Z(t): measure of [warm-up, t] with no request waiting in a prefill queue
+  KV_DEV double zeta(double t) const { return qdepth == 0 ? kadd(z_acc, ksub(clip(t), clip(zero_since))) : z_acc; }
   // a job starts on x at t: close x's idle period
   KV_DEV void job_begin(int x, double t) {
     const double z = zeta(t);
@@ -930,7 +927,6 @@ struct Sim {
       L_final -= o.kv_done + o.completed;
     }
     count_tokens(o.nb_old, t);
-    if (o.completed) live_add(-(int64_t)o.completed, t);
     if (policy == KVSIM_POLICY_ACCELLM) {
       const int y = partner_of(x);
       if (own(y)) { L_used -= o.copy_free; L_copy_tok -= o.copy_free; }
@@ -1371,7 +1367,6 @@ struct Sim {
     minrem = simt::warp_min_i32(minrem);
     simt::sync();
     count_tokens(k, t);
-    if (completed) live_add(-(int64_t)completed, t);
     if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
@@ -1475,7 +1470,6 @@ struct Sim {
     }
     simt::sync();
     count_tokens(k, t);
-    if (completed) live_add(-(int64_t)completed, t);
     log(KVSIM_EV_PREFILL_DONE, p, k, completed, 0);
     // one transfer per destination, ascending id; lane d keeps the finish time
     double fin_mine = 0.0;
@@ -1859,7 +1853,6 @@ struct Sim {
     simt::sync();
     if (own(x)) L_used -= kvfree;
     count_tokens(k, t);
-    if (completed) live_add(-(int64_t)completed, t);
     log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
     if constexpr (EXT) {
       if (is_dual(x)) {
@@ -2347,7 +2340,6 @@ struct Sim {
   // -------------------------------------------------------------- arrival
   KV_DEV_NOINLINE void arrive(double t) {
     EMU_COUNT(16);
-    live_add(1, t);
     const int64_t rid64 = next_rid;
     const int32_t rid = (int32_t)rid64;
     int32_t pl, dl;

@@ -45,6 +45,8 @@ def oracle():
                                        C.POINTER(RequestRecord), C.POINTER(EventRecord), C.c_int64,
                                        C.POINTER(C.c_int64), C.POINTER(InstanceRecord), C.c_int]
         L.kvo_run_sweep.argtypes = [C.POINTER(PointDesc), C.c_int64, C.c_int, C.POINTER(PointSummary)]
+        L.kvo_run_sweep_ex.argtypes = [C.POINTER(PointDesc), C.c_int64, C.c_int, C.POINTER(PointSummary),
+                                       C.POINTER(InstanceRecord), C.c_int]
         for fn in ("kvo_prefill_latency", "kvo_decode_step_latency"):
             getattr(L, fn).restype = C.c_double
             getattr(L, fn).argtypes = [C.POINTER(PointDesc), C.c_int64, C.c_int64]
@@ -195,3 +197,16 @@ def diff_results(a: Result, b: Result, *, events: bool = True) -> list[str]:
             first = sorted((sa ^ sb))[:5]
             errs.append(f"events differ: {len(ka)} vs {len(kb)}; first diffs {first}")
     return errs
+
+
+def oracle_sweep(points, detail=False, instances=True, threads=None):
+    """All points on the oracle, one per host thread; (summaries, instance
+    records per point or None)."""
+    L = oracle()
+    n = len(points)
+    P = (PointDesc * n)(*points)
+    S = (PointSummary * n)()
+    I = (InstanceRecord * (32 * n))() if instances else None
+    L.kvo_run_sweep_ex(P, n, threads or (os.cpu_count() or 1), S, I, 1 if detail else 0)
+    inst = [list(I[32 * i:32 * i + points[i].num_instances]) for i in range(n)] if instances else None
+    return list(S), inst
