@@ -223,3 +223,25 @@ def test_config2_config3_event_logs_10k(sim):
     pts += [config3(pol, 2.0, seed=0, n=10000) for pol in ("accellm", "splitwise", "unified")]
     for p in pts:
         check(sim, [p], ev=1 << 23)
+
+
+def test_rebalance_exhaustive_gpu(sim):
+    """rebalance_pair through the kernel (real MOVE events) vs exhaustive
+    search and bit-for-bit vs the oracle's event log."""
+    import random as _r
+    from paper_2411_05555_b200 import trace_view
+    from rebalance_case import case, exhaustive_best, first_rebalance, objectives
+    rng = _r.Random(7)
+    cases = [[1000, 1000, 100, 100]] + [[rng.randint(20, 1500) for _ in range(rng.randint(1, 4))]
+                                        for _ in range(30)]
+    for prompts in cases:
+        p, (arr, pl, dl) = case(prompts)
+        tv = trace_view(arr, pl, dl)
+        summ, recs, evs = sim.run([p], traces=[tv], records=True, events=1 << 16)
+        ref = run_oracle(p, trace=tv, ev_cap=1 << 16)
+        assert not diff_results(ref, Result(summ[0], recs[0], evs[0], ev_total=sim.last_event_counts[0]))
+        a, b = first_rebalance(evs[0], prompts)
+        before, after = objectives(prompts, []), objectives(a, b)
+        assert after[0] <= before[0] and after[1] <= before[1]
+        if prompts == [1000, 1000, 100, 100]:
+            assert after == exhaustive_best(prompts) == (0, 0)
