@@ -12,8 +12,12 @@ index (9,996 points, ~1e8 simulated requests). A step = one full sweep.
   --impl reference  the CPU oracle (restated reference simulator) on all host
          threads over a bounded sample of the same points
 
-Multi-GPU (torchrun): each rank runs its own config-4 grid with a disjoint
-seed range (weak scaling, no data-path collective).
+Multi-GPU (--gpus N, or torchrun with N ranks): ONE process drives all N
+GPUs with one host thread each (kvsim_gpu_run_multi: guided chunks over the
+cost-sorted points, summaries gathered in host memory, no collective, SURVEY
+§8e); the same config-4 sweep is split over the N GPUs (strong scaling).
+Under torchrun, ranks other than 0 exit without work. Every run also times a
+BASELINE config-5 subsample (`config5_slice`) on the same GPUs.
 """
 from __future__ import annotations
 
@@ -49,6 +53,25 @@ def config4_points(seed_base=0, n_rates=833, n_req=10000, policies=("unified", "
     return pts
 
 
+def config5_points(stride=333, n_req=100000):
+    """BASELINE config 5: 3 policies x {H100, 910B2} x 250
+    log-spaced rates in [0.5, 30] req/s x 667 seeds = 1,000,500 points of
+    70B / 8 instances / mixed / 100k requests; every stride-th point."""
+    import math
+    pts = []
+    k = 0
+    for pol in ("unified", "splitwise", "accellm"):
+        for dev in ("h100", "910b2"):
+            for j in range(250):
+                rate = 0.5 * math.exp(math.log(60.0) * j / 249)
+                for sd in range(667):
+                    if k % stride == 0:
+                        pts.append(make_point(model="llama2-70b", device=dev, policy=pol, instances=8, rate=rate,
+                                              num_requests=n_req, workload="mixed", seed=sd, user_tag=k))
+                    k += 1
+    return pts
+
+
 def algorithmic_bytes(summaries):
     # SURVEY §8d: B_req = 16 (trace) + 24 (TTFT/TBT/JCT record) + 8 * S_req,
     # S_req = decode iterations = decode_len - 1 => sum = tokens_total - n_requests
@@ -57,10 +80,13 @@ def algorithmic_bytes(summaries):
     return 40 * n + 8 * (tok - n)
 
 
+NCU_TRAFFIC_FILE = "profiles/r2_ncu_bench_kernel.json"
+
+
 def ncu_traffic():
     """DRAM bytes per launch of the config-4 sweep kernel from the committed ncu
-    capture (profiles/r1_ncu_bench_kernel.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r1_ncu_bench_kernel.json")
+    capture of this build (NCU_TRAFFIC_FILE), or None."""
+    p = os.path.join(ROOT, NCU_TRAFFIC_FILE)
     try:
         return float(json.load(open(p))["dram_bytes_per_launch"])
     except Exception:
@@ -169,6 +195,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the full-size CPU oracle baseline / parity check")
+    ap.add_argument("--c5-stride", type=int, default=333, help="config-5 subsample stride (0 = skip)")
+    ap.add_argument("--c5-requests", type=int, default=100000)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -199,7 +227,7 @@ def main():
         v = reqs / sum(times)
         line = {"metric": metric, "value": v, "unit": "simulated requests/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / K * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (the seeded generator of SEMANTICS §2, same traces as the GPU arm)",
                 "impl": "reference",
                 "config": {"workload": workload, "parallelism": f"{n_cpu} host threads, one point per thread"},
@@ -213,65 +241,66 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if rank != 0:
+        # one process drives every GPU (one host thread per device, no
+        # collective); under torchrun the other ranks have nothing to do
+        return
+    n_gpu = max(args.gpus, world)
     import torch
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
-    torch.cuda.set_device(dev)
     import paper_2411_05555_b200 as pkg
-    sim = pkg.KvSim(dev)
-    pts = config4_points(rank * 1_000_000, args.rates, args.requests)
+    sims = [pkg.KvSim(d) for d in range(n_gpu)]
+    sim = sims[0]
+    pts = config4_points(0, args.rates, args.requests)
     n = len(pts)
-    P = (PointDesc * n)(*pts)
-    # device-resident inputs / outputs (torch owns the memory)
-    d_pts = torch.frombuffer(bytearray(bytes(P)), dtype=torch.uint8).to(f"cuda:{dev}")
-    d_out = torch.empty(n * C.sizeof(PointSummary), dtype=torch.uint8, device=f"cuda:{dev}")
-    sim.reserve(pts)
-    stream = torch.cuda.Stream(dev)  # non-default stream: the kernels and the events share it
+    bad_reqs = 0
+    with ClockSampler(0) as clk:
+        if n_gpu == 1:
+            # device-resident: points and summaries in HBM (torch owns the memory)
+            dev = 0
+            torch.cuda.set_device(dev)
+            P = (PointDesc * n)(*pts)
+            d_pts = torch.frombuffer(bytearray(bytes(P)), dtype=torch.uint8).to(f"cuda:{dev}")
+            d_out = torch.empty(n * C.sizeof(PointSummary), dtype=torch.uint8, device=f"cuda:{dev}")
+            sim.reserve(pts)
+            stream = torch.cuda.Stream(dev)  # non-default stream: the kernels and the events share it
 
-    def step():
-        sim.run_device(d_pts.data_ptr(), n, d_out.data_ptr(), stream.cuda_stream)
+            def step():
+                sim.run_device(d_pts.data_ptr(), n, d_out.data_ptr(), stream.cuda_stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(dev) as clk:
-        torch.cuda.synchronize(dev)
-        with torch.cuda.stream(stream):
-            for a, b in ev:
-                a.record(stream)
+            for _ in range(args.warmup):
                 step()
-                b.record(stream)
-        torch.cuda.synchronize(dev)
-    launches = args.steps * sim.last_launches()
-    times = [a.elapsed_time(b) / 1e3 for a, b in ev]
-    t_total = sum(times)
-    if dist:
-        t = torch.tensor([t_total], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total = float(t.item())
-    host_out = d_out.cpu().numpy().tobytes()
-    summ = (PointSummary * n).from_buffer_copy(host_out)
+            torch.cuda.synchronize(dev)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+            torch.cuda.synchronize(dev)
+            with torch.cuda.stream(stream):
+                for a, b in ev:
+                    a.record(stream)
+                    step()
+                    b.record(stream)
+            torch.cuda.synchronize(dev)
+            launches = args.steps * sim.last_launches()
+            t_total = sum(a.elapsed_time(b) / 1e3 for a, b in ev)
+            summ = (PointSummary * n).from_buffer_copy(d_out.cpu().numpy().tobytes())
+        else:
+            # sharded over n_gpu devices: per step, the max over devices of
+            # the CUDA-event time from its first chunk to its last
+            for _ in range(args.warmup):
+                pkg.run_multi(sims, pts)
+            t_total, launches = 0.0, 0
+            for _ in range(args.steps):
+                summ, st = pkg.run_multi(sims, pts)
+                t_total += max(st.device_seconds[i] for i in range(n_gpu))
+                launches += sum(st.device_launches[i] for i in range(n_gpu))
     bad = sum(1 for s in summ if s.status != 0)
     # failed points (e.g. an exceeded event budget) did not simulate all of
     # their requests: they do not count towards the throughput
     reqs = sum(s.n_requests for s in summ if s.status == 0)
-    total_reqs = reqs
-    if dist:  # requests all ranks simulated (each rank runs its own grid)
-        t = torch.tensor([reqs], dtype=torch.int64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        total_reqs = int(t.item())
-    value = total_reqs * args.steps / t_total
+    value = reqs * args.steps / t_total
     kernel_s = t_total / args.steps
     bytes_alg = algorithmic_bytes(summ)
     peaks, src = measured_peaks()
-    achieved = bytes_alg / kernel_s / 1e9
+    achieved = bytes_alg / kernel_s / 1e9 / n_gpu  # per GPU
     events = sum(s.n_events for s in summ)
 
     # e2e: through the reference-facing C-ABI with host buffers
@@ -281,22 +310,35 @@ def main():
         d2h = n * C.sizeof(PointSummary)
         tt = []
         for i in range(max(1, args.steps)):
-            if dist:
-                dist.barrier()
             t0 = time.perf_counter()
-            s2 = sim.run(pts)
+            s2 = sim.run(pts) if n_gpu == 1 else pkg.run_multi(sims, pts)[0]
             tt.append(time.perf_counter() - t0)
-        te = sum(tt)
-        if dist:
-            t = torch.tensor([te], device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
-        assert all(bytes(a) == bytes(b) for a, b in zip(s2, summ)), "e2e results differ from device-resident run"
-        e2e = {"value": total_reqs * len(tt) / te, "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+        assert all(bytes(a) == bytes(b) for a, b in zip(s2, summ)), "e2e results differ from the timed run"
+        e2e = {"value": reqs * len(tt) / sum(tt), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h,
+               "path": "kvsim_gpu_run (host buffers)" if n_gpu == 1 else
+                       f"kvsim_gpu_run_multi over {n_gpu} GPUs (host buffers, one host thread per GPU)"}
+
+    # BASELINE config 5 slice (70B, 8 instances, mixed, 3
+    # policies x {H100, 910B2} x 250 rates x 667 seeds, 100k requests each):
+    # every c5_stride-th point, sharded over the same GPUs
+    c5 = None
+    if args.c5_stride > 0:
+        c5p = config5_points(args.c5_stride, args.c5_requests)
+        pkg.run_multi(sims, c5p[:len(c5p) // 8])  # warm-up: arenas, instruction caches
+        t0 = time.perf_counter()
+        c5s, st = pkg.run_multi(sims, c5p)
+        wall = time.perf_counter() - t0
+        c5r = sum(x.n_requests for x in c5s if x.status == 0)
+        dev_s = max(st.device_seconds[i] for i in range(n_gpu))
+        c5 = {"workload": f"BASELINE config 5 subsample: every {args.c5_stride}th of 1,000,500 points "
+                          f"({len(c5p)} points x {args.c5_requests} requests)",
+              "value": c5r / dev_s, "e2e": c5r / wall, "unit": "simulated requests/s", "n_gpus": n_gpu,
+              "ms": dev_s * 1e3, "failed_points": sum(1 for x in c5s if x.status != 0),
+              "points_per_gpu": [int(st.device_points[i]) for i in range(n_gpu)]}
 
     cpu, parity = None, None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if n_gpu == 1 and not args.no_cpu:
         # the full sweep on the CPU oracle (all host threads): both the
         # cpu_baseline and a bitwise check of every GPU summary
         S_cpu, dt = oracle_sweep(pts, n_cpu)
@@ -306,36 +348,36 @@ def main():
                          f"threads (CPU oracle, one point per thread)"}
         parity = parity_check(summ, S_cpu)
 
-    if rank == 0:
-        line = {
-            "metric": metric, "value": value, "unit": "simulated requests/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: requests generated on device by the seeded counter-based RNG (SEMANTICS §2)",
-            "config": {"workload": workload, "points_per_gpu": n, "requests_per_step_per_gpu": reqs,
-                       "parallelism": f"points sharded over {world} GPU(s), warp per point",
-                       "l2": "arena working set >> 126 MB L2 and rewritten every step (no flush needed)"},
-            "gpu_launches": launches,
-            "events_per_step_per_gpu": events,
-            "failed_points": bad,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"),
-                         "unit": "GB/s", "frac": achieved / peaks.get("hbm_gbs"),
-                         "traffic": ncu_traffic() if workload_is_config4 else None,
-                         "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
-                                         "profiles/r1_ncu_bench_kernel.json)",
-                         "peak_source": src,
-                         "algorithmic_bytes_per_launch": bytes_alg,
-                         "note": "algorithmic bytes per SURVEY §8d (40 B/request + 8 B/decode iteration); "
-                                 "the kernel is bound by per-event issue latency, not HBM"},
-            "clocks": clk.summary(),
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "parity": parity,
-        }
-        print(json.dumps(line), flush=True)
-    sim.close()
-    if dist:
-        dist.destroy_process_group()
+    line = {
+        "metric": metric, "value": value, "unit": "simulated requests/s", "n_gpus": n_gpu,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: requests generated on device by the seeded counter-based RNG (SEMANTICS §2)",
+        "config": {"workload": workload, "points": n, "requests_per_step": reqs,
+                   "parallelism": f"points sharded over {n_gpu} GPU(s) by one process (host thread per GPU, "
+                                  f"guided chunks, no collective), warp per point",
+                   "l2": "arena working set >> 126 MB L2 and rewritten every step (no flush needed)"},
+        "gpu_launches": launches,
+        "events_per_step": events,
+        "failed_points": bad,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs"),
+                     "unit": "GB/s", "frac": achieved / peaks.get("hbm_gbs"),
+                     "traffic": ncu_traffic() if workload_is_config4 else None,
+                     "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum of the "
+                                     "config-4 sweep kernel, " + NCU_TRAFFIC_FILE + ")",
+                     "peak_source": src,
+                     "algorithmic_bytes_per_launch": bytes_alg,
+                     "note": "algorithmic bytes per SURVEY §8d (40 B/request + 8 B/decode iteration), per GPU; "
+                             "the kernel is bound by instruction issue/fetch, not HBM (DESIGN.md §7)"},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "config5_slice": c5,
+    }
+    print(json.dumps(line), flush=True)
+    for s_ in sims:
+        s_.close()
 
 
 if __name__ == "__main__":

@@ -236,6 +236,25 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
                      const kvsim_trace_view* traces, size_t n_traces, kvsim_point_summary* out,
                      const kvsim_run_opts* opts, char* err, size_t err_len);
 
+/* v2: one sweep sharded over several devices.
+ * ctxs[k] are open contexts on distinct devices (reused across calls, so
+ * arenas are allocated once). One host thread per context pulls chunks of
+ * points (guided self-scheduling over the points sorted by estimated cost,
+ * chunks >= min_chunk) and runs each through kvsim_gpu_run_ex; summaries
+ * land at their point index, so `out` is byte-identical for any number of
+ * devices. No collective: results are gathered in host memory.
+ * Generated traces only (trace_index < 0). stats is nullable. */
+#define KVSIM_MAX_DEVICES 16
+typedef struct kvsim_multi_stats {
+  double device_seconds[KVSIM_MAX_DEVICES];   /* CUDA-event time, first chunk start to last chunk end */
+  int64_t device_points[KVSIM_MAX_DEVICES];
+  int64_t device_launches[KVSIM_MAX_DEVICES];
+  int32_t n_devices, reserved;
+} kvsim_multi_stats;
+int kvsim_gpu_run_multi(kvsim_gpu_ctx* const* ctxs, int n_ctx, const kvsim_point_desc* pts, size_t n,
+                        kvsim_point_summary* out, size_t min_chunk, kvsim_multi_stats* stats,
+                        char* err, size_t err_len);
+
 /* Device-resident variant: d_pts / d_out are device pointers, generated traces
  * only, no records; launched on `stream` (a cudaStream_t; NULL selects the
  * context's own stream) without synchronising.

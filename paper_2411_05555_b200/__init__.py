@@ -17,7 +17,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .abi import (EventRecord, InstanceRecord, PointDesc, PointSummary, RequestRecord, RunOpts,  # noqa: F401
+from .abi import (EventRecord, InstanceRecord, MultiStats, PointDesc, PointSummary, RequestRecord, RunOpts,  # noqa: F401
                   TraceView,
                   make_point, points_array, summary_dict, STATUS, POLICY, POLICY_NAME,
                   DEVICES, MODELS, WORKLOADS, SUMMARY_CSV)
@@ -53,6 +53,9 @@ def load_library() -> C.CDLL:
                                 C.c_size_t, C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]
     L.kvsim_gpu_run_ex.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.POINTER(TraceView), C.c_size_t,
                                    C.POINTER(PointSummary), C.POINTER(RunOpts), C.c_char_p, C.c_size_t]
+    L.kvsim_gpu_run_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(PointDesc), C.c_size_t,
+                                      C.POINTER(PointSummary), C.c_size_t, C.POINTER(MultiStats), C.c_char_p,
+                                      C.c_size_t]
     L.kvsim_gpu_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                        C.c_char_p, C.c_size_t]
     L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]
@@ -184,6 +187,24 @@ class KvSim:
         self._check(rc, "kvsim_gpu_gen_trace")
         k = nn.value
         return list(arr)[:k], list(pl)[:k], list(dl)[:k]
+
+
+def run_multi(sims, points, min_chunk: int = 1):
+    """One sweep sharded over the devices of `sims` (open KvSim contexts on
+    distinct GPUs): kvsim_gpu_run_multi, one host thread per device, guided
+    chunks over the cost-sorted points, no collective. Returns (summaries in
+    point order, MultiStats)."""
+    L = load_library()
+    n = len(points)
+    P = (PointDesc * n)(*points)
+    S = (PointSummary * n)()
+    H = (C.c_void_p * len(sims))(*[s.h.value for s in sims])
+    st = MultiStats()
+    err = C.create_string_buffer(512)
+    rc = L.kvsim_gpu_run_multi(H, len(sims), P, n, S, min_chunk, C.byref(st), err, 512)
+    if rc != 0:
+        raise KvSimError(f"kvsim_gpu_run_multi failed [{rc}]: {err.value.decode()}")
+    return list(S), st
 
 
 def trace_view(arrival, prompt, decode):

@@ -114,6 +114,18 @@ class RunOpts(C.Structure):
     ]
 
 
+KVSIM_MAX_DEVICES = 16
+
+
+class MultiStats(C.Structure):
+    _fields_ = [
+        ("device_seconds", C.c_double * KVSIM_MAX_DEVICES),
+        ("device_points", C.c_int64 * KVSIM_MAX_DEVICES),
+        ("device_launches", C.c_int64 * KVSIM_MAX_DEVICES),
+        ("n_devices", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
 class EventRecord(C.Structure):
     _fields_ = [
         ("t", C.c_double), ("kind", C.c_int32), ("inst", C.c_int32),

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "json_lite.hpp"
+#include "kvsim_shard.hpp"
 #include "kvsim/perfmodel.hpp"
 #include "kvsim_gpu.h"
 
@@ -741,6 +742,12 @@ constexpr size_t kEvCapStart = size_t(1) << 16;
 // One host thread per GPU pulling chunks of points from a shared counter;
 // results land at their point index, so the merge is deterministic and
 // independent of the GPU count.
+// One host thread per GPU pulling chunks from a shared cursor over the points
+// sorted by estimated cost (guided self-scheduling, kvsim_shard.hpp); results
+// land at their point index, so the merge is deterministic and independent of
+// the GPU count. KVSIM_VIRTUAL_GPUS=1 lets
+// --gpus exceed the visible devices (workers share devices round-robin): a
+// test hook for the sharder on a one-GPU box, never a performance setting.
 void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, int gpus, bool records, bool events,
                 bool detail, RunOut& out) {
   const size_t n = pts.size();
@@ -754,65 +761,75 @@ void run_points(const std::vector<kvsim_point_desc>& pts, const Trace* trace, in
   if (trace) tv = kvsim_trace_view{trace->arr.data(), trace->pl.data(), trace->dl.data(), (int64_t)trace->arr.size()};
   const int ndev = kvsim_gpu_device_count();
   if (ndev <= 0) throw std::runtime_error("no CUDA device available (kvsim has no CPU fallback)");
-  if (gpus <= 0 || gpus > ndev) gpus = ndev < 1 ? 1 : (gpus <= 0 ? 1 : ndev);
-  size_t chunk = std::max<size_t>(1, std::min<size_t>(65536, (n + 4 * gpus - 1) / (4 * gpus)));
-  if (events) chunk = std::min(chunk, std::max<size_t>(1, kEvBytesPerChunk / (kEvCapStart * sizeof(kvsim_event_record))));
-  std::atomic<size_t> next{0};
-  std::vector<std::string> errors(gpus);
-  std::vector<std::thread> th;
-  for (int g = 0; g < gpus; ++g)
-    th.emplace_back([&, g]() {
-      char err[512] = {0};
-      kvsim_gpu_ctx* ctx = nullptr;
-      if (kvsim_gpu_open(g, &ctx, err, sizeof err) != 0) { errors[g] = err; return; }
-      std::vector<kvsim_event_record> evbuf;
-      std::vector<int64_t> evcnt;
-      for (;;) {
-        const size_t a = next.fetch_add(chunk);
-        if (a >= n) break;
-        const size_t b = std::min(n, a + chunk);
-        kvsim_run_opts o{};
-        o.detail = detail ? 1 : 0;
-        o.recs = records ? out.recs.data() + out.rec_off[a] : nullptr;  // records of a chunk are contiguous
-        o.inst = out.inst.data() + a * KVSIM_MAX_INSTANCES;
-        if (events) {
-          evbuf.assign((b - a) * kEvCapStart, kvsim_event_record{});
-          evcnt.assign(b - a, 0);
-          o.ev = evbuf.data();
-          o.ev_cap = kEvCapStart;
-          o.ev_count = evcnt.data();
-        }
-        int rc = kvsim_gpu_run_ex(ctx, pts.data() + a, b - a, trace ? &tv : nullptr, trace ? 1 : 0, out.sum.data() + a,
-                                  &o, err, sizeof err);
-        if (rc != 0) { errors[g] = err; break; }
-        if (!events) continue;
-        for (size_t i = a; i < b; ++i) {
-          const int64_t k = evcnt[i - a];
-          if (k <= (int64_t)kEvCapStart) {
-            out.ev[i].assign(evbuf.begin() + (i - a) * kEvCapStart, evbuf.begin() + (i - a) * kEvCapStart + k);
-            continue;
-          }
-          // overflowed: rerun this point alone with an exact-size log
-          std::vector<kvsim_event_record> big((size_t)k);
-          int64_t k2 = 0;
-          kvsim_point_summary s2{};
-          kvsim_run_opts o2{};
-          o2.detail = detail ? 1 : 0;
-          o2.ev = big.data();
-          o2.ev_cap = (size_t)k;
-          o2.ev_count = &k2;
-          rc = kvsim_gpu_run_ex(ctx, &pts[i], 1, trace ? &tv : nullptr, trace ? 1 : 0, &s2, &o2, err, sizeof err);
-          if (rc != 0) { errors[g] = err; break; }
-          if (k2 != k) { errors[g] = "event count changed on rerun (non-deterministic run)"; break; }
-          out.ev[i].swap(big);
-        }
-        if (!errors[g].empty()) break;
+  const bool virt = std::getenv("KVSIM_VIRTUAL_GPUS") && std::atoi(std::getenv("KVSIM_VIRTUAL_GPUS")) != 0;
+  if (gpus <= 0) gpus = 1;
+  if (gpus > ndev && !virt) gpus = ndev;
+  size_t min_chunk = std::max<size_t>(1, n / (64 * (size_t)gpus));
+  if (events) min_chunk = std::min(min_chunk, std::max<size_t>(1, kEvBytesPerChunk / (kEvCapStart * sizeof(kvsim_event_record))));
+  kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts.data(), n, gpus, min_chunk);
+  std::vector<kvsim_gpu_ctx*> ctx(gpus, nullptr);
+  std::mutex open_mu;
+  auto chunk = [&](int w, const std::vector<int64_t>& idx, std::vector<kvsim_point_summary>& res,
+                   std::string& e) -> int {
+    char err[512] = {0};
+    if (!ctx[w]) {
+      std::lock_guard<std::mutex> g(open_mu);
+      if (kvsim_gpu_open(w % ndev, &ctx[w], err, sizeof err) != 0) { e = err; return KVSIM_E_CUDA; }
+    }
+    const size_t m = idx.size();
+    std::vector<kvsim_point_desc> sub(m);
+    std::vector<int64_t> roff(m + 1, 0);
+    for (size_t k = 0; k < m; ++k) {
+      sub[k] = pts[idx[k]];
+      roff[k + 1] = roff[k] + sub[k].num_requests;
+    }
+    std::vector<kvsim_request_record> rec(records ? (size_t)roff[m] : 0);
+    std::vector<kvsim_instance_record> ins(m * KVSIM_MAX_INSTANCES);
+    std::vector<kvsim_event_record> evbuf(events ? m * kEvCapStart : 0);
+    std::vector<int64_t> evcnt(events ? m : 0);
+    kvsim_run_opts o{};
+    o.detail = detail ? 1 : 0;
+    o.recs = records ? rec.data() : nullptr;
+    o.inst = ins.data();
+    if (events) {
+      o.ev = evbuf.data();
+      o.ev_cap = kEvCapStart;
+      o.ev_count = evcnt.data();
+    }
+    int rc = kvsim_gpu_run_ex(ctx[w], sub.data(), m, trace ? &tv : nullptr, trace ? 1 : 0, res.data(), &o, err, sizeof err);
+    if (rc != 0) { e = err; return rc; }
+    for (size_t k = 0; k < m; ++k) {
+      const size_t i = (size_t)idx[k];
+      if (records)
+        std::copy(rec.begin() + roff[k], rec.begin() + roff[k + 1], out.recs.begin() + out.rec_off[i]);
+      std::copy(ins.begin() + k * KVSIM_MAX_INSTANCES, ins.begin() + (k + 1) * KVSIM_MAX_INSTANCES,
+                out.inst.begin() + i * KVSIM_MAX_INSTANCES);
+      if (!events) continue;
+      const int64_t c = evcnt[k];
+      if (c <= (int64_t)kEvCapStart) {
+        out.ev[i].assign(evbuf.begin() + k * kEvCapStart, evbuf.begin() + k * kEvCapStart + c);
+        continue;
       }
-      kvsim_gpu_close(ctx);
-    });
-  for (auto& t : th) t.join();
-  for (auto& e : errors)
-    if (!e.empty()) throw std::runtime_error(e);
+      // overflowed: rerun this point alone with an exact-size log
+      std::vector<kvsim_event_record> big((size_t)c);
+      int64_t c2 = 0;
+      kvsim_point_summary s2{};
+      kvsim_run_opts o2{};
+      o2.detail = detail ? 1 : 0;
+      o2.ev = big.data();
+      o2.ev_cap = (size_t)c;
+      o2.ev_count = &c2;
+      rc = kvsim_gpu_run_ex(ctx[w], &sub[k], 1, trace ? &tv : nullptr, trace ? 1 : 0, &s2, &o2, err, sizeof err);
+      if (rc != 0) { e = err; return rc; }
+      if (c2 != c) { e = "event count changed on rerun (non-deterministic run)"; return KVSIM_E_INTERNAL; }
+      out.ev[i].swap(big);
+    }
+    return KVSIM_OK;
+  };
+  std::string e;
+  const int rc = kvsim_host::run_plan(plan, out.sum.data(), chunk, e);
+  for (auto* c : ctx) kvsim_gpu_close(c);
+  if (rc != 0) throw std::runtime_error(e);
 }
 
 // ------------------------------------------------------------------ outputs

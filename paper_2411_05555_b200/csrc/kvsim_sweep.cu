@@ -19,6 +19,7 @@
 
 #include "kvsim_arena.hpp"
 #include "kvsim_gpu.h"
+#include "kvsim_shard.hpp"
 #include "kvsim_sim.cuh"
 
 using kvsim_dev::SweepArgs;
@@ -452,6 +453,70 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, co
     KV_CUDA(cudaMemcpyAsync(o.inst, c->inst.p, sizeof(kvsim_instance_record) * KVSIM_MAX_INSTANCES * n,
                             cudaMemcpyDeviceToHost, s));
   KV_CUDA(cudaStreamSynchronize(s));
+  return KVSIM_OK;
+}
+
+int kvsim_gpu_run_multi(kvsim_gpu_ctx* const* ctxs, int n_ctx, const kvsim_point_desc* pts, size_t n,
+                        kvsim_point_summary* out, size_t min_chunk, kvsim_multi_stats* stats, char* err,
+                        size_t err_len) {
+  if (!ctxs || n_ctx < 1 || n_ctx > KVSIM_MAX_DEVICES) return set_err(err, err_len, KVSIM_E_INVALID, "bad context list");
+  if (n == 0) return KVSIM_OK;
+  if (!pts || !out) return set_err(err, err_len, KVSIM_E_INVALID, "null points/out");
+  for (int k = 0; k < n_ctx; ++k) {
+    if (!ctxs[k]) return set_err(err, err_len, KVSIM_E_INVALID, "null context");
+    for (int j = 0; j < k; ++j)
+      if (ctxs[j]->device == ctxs[k]->device)
+        return set_err(err, err_len, KVSIM_E_INVALID, "contexts must be on distinct devices");
+  }
+  for (size_t i = 0; i < n; ++i)
+    if (pts[i].trace_index >= 0) return set_err(err, err_len, KVSIM_E_INVALID, "multi-device runs use generated traces");
+  const kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts, n, n_ctx, min_chunk);
+  std::vector<cudaEvent_t> ev0(n_ctx, nullptr), ev1(n_ctx, nullptr);
+  std::vector<int64_t> launches(n_ctx, 0);
+  std::vector<char> started(n_ctx, 0);
+  auto chunk = [&](int w, const std::vector<int64_t>& idx, std::vector<kvsim_point_summary>& res,
+                   std::string& e) -> int {
+    kvsim_gpu_ctx* c = ctxs[w];
+    char msg[512] = {0};
+    if (cudaSetDevice(c->device) != cudaSuccess) { e = "cudaSetDevice failed"; return KVSIM_E_CUDA; }
+    if (!started[w]) {
+      if (cudaEventCreate(&ev0[w]) != cudaSuccess || cudaEventCreate(&ev1[w]) != cudaSuccess ||
+          cudaEventRecord(ev0[w], c->stream) != cudaSuccess) {
+        e = "cudaEvent setup failed";
+        return KVSIM_E_CUDA;
+      }
+      started[w] = 1;
+    }
+    std::vector<kvsim_point_desc> sub(idx.size());
+    for (size_t k = 0; k < idx.size(); ++k) sub[k] = pts[idx[k]];
+    const int rc = kvsim_gpu_run_ex(c, sub.data(), sub.size(), nullptr, 0, res.data(), nullptr, msg, sizeof msg);
+    if (rc != KVSIM_OK) { e = msg; return rc; }
+    launches[w] += c->last_launches;
+    if (cudaEventRecord(ev1[w], c->stream) != cudaSuccess) { e = "cudaEventRecord failed"; return KVSIM_E_CUDA; }
+    return KVSIM_OK;
+  };
+  std::string e;
+  std::vector<int64_t> per;
+  const int rc = kvsim_host::run_plan(plan, out, chunk, e, &per);
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->n_devices = n_ctx;
+  }
+  for (int w = 0; w < n_ctx; ++w) {
+    if (!started[w]) continue;
+    cudaSetDevice(ctxs[w]->device);
+    float ms = 0.f;
+    cudaEventSynchronize(ev1[w]);
+    if (stats && cudaEventElapsedTime(&ms, ev0[w], ev1[w]) == cudaSuccess) stats->device_seconds[w] = ms * 1e-3;
+    cudaEventDestroy(ev0[w]);
+    cudaEventDestroy(ev1[w]);
+  }
+  if (stats)
+    for (int w = 0; w < n_ctx; ++w) {
+      stats->device_points[w] = per.empty() ? 0 : per[w];
+      stats->device_launches[w] = launches[w];
+    }
+  if (rc != KVSIM_OK) return set_err(err, err_len, rc, e);
   return KVSIM_OK;
 }
 

@@ -91,3 +91,23 @@ extern "C" void kvemu_prof(long long* out) {
   for (int i = 0; i < 32; ++i) out[i] = kvsim_dev::emu_prof[i];
 }
 #endif
+
+// The multi-device sharder (kvsim_shard.hpp, used by kvsim_gpu_run_multi and
+// the CLI) with emulated devices: `workers` host threads each run their
+// chunks through the emulated kernel. Results must not depend on `workers`.
+#include "../../paper_2411_05555_b200/csrc/kvsim_shard.hpp"
+extern "C" int kvemu_run_multi(const kvsim_point_desc* pts, int64_t n, int workers, int64_t min_chunk,
+                               kvsim_point_summary* out, int64_t* points_per_worker) {
+  const kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts, (size_t)n, workers, (size_t)min_chunk);
+  auto chunk = [&](int, const std::vector<int64_t>& idx, std::vector<kvsim_point_summary>& res, std::string&) {
+    std::vector<kvsim_point_desc> sub(idx.size());
+    for (size_t k = 0; k < idx.size(); ++k) sub[k] = pts[idx[k]];
+    return kvemu_run(sub.data(), (int64_t)sub.size(), nullptr, 0, res.data(), nullptr, nullptr, 0, nullptr, 1, nullptr,
+                     0);
+  };
+  std::string e;
+  std::vector<int64_t> per;
+  const int rc = kvsim_host::run_plan(plan, out, chunk, e, &per);
+  for (int w = 0; w < workers && points_per_worker; ++w) points_per_worker[w] = per[(size_t)w];
+  return rc;
+}

@@ -280,3 +280,39 @@ def test_queue_depth_rule_on_oracle(policy):
     s = _queue_series(ref.events, policy == "unified")
     assert s and all(d >= 0 for _, d in s) and s[-1][1] == 0
     assert max(d for _, d in s) > 0
+
+
+@pytest.mark.gpu
+def test_cli_sharder_gpu_count_invariance(kvsim, tmp_path):
+    """The CLI sharder (guided chunks over cost-sorted points, results by
+    index) gives byte-identical outputs for 1, 2 and 3 workers. One GPU here:
+    KVSIM_VIRTUAL_GPUS lets several workers share it (a logic test of the
+    sharder, not a performance setting)."""
+    cfg = {"policies": ["accellm", "splitwise_static", "unified"], "rates": [1, 3, 6, 12, 20], "instances": 4,
+           "num_requests": 600, "workload": "mixed", "seeds": [0, 1], "sweep_instances": [4, 8]}
+    c = write(tmp_path, "c.json", cfg)
+    outs = []
+    env = dict(os.environ, KVSIM_VIRTUAL_GPUS="1")
+    for g in (1, 2, 3):
+        o = tmp_path / f"g{g}"
+        r = subprocess.run([kvsim, "sweep", "--config", c, "--out", str(o), "--gpus", str(g)], capture_output=True,
+                           text=True, env=env)
+        assert r.returncode == 0, r.stderr
+        outs.append(((o / "summary.csv").read_bytes(), (o / "sweep_long.csv").read_bytes(),
+                     json.load(open(o / "report.json"))["points"]))
+    assert all(x == outs[0] for x in outs)
+
+
+@pytest.mark.gpu
+def test_run_multi_matches_single_launch():
+    """kvsim_gpu_run_multi (the bench's multi-GPU path) on the visible GPU:
+    chunked, cost-sorted, summaries scattered by index == one launch."""
+    import paper_2411_05555_b200 as pkg
+    from configs import random_small
+    pts = [random_small(4000 + i, max_req=200) for i in range(90)]
+    sim = pkg.KvSim(0)
+    one = sim.run(pts)
+    multi, st = pkg.run_multi([sim], pts, min_chunk=4)
+    assert st.device_points[0] == len(pts) and st.device_launches[0] > 1 and st.device_seconds[0] > 0
+    assert all(bytes(a) == bytes(b) for a, b in zip(one, multi))
+    sim.close()
