@@ -172,6 +172,10 @@ struct Inst {
   // idle_t (last job end) when the cluster's zero-live measure was idle_z
   double idle_t = 0, idle_z = 0, idle_rb = 0;
   int role0 = DECODE;
+  // inter-pair leveling: KV of migrated requests still held as the source of
+  // in-flight transfers, released at the first boundary >= lvl_until (§6b)
+  int64_t lvl_hold = 0;
+  double lvl_until = 0;
 };
 
 struct Sim {
@@ -734,6 +738,7 @@ struct Sim {
   }
   void acc_boundary(int x, double t) {
     Inst& X = I[x];
+    if (X.lvl_hold > 0 && t >= X.lvl_until) { X.used -= X.lvl_hold; X.lvl_hold = 0; }
     join(x, t);
     if (X.switch_pending) {
       X.switch_pending = false;
@@ -991,7 +996,6 @@ struct Sim {
     for (int rid : moved) {
       Req& r = R[rid];
       const int64_t k = r.kv();
-      X.used -= k;
       if (r.copy >= 0) I[r.copy].used -= k;
       r.copy = -1;
       r.primary = y;
@@ -999,6 +1003,9 @@ struct Sim {
       double start = t > busy ? t : busy;
       double fin = start + transfer_lat(f, (double)k * f.kvb);
       busy = fin;
+      // x stays the source of the transfer: it holds the KV until it is done
+      X.lvl_hold += k;
+      if (fin > X.lvl_until) X.lvl_until = fin;
       level_tokens += k;
       r.n_moves += 1;
       ++n_moves;
@@ -1164,6 +1171,7 @@ struct Sim {
         else sum[x] += r.qlen;
       }
       if (policy == KVSIM_POLICY_SPLITWISE && X.job != NONE && x < n_prefill) sum[x] += X.job_s1;
+      sum[x] += X.lvl_hold;
     }
     for (int x = 0; x < n; ++x) {
       if (sum[x] != I[x].used) {

@@ -168,6 +168,8 @@ struct Sim {
   // migration (destination, token budget); lane g owns degraded group g
   int32_t L_partner, L_lvl_dst;
   int64_t L_lvl_bud;
+  int64_t L_lvl_hold;  // KV of leveled requests held until their transfers finish
+  double L_lvl_until;
   int32_t G_mode, G_cnt;
   int64_t tick;
   // idle while runnable: this lane's instance has been idle
@@ -410,6 +412,8 @@ struct Sim {
     L_partner = lane ^ 1;
     L_lvl_dst = -1;
     L_lvl_bud = 0;
+    L_lvl_hold = 0;
+    L_lvl_until = 0.0;
     G_mode = G_cnt = 0;
     tick = 1;
     L_idle_t = L_idle_z = L_idle_rb = 0.0;
@@ -1808,6 +1812,9 @@ struct Sim {
 
   KV_DEV_NOINLINE void acc_boundary(int x, double t) {
     EMU_COUNT(9);
+    if constexpr (EXT) {
+      if (own(x) && L_lvl_hold > 0 && t >= L_lvl_until) { L_used -= L_lvl_hold; L_lvl_hold = 0; }
+    }
     join(x, t);
     if (get(L_pend, x)) {
       if (own(x)) L_pend = 0;
@@ -2283,12 +2290,17 @@ struct Sim {
         if (own(x)) L_ncopy -= 1;
       }
       batch_remove(x, idx);
-      if (own(x)) { L_skv -= kv; L_used -= kv; }
       add_used(y, kv);
       const double busy = link_get(x, y);
       const double start = t > busy ? t : busy;
       const double fin = kadd(start, transfer_latency(PC.f, kmul((double)kv, PC.f.kvb)));
       link_set(x, y, fin);
+      // x stays the source of the transfer: it holds the KV until it is done
+      if (own(x)) {
+        L_skv -= kv;
+        L_lvl_hold += kv;
+        if (fin > L_lvl_until) L_lvl_until = fin;
+      }
       incoming_append(y, rid, fin);
       if (own(y)) L_skv_in += kv;
       if (lane == 0) { ws()->ct.n_moves += 1; ws()->ct.lvl_tokens += kv; }
