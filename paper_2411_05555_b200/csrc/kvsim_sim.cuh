@@ -997,6 +997,7 @@ struct Sim {
   // per-member register state of an AcceLLM pair chain (driver lane)
   struct MemberChain {
     double e, js, busy, link, mfin, prev, de1, dpe, dG, mr, comp, mlat;
+    double Kd;  // == (double)(skv + steps * B): the running KV sum of the next step
     int64_t skv, skv_in, used, peak, copy_tok, kvmin, tw;
     int32_t B, ni, m, minrem, dj, role, steps;
     bool stepping;
@@ -1007,24 +1008,29 @@ struct Sim {
   };
   // one virtual step end of a chained pair member (bookkeeping only; the
   // caller has evaluated the stop tests)
+  // (c.tw counts steps ending in the window; skv is applied after the chain)
   KV_DEV void lean_step(MemberChain& c, const ChainK& K, int cid) {
     const double e = c.e;
-    if (c.js >= K.warmup) c.busy = kadd(c.busy, ksub(e, c.js));
-    if (e >= K.warmup) c.tw += c.B;
+    const double st = ksub(e, c.js);
+    if (c.js >= K.warmup) c.busy = kadd(c.busy, st);
+    if (e >= K.warmup) c.tw += 1;
     if (c.dj == 0) { c.de1 = e; c.dpe = c.prev; }
-    else { const double g = ksub(e, c.prev); if (g > c.dG) c.dG = g; }
+    else {  // deferred steps pending: the previous step ended where this one started
+      const double g = c.js == c.prev ? st : ksub(e, c.prev);
+      if (g > c.dG) c.dG = g;
+    }
     if (c.m > 0) {
-      const double st = e > c.link ? e : c.link;
-      c.link = kadd(st, c.mlat);
+      const double lk = e > c.link ? e : c.link;
+      c.link = kadd(lk, c.mlat);
       c.mfin = c.link;
       if constexpr (LOG) log_one(e, KVSIM_EV_TRANSFER, cid, cid ^ 1, 1, c.m);
     }
     if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, cid, c.B, 0, 0);
-    c.skv += c.B;
-    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv);
+    c.Kd = kadd(c.Kd, (double)c.B);
+    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv + (int64_t)(c.steps + 1) * c.B);
     c.prev = e;
     c.js = e;
-    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul((double)c.skv, K.kvb)), K.mden, K.mrcp), c.comp));
+    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul(c.Kd, K.kvb)), K.mden, K.mrcp), c.comp));
     c.dj += 1;
     c.steps += 1;
   }
@@ -1066,35 +1072,61 @@ struct Sim {
         const double Wb = PC.f.W, kvb = PC.f.kvb, mden = PC.f.mem_den, mrcp = PC.f.mem_rcp;
         double e = L_busy_until, js = L_job_start, busy = L_busy_time, prev = L_prev_end;
         double dG = L_dG, de1 = L_de1, dpe = L_dpe;
-        int64_t skv = L_skv, used = L_used, peak = L_peak;
-        int32_t dj = L_dj, minrem = L_minrem;
+        const int64_t skv0 = L_skv, used0 = L_used;
+        const int32_t dj0 = L_dj, minrem0 = L_minrem;
+        // the integer stop tests as one trip count: no member may complete
+        // (minrem >= 2), the next step's KV growth fits, the event budget
+        int64_t nmax = (int64_t)minrem0 - 1;
+        const int64_t room = (cap - used0) / B;
+        if (room < nmax) nmax = room;
         const int64_t lim = budget < (int64_t)0x7fffffff ? budget : (int64_t)0x7fffffff;
-        int32_t k = 0;
-        while (minrem >= 2 && used + B <= cap && k < lim) {
-          if (!(e < ht || (e == ht && key < hk))) break;
-          if (e >= mr) break;
+        if (lim < nmax) nmax = lim;
+        // the time tests (e < ht || (e == ht && key < hk)) && e < mr as one
+        // comparison e < tl (e <= t <=> e < nextup(t) for non-negative t)
+        double tl = ht;
+        bool strict = !(key < hk);
+        if (mr <= tl) { tl = mr; strict = true; }
+        if (!strict && tl < kInf) tl = as_f64(as_u64(tl) + 1);
+        double Kd = (double)skv0;  // == (double)skv at every step (exact below 2^53)
+        const double Bd = (double)B;
+        int64_t k = 0, ntw = 0;
+        if (nmax > 0 && e < tl) {
+          // first chained step: its members' gap is taken at flush (de1 / dpe)
           if (js >= warmup) busy = kadd(busy, ksub(e, js));
-          if (e >= warmup) tw += B;
-          if (dj == 0) { de1 = e; dpe = prev; }
+          if (e >= warmup) ntw += 1;
+          if (dj0 == 0) { de1 = e; dpe = prev; }
           else { const double g = ksub(e, prev); if (g > dG) dG = g; }
           if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
-          skv += B;
-          used += B;
-          if (used > peak) peak = used;
-          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv);
-          prev = e;
+          Kd = kadd(Kd, Bd);
+          if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + B);
           js = e;
-          e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul((double)skv, kvb)), mden, mrcp), comp));
-          dj += 1;
-          minrem -= 1;
-          k += 1;
-        }
-        if (k > 0) {
+          e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+          k = 1;
+          // steady state: the step that just ended started at the previous
+          // end (js == prev), so one difference is both the busy increment
+          // and the members' gap
+          while (k < nmax && e < tl) {
+            const double st = ksub(e, js);
+            if (js >= warmup) busy = kadd(busy, st);
+            if (st > dG) dG = st;
+            if (e >= warmup) ntw += 1;
+            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+            Kd = kadd(Kd, Bd);
+            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (k + 1) * B);
+            js = e;
+            e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+            k += 1;
+          }
+          prev = js;
+          const int64_t grow = k * B;
           L_busy_until = e; L_job_start = js; L_busy_time = busy; L_prev_end = prev;
           L_dG = dG; L_de1 = de1; L_dpe = dpe;
-          L_skv = skv; L_used = used; L_peak = peak; L_dj = dj; L_minrem = minrem;
+          L_skv = skv0 + grow; L_used = used0 + grow;
+          if (L_used > L_peak) L_peak = L_used;  // the ledger only grows in a chain
+          L_dj = dj0 + (int32_t)k; L_minrem = minrem0 - (int32_t)k;
           steps = k;
           tmax = prev;
+          tw = ntw * B;
         }
         tok = steps * B;
       }
@@ -1132,7 +1164,7 @@ struct Sim {
       const int32_t bcompB = simt::shfl(L_compB, pl);
       const double bcomp = simt::shfl(L_comp, pl);
       b.mr = b.ni > 0 ? bmr : kInf;
-      b.tw = 0; b.steps = 0;
+      b.tw = 0; b.steps = 0; b.Kd = (double)b.skv;
       const bool drv = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) &&
                        (qn_pair == 0 || L_role == ROLE_PREFILL || b.role == ROLE_PREFILL) &&
                        !L_pend && !bpend && (L_job == JOB_STEP || b.stepping);
@@ -1143,7 +1175,7 @@ struct Sim {
       a.peak = L_peak; a.copy_tok = L_copy_tok; a.m = L_ncopy; a.minrem = L_minrem; a.role = L_role;
       a.kvmin = L_kvmin; a.dj = L_dj; a.dG = L_dG; a.de1 = L_de1; a.dpe = L_dpe;
       a.mr = L_ni > 0 ? L_min_ready : kInf;
-      a.tw = 0; a.steps = 0;
+      a.tw = 0; a.steps = 0; a.Kd = (double)a.skv;
       if (drv) {
         double pht = ht;
         int32_t phk = hk;
@@ -1188,19 +1220,23 @@ struct Sim {
         int64_t SA = cap - a.used, SB = cap - b.used;
         int32_t rA = a.minrem - 1, rB = b.minrem - 1;
         const int32_t kA = 3 * 64 + lane, kB = kA + 1;
+        // per member, (e < pht || (e == pht && key < phk)) && e < mr as one
+        // comparison e < tl (e <= t <=> e < nextup(t) for non-negative t)
+        auto tlim = [&](int32_t key, double mr) {
+          double tl = pht;
+          bool strict = !(key < phk);
+          if (mr <= tl) { tl = mr; strict = true; }
+          if (!strict && tl < kInf) tl = as_f64(as_u64(tl) + 1);
+          return tl;
+        };
+        const double tlA = tlim(kA, a.mr), tlB = b.stepping ? tlim(kB, b.mr) : -1.0;
         for (;;) {
           if (a.stepping && (!b.stepping || !(b.e < a.e))) {  // ties: lower id (even lane)
-            const double e = a.e;
-            if (!(e < pht || (e == pht && kA < phk)) || e >= a.mr || rA <= 0 || budget <= 0 || GA >= 0 ||
-                SA < a.B || SB < a.m)
-              break;
+            if (!(a.e < tlA) || rA <= 0 || budget <= 0 || GA >= 0 || SA < a.B || SB < a.m) break;
             lean_step(a, K, lane);
             rA -= 1; SA -= a.B; SB -= a.m; GA += a.B - 1; GB -= a.B;
           } else {
-            const double e = b.e;
-            if (!b.stepping || !(e < pht || (e == pht && kB < phk)) || e >= b.mr || rB <= 0 || budget <= 0 ||
-                GB >= 0 || SB < b.B || SA < b.m)
-              break;
+            if (!(b.e < tlB) || rB <= 0 || budget <= 0 || GB >= 0 || SB < b.B || SA < b.m) break;
             lean_step(b, K, lane + 1);
             rB -= 1; SB -= b.B; SA -= b.m; GB += b.B - 1; GA -= b.B;
           }
@@ -1216,6 +1252,8 @@ struct Sim {
           a.minrem -= a.steps; b.minrem -= b.steps;
           if (a.kvmin != INT64_MAX) a.kvmin += a.steps;
           if (b.kvmin != INT64_MAX) b.kvmin += b.steps;
+          a.skv += (int64_t)a.steps * a.B; b.skv += (int64_t)b.steps * b.B;
+          a.tw *= a.B; b.tw *= b.B;
         }
         if (!a.stepping) a.B = L_nb;
         steps = a.steps + b.steps;

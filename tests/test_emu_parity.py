@@ -77,3 +77,21 @@ def test_detail_metrics_random(chunk):
         if g.status == 0 and g.summary.n_tbt_samples > 0:
             assert not math.isnan(g.summary.tbt_p50) and g.summary.tbt_p50 <= g.summary.tbt_p95 <= g.summary.tbt_max
     assert not bad, bad
+
+
+@pytest.mark.parametrize("chunk", range(2))
+def test_sweep_specialisation_no_log(chunk):
+    """The sweep specialisation (no event log compiled in, the chained step
+    loops the benchmark runs) against the oracle: summaries, per-request and
+    per-instance records bit for bit."""
+    pts = [random_small(i) for i in range(600 + chunk * 40, 640 + chunk * 40)]
+    pts += [random_small(900 + i, max_req=300) for i in range(chunk * 10, chunk * 10 + 10)]
+    pts += [config1(seed=5 + chunk, n=200), config2("accellm", 9.0, n=150), config2("unified", 9.0, n=150),
+            config2("splitwise", 9.0, n=150)]
+    got = run_points_emu(pts, ev_cap=0, warps=4)
+    bad = []
+    for p, g in zip(pts, got):
+        d = diff_results(run_oracle(p, ev_cap=0), g, events=False)
+        if d:
+            bad.append((p.policy, p.num_instances, p.num_requests, d[:4]))
+    assert not bad, bad
