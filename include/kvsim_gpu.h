@@ -96,7 +96,12 @@ typedef struct kvsim_point_desc {
    * PAPER.md:309,457; docs/SEMANTICS.md §6b). Zero = off / default. */
   int32_t accellm_flags;        /* bit 0 degraded mode, bit 1 inter-pair leveling */
   int32_t degraded_trigger_ticks;   /* 0 => 3 consecutive timer ticks */
-  int32_t reserved_i[6];
+  /* v2: Splitwise high-load co-batching (off by default):
+   * while a prompt waits and every prefill instance is busy, a decode
+   * instance co-batches queued prompts into its next iteration
+   * (docs/SEMANTICS.md §6 splitwise) */
+  int32_t splitwise_cobatch;
+  int32_t reserved_i[5];
   double policy_timer_s;        /* 0 => 1.0 s timer period */
   double leveling_link_fraction;/* 0 => 0.10 of link capacity per timer period */
   double degraded_redundancy;   /* 0 => 0.5: enter when copies < this x live */

@@ -210,6 +210,7 @@ struct Sim {
   // (x^1 normally; the dual instance for a degraded group's decoders; -1 for
   // the dual instance itself).
   bool ext = false, deg_on = false, lvl_on = false;
+  bool cobatch = false;  // splitwise high-load co-batching
   double timer_P = 1.0, red_thr = 0.5, exit_fill = 0.5, lvl_frac = 0.10, dual_frac = 1.0 / 3.0;
   int trig = 3;
   int64_t tick = 1;
@@ -233,6 +234,7 @@ struct Sim {
       for (int i = 0; i < n_prefill; ++i) I[i].role = I[i].role0 = PREFILL;
     } else Q.resize(n / 2);
     qtokens.assign(Q.size(), 0);
+    cobatch = policy == KVSIM_POLICY_SPLITWISE && p.splitwise_cobatch != 0;
     if (policy == KVSIM_POLICY_ACCELLM && (p.accellm_flags & 3)) {
       ext = true;
       deg_on = (p.accellm_flags & KVSIM_ACCELLM_DEGRADED) != 0;
@@ -400,9 +402,18 @@ struct Sim {
   }
 
   // ---- decode step (splitwise / accellm decode instances)
+  bool all_prefill_busy() const {
+    for (int p = 0; p < n_prefill; ++p)
+      if (I[p].job == NONE) return false;
+    return true;
+  }
+  // splitwise with co-batching: a decode iteration also prefills queued
+  // prompts while every prefill instance is busy (SEMANTICS §6)
+  bool sw_overflow() const { return cobatch && !Q[0].empty() && all_prefill_busy(); }
   void step_start(int x, double t) {
     Inst& X = I[x];
     bool preempted = false;
+    if (cobatch) { sw_cobatch_start(x, t); return; }
     if (X.batch.empty()) return;
     while (X.used + (int64_t)X.batch.size() > f.cap) {
       int victim = policy == KVSIM_POLICY_ACCELLM ? largest_copy_on(x) : -1;
@@ -436,6 +447,39 @@ struct Sim {
     if (preempted && policy == KVSIM_POLICY_ACCELLM) ensure_prefill(qid(x / 2), t);
   }
 
+  void sw_cobatch_start(int x, double t) {
+    Inst& X = I[x];
+    if (X.batch.empty() && !sw_overflow()) return;
+    while (X.used + (int64_t)X.batch.size() > f.cap) preempt_newest(x);
+    int64_t B = (int64_t)X.batch.size(), K = 0;
+    for (int rid : X.batch) { K += R[rid].kv(); R[rid].stepping = true; }
+    bump(x, B);
+    X.job_reqs.clear();
+    int64_t s1 = 0, s2 = 0;
+    if (sw_overflow()) {
+      while (!Q[0].empty()) {
+        int head = Q[0].front();
+        int64_t len = R[head].qlen;
+        if (!X.job_reqs.empty() && s1 + len > budget) break;
+        if (X.used + len > f.cap) break;
+        pop_front(0);
+        bump(x, len);
+        R[head].primary = x;
+        if (R[head].emitted == 0) R[head].pf_start = t;
+        X.job_reqs.push_back(head);
+        s1 += len;
+        s2 += len * len;
+      }
+    }
+    if (B == 0 && X.job_reqs.empty()) return;
+    double lat = (X.job_reqs.empty() ? 0.0 : prefill_lat(f, s1, s2)) + (B ? decode_lat(f, B, K) : 0.0);
+    job_begin(X, t);
+    X.job = JOB_STEP;
+    X.job_start = t;
+    X.busy_until = t + lat;
+    log(KVSIM_EV_STEP_START, x, (int)B, (int)X.job_reqs.size(), K);
+  }
+
   void step_end(int x, double t) {
     Inst& X = I[x];
     account_job(X, t);
@@ -463,6 +507,15 @@ struct Sim {
         keep.push_back(rid);
       }
     }
+    // splitwise co-batched prompts: first token, then join this batch
+    for (int rid : X.job_reqs) {
+      Req& r = R[rid];
+      emit(r, t);
+      if (r.emitted == r.decode) { X.used -= r.kv(); finish_req(r, t); ++completed; }
+      else keep.push_back(rid);
+    }
+    if (!X.job_reqs.empty()) ++n_prefills;
+    X.job_reqs.clear();
     X.batch.swap(keep);
     if (policy == KVSIM_POLICY_ACCELLM && m > 0) {
       double& busy = link_busy[(size_t)x * n + y];
@@ -551,6 +604,7 @@ struct Sim {
           if (d < 0 || fr > best) { d = j; best = fr; }
         }
         if (best < len) break;
+        if (X.used + s1 + len > f.cap) break;  // the prefill instance holds the job's prompts
         pop_front(0);
         bump(d, len);
         R[head].primary = d;
@@ -568,6 +622,9 @@ struct Sim {
       X.busy_until = t + prefill_lat(f, s1, s2);
       log(KVSIM_EV_PREFILL_START, p, (int)X.job_reqs.size(), X.job_reqs[0], s1);
     }
+    if (cobatch)  // idle decode instances (ascending id) take overflow prompts
+      for (int d = n_prefill; d < n && sw_overflow(); ++d)
+        if (I[d].job == NONE) sw_cobatch_start(d, t);
   }
   void sw_prefill_done(int p, double t) {
     Inst& X = I[p];
@@ -1155,7 +1212,10 @@ struct Sim {
       for (int rid : I[x].job_reqs) in_job[rid] = 1;
     for (int64_t i = 0; i < next_arrival; ++i) {
       const Req& r = R[i];
-      if (r.emitted > r.decode) return false;
+      if (r.emitted > r.decode) {
+        if (getenv("KVO_DEBUG")) fprintf(stderr, "emitted>decode rid=%lld\n", (long long)i);
+        return false;
+      }
       if (r.done || r.primary < 0 || in_job[i]) continue;  // job members: reserved below
       sum[r.primary] += r.held();
       if (r.copy >= 0) {
@@ -1178,7 +1238,10 @@ struct Sim {
         if (getenv("KVO_DEBUG")) fprintf(stderr, "ledger x=%d sum=%lld used=%lld t=%.9g policy=%d\n", x, (long long)sum[x], (long long)I[x].used, now, policy);
         return false;
       }
-      if (I[x].used > f.cap || I[x].used < 0) return false;
+      if (I[x].used > f.cap || I[x].used < 0) {
+        if (getenv("KVO_DEBUG")) fprintf(stderr, "capacity x=%d used=%lld cap=%lld t=%.9g\n", x, (long long)I[x].used, (long long)f.cap, now);
+        return false;
+      }
     }
     return true;
   }

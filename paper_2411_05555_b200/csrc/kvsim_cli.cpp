@@ -251,8 +251,7 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
         std::end(kKeys))
       throw ConfigError("unknown config key: " + kv.first);
   if (const jl::Value* v = in.find("splitwise_cobatch"))
-    if (!(v->kind == jl::Value::Bool && !v->b))
-      throw ConfigError("splitwise_cobatch is not modelled in this version (must be false)");
+    if (v->kind != jl::Value::Bool) throw ConfigError("splitwise_cobatch must be a boolean");
   jl::Value c = jl::Value::object();
   c.set("model", model_obj(in.find("model")));
   c.set("device", device_obj(in.find("device") ? *in.find("device") : jl::Value::string("h100")));
@@ -391,6 +390,8 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
     const double tt = c.find("degraded_mode")->find("trigger_ticks")->num;
     if (tt != std::floor(tt)) throw ConfigError("degraded_mode.trigger_ticks must be an integer");
   }
+  // Splitwise high-load co-batching: off by default
+  c.set("splitwise_cobatch", jl::Value::boolean(in.find("splitwise_cobatch") ? in.find("splitwise_cobatch")->b : false));
   c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
                                                ? in.find("emit_records")->b
                                                : cmd == "run"));
@@ -662,6 +663,7 @@ kvsim_point_desc base_point(const jl::Value& c, const jl::Value& dev) {
   const jl::Value& dm = *c.find("degraded_mode");
   const jl::Value& lv = *c.find("inter_pair_leveling");
   p.accellm_flags = (dm.find("enabled")->b ? KVSIM_ACCELLM_DEGRADED : 0) | (lv.find("enabled")->b ? KVSIM_ACCELLM_LEVELING : 0);
+  p.splitwise_cobatch = c.find("splitwise_cobatch")->b ? 1 : 0;
   p.degraded_trigger_ticks = (int32_t)dm.find("trigger_ticks")->num;
   p.degraded_redundancy = dm.find("redundancy_threshold")->num;
   p.degraded_exit_fill = dm.find("exit_fill")->num;

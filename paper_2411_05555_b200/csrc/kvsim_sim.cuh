@@ -59,6 +59,7 @@ struct PointConst {
   double timer_P, red_thr, exit_fill;
   int64_t lvl_budget, dual_budget;
   int32_t deg_on, lvl_on, trig;
+  int32_t cobatch;  // splitwise high-load co-batching
 };
 struct Counters {
   int64_t n_steps, n_prefills, n_moves, n_preempt, n_evict;
@@ -361,6 +362,7 @@ struct Sim {
     pc.red_thr = d.degraded_redundancy > 0.0 ? d.degraded_redundancy : 0.5;
     pc.exit_fill = d.degraded_exit_fill > 0.0 ? d.degraded_exit_fill : 0.5;
     pc.trig = d.degraded_trigger_ticks > 0 ? d.degraded_trigger_ticks : 3;
+    pc.cobatch = POL == KVSIM_POLICY_SPLITWISE && d.splitwise_cobatch != 0;
     {
       const double lf = d.leveling_link_fraction > 0.0 ? d.leveling_link_fraction : 0.10;
       const double df = d.dual_copy_fraction > 0.0 ? d.dual_copy_fraction : 1.0 / 3.0;
@@ -868,6 +870,9 @@ struct Sim {
   // ------------------------------------------- decode step (splitwise/accellm)
   KV_DEV_NOINLINE void step_start(int x, double t) {
     EMU_COUNT(2);
+    if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
+      if (PC.cobatch) { sw_cobatch_start(x, t); return; }
+    }
     int32_t nb = get(L_nb, x);
     if (nb == 0) return;
     const bool acc = policy == KVSIM_POLICY_ACCELLM;
@@ -1041,6 +1046,7 @@ struct Sim {
     double ht = has_next ? t_next : kInf;
     int32_t hk = -1;  // arrivals precede instance events at equal time
     if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
+      if (PC.cobatch) return;  // co-batching points run the plain event loop
       const bool all_busy = simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
       if (!all_busy) {
         if (get(Q_n, 0) != 0) return;
@@ -1365,6 +1371,69 @@ struct Sim {
 
   }
 
+  // ------------------------------------------- splitwise high-load co-batching
+  // while a prompt waits and every prefill instance is busy, a decode
+  // iteration also prefills queued prompts (SEMANTICS §6 splitwise)
+  KV_DEV bool sw_overflow() {
+    return get(Q_n, 0) > 0 && simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
+  }
+  KV_DEV_NOINLINE void sw_cobatch_start(int x, double t) {
+    int32_t nb = get(L_nb, x);
+    if (nb == 0 && !sw_overflow()) return;
+    while (get(L_used, x) + nb > PC.f.cap) {
+      preempt_newest(x);
+      nb -= 1;
+    }
+    add_used(x, nb);
+    const int64_t K = get(L_skv, x);
+    int32_t k = 0;
+    int64_t s1 = 0, s2 = 0;
+    if (sw_overflow()) {
+      const int32_t h = get(Q_head, 0), qn = get(Q_n, 0);
+      int64_t used = get(L_used, x);
+      while (k < qn) {
+        const int32_t i = k + lane;
+        const bool valid = i < qn;
+        int32_t rid = 0;
+        int64_t len = 0;
+        if (valid) { rid = q_at(0, h, i); len = c_qlen()[rid]; }
+        const int64_t incl = simt::warp_incl_scan(len);
+        const bool okb = (k == 0 && lane == 0) || s1 + incl <= PC.budget;
+        const bool okm = used + incl <= PC.f.cap;
+        const unsigned fail = simt::ballot(valid && !(okb && okm));
+        const int32_t nvalid = simt::popc(simt::ballot(valid));
+        const int32_t take = fail ? simt::ffs(fail) - 1 : nvalid;
+        if (lane < take) {
+          j_rid(x)[k + lane] = rid;
+          if (c_em()[rid] == 0) c_qs()[rid] = t;
+        }
+        const int64_t tsum = take > 0 ? simt::shfl(incl, take - 1) : 0;
+        const int64_t tsq = simt::warp_sum_nn(lane < take ? len * len : (int64_t)0);
+        s1 += tsum;
+        s2 += tsq;
+        used += tsum;
+        k += take;
+        if (take < nvalid || fail) break;
+      }
+      simt::sync();
+      if (k > 0) {
+        q_pop(0, k, s1);
+        add_used(x, s1);
+      }
+    }
+    if (nb == 0 && k == 0) return;
+    const double lat = kadd(k ? prefill_latency(PC.f, s1, s2) : 0.0, nb ? decode_latency(PC.f, nb, K) : 0.0);
+    job_begin(x, t);
+    if (own(x)) {
+      L_job = JOB_STEP;
+      L_job_start = t;
+      L_busy_until = kadd(t, lat);
+      L_njob = k;
+      L_job_s1 = s1;
+    }
+    log(KVSIM_EV_STEP_START, x, nb, k, K);
+  }
+
   KV_DEV_NOINLINE void unified_end(int x, double t) {
     EMU_COUNT(18);
     account_job(x, t);
@@ -1420,7 +1489,7 @@ struct Sim {
       L_minrem = minrem;
     }
     log(KVSIM_EV_STEP_END, x, o.nb_old, completed, 0);
-    unified_start(x, t);
+    if constexpr (POL == KVSIM_POLICY_UNIFIED) unified_start(x, t);
   }
 
   // ------------------------------------------------------------ splitwise
@@ -1450,6 +1519,7 @@ struct Sim {
           const int64_t best = simt::warp_max_i64(fr);
           const int d = simt::ffs(simt::ballot(fr == best)) - 1;
           if (best < len) { stop = true; break; }
+          if (get(L_used, p) + s1 + len > PC.f.cap) { stop = true; break; }  // p holds the job's prompts
           add_used(d, len);
           if (lane == 0) {
             j_rid(p)[k] = rid;
@@ -1476,6 +1546,9 @@ struct Sim {
       }
       log(KVSIM_EV_PREFILL_START, p, k, j_rid(p)[0], s1);
     }
+    if (PC.cobatch)  // idle decode instances (ascending id) take overflow prompts
+      for (int d = n_prefill; d < n && sw_overflow(); ++d)
+        if (get(L_job, d) == JOB_NONE) sw_cobatch_start(d, t);
   }
 
   KV_DEV_NOINLINE void sw_prefill_done(int p, double t) {
@@ -2504,6 +2577,10 @@ struct Sim {
         } else {
           if (policy == KVSIM_POLICY_UNIFIED) {
             unified_end(x, t);
+          } else if (POL == KVSIM_POLICY_SPLITWISE && PC.cobatch) {
+            unified_end(x, t);  // decode members + co-batched prompts (no restart)
+            join(x, t);
+            step_start(x, t);
           } else {
             step_end(x, t);
             if (policy == KVSIM_POLICY_ACCELLM) acc_boundary(x, t);

@@ -52,6 +52,8 @@ def random_small(i: int, max_req: int = 50):
                    arrival=r.choice(["poisson", "poisson", "fixed"]), link=r.choice(["striped", "single"]),
                    prefill_budget=r.choice([8192, 2048, 700]),
                    warmup_s=r.choice([0.0, 0.0, 1.0]))
+    if policy == "splitwise" and r.random() < 0.4:
+        p.splitwise_cobatch = 1  # high-load co-batching
     if r.random() < 0.5:
         # memory-starved: KV capacity of a few thousand tokens forces evictions/preemptions
         from paper_2411_05555_b200.abi import MODELS

@@ -51,7 +51,7 @@ def test_validate_echoes_defaults(kvsim, tmp_path):
                  "link_bandwidth": 1e9}}, "model does not fit in instance memory"),
     ({"workload": {"prompt_range": [10, 5], "decode_range": [1, 2]}}, "1 <= min <= max"),
     ({"policy": "fcfs"}, "unknown policy"),
-    ({"splitwise_cobatch": True}, "not modelled"),
+    ({"splitwise_cobatch": 1}, "splitwise_cobatch must be a boolean"),
     ({"degraded_mode": {"trigger_tick": 2}}, "unknown degraded_mode key: trigger_tick"),
     ({"inter_pair_leveling": 3}, "must be a boolean or an object"),
     ({"policy_timer_s": 0}, "policy_timer_s must be > 0"),
