@@ -189,7 +189,7 @@ class KvSim:
         return list(arr)[:k], list(pl)[:k], list(dl)[:k]
 
 
-def run_multi(sims, points, min_chunk: int = 1):
+def run_multi(sims, points, min_chunk: int = 0):
     """One sweep sharded over the devices of `sims` (open KvSim contexts on
     distinct GPUs): kvsim_gpu_run_multi, one host thread per device, guided
     chunks over the cost-sorted points, no collective. Returns (summaries in

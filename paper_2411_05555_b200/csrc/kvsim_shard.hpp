@@ -9,7 +9,10 @@
 //
 // Chunks follow guided self-scheduling: a claim takes max(min_chunk,
 // remaining / (2 G)) points, so the expensive points go out first in large
-// chunks and the tail of the sweep is cut into small ones.
+// chunks and the tail of the sweep is cut into small ones. Every chunk is
+// one kernel launch whose own tail leaves warps idle, so min_chunk should
+// cover a few waves of resident warps (kvsim_gpu_run_multi: 2 x slots,
+// capped at n / G so every device gets work).
 #pragma once
 #include <stdint.h>
 
@@ -36,7 +39,25 @@ struct ShardPlan {
   std::vector<int64_t> order;  // point indices, most expensive first
   size_t min_chunk = 1;
   int workers = 1;
+  // static mode (few points per device): worker w runs fixed[w] as one chunk
+  std::vector<std::vector<int64_t>> fixed;
 };
+
+// Few points per device (below a few waves of resident warps): one launch
+// per device, points dealt by greedy LPT on the cost estimate (most
+// expensive first, each to the least-loaded device), so launches end
+// together instead of stacking per-launch tails.
+inline void make_static(ShardPlan& s, const kvsim_point_desc* pts) {
+  s.fixed.assign((size_t)s.workers, {});
+  std::vector<double> load((size_t)s.workers, 0.0);
+  for (int64_t i : s.order) {
+    size_t w = 0;
+    for (size_t k = 1; k < load.size(); ++k)
+      if (load[k] < load[w]) w = k;
+    s.fixed[w].push_back(i);
+    load[w] += point_cost(pts[i]);
+  }
+}
 
 inline ShardPlan make_plan(const kvsim_point_desc* pts, size_t n, int workers, size_t min_chunk) {
   ShardPlan s;
@@ -65,6 +86,30 @@ inline int run_plan(const ShardPlan& plan, kvsim_point_summary* out, const Chunk
   std::mutex claim_mu;  // claims are tiny; a lock keeps the guided size exact
   std::vector<std::string> errs((size_t)plan.workers);
   std::vector<int64_t> done((size_t)plan.workers, 0);
+  if (!plan.fixed.empty()) {  // static mode: one chunk per worker
+    std::vector<std::thread> th;
+    for (int w = 0; w < plan.workers; ++w)
+      th.emplace_back([&, w]() {
+        const std::vector<int64_t>& idx = plan.fixed[(size_t)w];
+        if (idx.empty()) return;
+        std::vector<kvsim_point_summary> res(idx.size());
+        std::string e;
+        if (run_chunk(w, idx, res, e) != 0) {
+          errs[(size_t)w] = e.empty() ? "chunk failed" : e;
+          return;
+        }
+        for (size_t k = 0; k < idx.size(); ++k) out[idx[k]] = res[k];
+        done[(size_t)w] = (int64_t)idx.size();
+      });
+    for (auto& t : th) t.join();
+    if (points_per_worker) *points_per_worker = done;
+    for (auto& e : errs)
+      if (!e.empty()) {
+        err = e;
+        return KVSIM_E_INTERNAL;
+      }
+    return KVSIM_OK;
+  }
   auto claim = [&](size_t& a, size_t& b) {
     std::lock_guard<std::mutex> g(claim_mu);
     a = cursor.load();

@@ -98,7 +98,8 @@ extern "C" void kvemu_prof(long long* out) {
 #include "../../paper_2411_05555_b200/csrc/kvsim_shard.hpp"
 extern "C" int kvemu_run_multi(const kvsim_point_desc* pts, int64_t n, int workers, int64_t min_chunk,
                                kvsim_point_summary* out, int64_t* points_per_worker) {
-  const kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts, (size_t)n, workers, (size_t)min_chunk);
+  kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts, (size_t)n, workers, (size_t)(min_chunk ? min_chunk : 1));
+  if (min_chunk == 0) kvsim_host::make_static(plan, pts);
   auto chunk = [&](int, const std::vector<int64_t>& idx, std::vector<kvsim_point_summary>& res, std::string&) {
     std::vector<kvsim_point_desc> sub(idx.size());
     for (size_t k = 0; k < idx.size(); ++k) sub[k] = pts[idx[k]];

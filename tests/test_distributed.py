@@ -77,3 +77,25 @@ def test_sharder_worker_count_invariance():
         assert sum(per) == len(pts) and min(per) > 0
         outs.append(b"".join(bytes(s) for s in S))
     assert all(o == outs[0] for o in outs)
+
+
+def test_sharder_static_lpt_mode():
+    """Few points per device: one launch per worker, points dealt by greedy
+    LPT (kvsim_shard.hpp make_static); results identical to one worker."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from harness import emu
+    from paper_2411_05555_b200.abi import PointDesc, PointSummary
+    L = emu()
+    L.kvemu_run_multi.argtypes = [C.POINTER(PointDesc), C.c_int64, C.c_int, C.c_int64, C.POINTER(PointSummary),
+                                  C.POINTER(C.c_int64)]
+    pts = _points()
+    P = (PointDesc * len(pts))(*pts)
+    outs = []
+    for w in (1, 3):
+        S = (PointSummary * len(pts))()
+        per = (C.c_int64 * w)()
+        assert L.kvemu_run_multi(P, len(pts), w, 0, S, per) == 0  # min_chunk 0: static LPT deal
+        assert sum(per) == len(pts)
+        outs.append(b"".join(bytes(s) for s in S))
+    assert outs[0] == outs[1]
