@@ -1014,9 +1014,7 @@ struct Sim {
   // one virtual step end of a chained pair member (bookkeeping only; the
   // caller has evaluated the stop tests)
   // (c.tw counts steps ending in the window; skv is applied after the chain)
-  // dur < 0: evaluate the next step's duration here; else use dur (the
-  // cooperative chain precomputes them). log: this lane writes the log.
-  KV_DEV void lean_step(MemberChain& c, const ChainK& K, int cid, double dur = -1.0, bool log = true) {
+  KV_DEV void lean_step(MemberChain& c, const ChainK& K, int cid) {
     const double e = c.e;
     const double st = ksub(e, c.js);
     if (c.js >= K.warmup) c.busy = kadd(c.busy, st);
@@ -1030,148 +1028,17 @@ struct Sim {
       const double lk = e > c.link ? e : c.link;
       c.link = kadd(lk, c.mlat);
       c.mfin = c.link;
-      if constexpr (LOG) if (log) log_one(e, KVSIM_EV_TRANSFER, cid, cid ^ 1, 1, c.m);
+      if constexpr (LOG) log_one(e, KVSIM_EV_TRANSFER, cid, cid ^ 1, 1, c.m);
     }
-    if constexpr (LOG) if (log) log_one(e, KVSIM_EV_STEP_END, cid, c.B, 0, 0);
+    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, cid, c.B, 0, 0);
     c.Kd = kadd(c.Kd, (double)c.B);
-    if constexpr (LOG) if (log) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv + (int64_t)(c.steps + 1) * c.B);
+    if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, cid, c.B, 0, c.skv + (int64_t)(c.steps + 1) * c.B);
     c.prev = e;
     c.js = e;
-    if (dur < 0.0) dur = kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul(c.Kd, K.kvb)), K.mden, K.mrcp), c.comp);
-    c.e = kadd(e, dur);
+    c.e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul(c.Kd, K.kvb)), K.mden, K.mrcp), c.comp));
     c.dj += 1;
     c.steps += 1;
   }
-  // Chain of instance x's virtual step ends, run by the whole warp
-  // (unified / splitwise; same stop tests and arithmetic as the per-lane loop
-  // in advance()). Step k of the chain (k >= 0) lasts
-  // D(skv0 + (k+1) B) = max(RN((W + K kvb) / mem_den), comp); 32 of them are
-  // evaluated at once, one per lane, and the serial part -- e += D, the busy
-  // time, the members' largest gap, the window token count -- runs on every
-  // lane with the duration broadcast by a shuffle. Results are committed to
-  // lane x's state; steps/tok/tw/tmax are set on lane x only.
-  KV_DEV_NOINLINE void chain_coop(int x, double ht, int32_t hk, int64_t budget, int64_t& steps, int64_t& tok,
-                                  int64_t& tw, double& tmax) {
-    const double kInf = as_f64(0x7ff0000000000000ull);
-    const int64_t cap = PC.f.cap;
-    const double warmup = PC.warmup;
-    const int32_t B = get(L_nb, x);
-    const double mr = get(L_ni, x) > 0 ? get(L_min_ready, x) : kInf;
-    const double comp = kdiv(kmul(PC.f.two_p, (double)B), PC.f.pf_den);
-    const int32_t key = 3 * 64 + x;
-    const double Wb = PC.f.W, kvb = PC.f.kvb, mden = PC.f.mem_den, mrcp = PC.f.mem_rcp;
-    double e = get(L_busy_until, x), js = get(L_job_start, x), busy = get(L_busy_time, x);
-    double prev = get(L_prev_end, x), dG = get(L_dG, x), de1 = get(L_de1, x), dpe = get(L_dpe, x);
-    const int64_t skv0 = get(L_skv, x), used0 = get(L_used, x);
-    const int32_t dj0 = get(L_dj, x), minrem0 = get(L_minrem, x);
-    int64_t nmax = (int64_t)minrem0 - 1;
-    const int64_t room = (cap - used0) / B;
-    if (room < nmax) nmax = room;
-    const int64_t lim = budget < (int64_t)0x7fffffff ? budget : (int64_t)0x7fffffff;
-    if (lim < nmax) nmax = lim;
-    double tl = ht;
-    bool strict = !(key < hk);
-    if (mr <= tl) { tl = mr; strict = true; }
-    if (!strict && tl < kInf) tl = as_f64(as_u64(tl) + 1);
-    if (!(nmax > 0 && e < tl)) return;
-    int64_t k = 0, ntw = 0;
-    while (k < nmax && e < tl) {
-      // durations of chain steps k .. k+31 (lane j: step k+j)
-      const double Kj = (double)(skv0 + (k + 1 + lane) * (int64_t)B);
-      const double dur = kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kj, kvb)), mden, mrcp), comp);
-      for (int j = 0; j < 32; ++j) {
-        if (!(k < nmax && e < tl)) break;
-        const double st = ksub(e, js);
-        if (js >= warmup) busy = kadd(busy, st);
-        if (e >= warmup) ntw += 1;
-        if (k == 0 && dj0 == 0) { de1 = e; dpe = prev; }
-        else {  // after the chain's first step js == prev, so st is the gap
-          const double g = k == 0 ? ksub(e, prev) : st;
-          if (g > dG) dG = g;
-        }
-        if constexpr (LOG) {
-          if (lane == x) {
-            log_one(e, KVSIM_EV_STEP_END, x, B, 0, 0);
-            log_one(e, KVSIM_EV_STEP_START, x, B, 0, skv0 + (k + 1) * B);
-          }
-        }
-        js = e;
-        e = kadd(e, simt::shfl(dur, j));
-        k += 1;
-      }
-    }
-    if (own(x)) {
-      prev = js;
-      const int64_t grow = k * B;
-      L_busy_until = e; L_job_start = js; L_busy_time = busy; L_prev_end = prev;
-      L_dG = dG; L_de1 = de1; L_dpe = dpe;
-      L_skv = skv0 + grow; L_used = used0 + grow;
-      if (L_used > L_peak) L_peak = L_used;  // the ledger only grows in a chain
-      L_dj = dj0 + (int32_t)k; L_minrem = minrem0 - (int32_t)k;
-      steps = k;
-      tmax = prev;
-      tw = ntw * B;
-      tok = k * B;
-    }
-  }
-
-  static KV_DEV void bcast(MemberChain& c, int s) {
-    c.e = simt::shfl(c.e, s); c.js = simt::shfl(c.js, s); c.busy = simt::shfl(c.busy, s);
-    c.link = simt::shfl(c.link, s); c.mfin = simt::shfl(c.mfin, s); c.prev = simt::shfl(c.prev, s);
-    c.de1 = simt::shfl(c.de1, s); c.dpe = simt::shfl(c.dpe, s); c.dG = simt::shfl(c.dG, s);
-    c.mr = simt::shfl(c.mr, s); c.comp = simt::shfl(c.comp, s); c.mlat = simt::shfl(c.mlat, s);
-    c.Kd = simt::shfl(c.Kd, s);
-    c.skv = simt::shfl(c.skv, s); c.skv_in = simt::shfl(c.skv_in, s); c.used = simt::shfl(c.used, s);
-    c.peak = simt::shfl(c.peak, s); c.copy_tok = simt::shfl(c.copy_tok, s); c.kvmin = simt::shfl(c.kvmin, s);
-    c.tw = simt::shfl(c.tw, s);
-    c.B = simt::shfl(c.B, s); c.ni = simt::shfl(c.ni, s); c.m = simt::shfl(c.m, s);
-    c.minrem = simt::shfl(c.minrem, s); c.dj = simt::shfl(c.dj, s); c.role = simt::shfl(c.role, s);
-    c.steps = simt::shfl(c.steps, s);
-    c.stepping = simt::shfl((int32_t)c.stepping, s) != 0;
-  }
-  // The pair chain of driver lane d (members d, d+1) run by the whole warp:
-  // the same merged order, stop tests and bookkeeping as the per-lane loop
-  // in advance(), with each member's next 16 step durations evaluated in
-  // parallel (lanes 0-15 member a, 16-31 member b; step i of a member lasts
-  // D(skv0 + (i+1) B)) and broadcast to the serial part. On return every lane
-  // holds the final member states (lane d continues with them).
-  KV_DEV_NOINLINE void pair_chain_coop(int d, MemberChain& a, MemberChain& b, ChainK& K, double& tlA, double& tlB,
-                                       int64_t& GA, int64_t& GB, int64_t& SA, int64_t& SB, int32_t& rA,
-                                       int32_t& rB, int64_t& budget) {
-    bcast(a, d);
-    bcast(b, d);
-    K.Wb = simt::shfl(K.Wb, d); K.kvb = simt::shfl(K.kvb, d); K.mden = simt::shfl(K.mden, d);
-    K.mrcp = simt::shfl(K.mrcp, d); K.warmup = simt::shfl(K.warmup, d); K.cap = simt::shfl(K.cap, d);
-    tlA = simt::shfl(tlA, d); tlB = simt::shfl(tlB, d);
-    GA = simt::shfl(GA, d); GB = simt::shfl(GB, d); SA = simt::shfl(SA, d); SB = simt::shfl(SB, d);
-    rA = simt::shfl(rA, d); rB = simt::shfl(rB, d); budget = simt::shfl(budget, d);
-    const bool logger = lane == d;
-    const int j = lane & 15;
-    int ia = 16, ib = 16;
-    double dur = 0.0;
-    for (;;) {
-      if (ia == 16 || ib == 16) {  // next 16 durations of both members
-        const MemberChain& c = lane < 16 ? a : b;
-        const double Kj = (double)(c.skv + (int64_t)(c.steps + 1 + j) * c.B);
-        dur = c.stepping ? kvsim_math::kmax(kdiv_rcp(kadd(K.Wb, kmul(Kj, K.kvb)), K.mden, K.mrcp), c.comp) : 0.0;
-        ia = 0;
-        ib = 0;
-      }
-      if (a.stepping && (!b.stepping || !(b.e < a.e))) {  // ties: lower id (even lane)
-        if (!(a.e < tlA) || rA <= 0 || budget <= 0 || GA >= 0 || SA < a.B || SB < a.m) break;
-        lean_step(a, K, d, simt::shfl(dur, ia), logger);
-        ia += 1;
-        rA -= 1; SA -= a.B; SB -= a.m; GA += a.B - 1; GB -= a.B;
-      } else {
-        if (!(b.e < tlB) || rB <= 0 || budget <= 0 || GB >= 0 || SB < b.B || SA < b.m) break;
-        lean_step(b, K, d + 1, simt::shfl(dur, 16 + ib), logger);
-        ib += 1;
-        rB -= 1; SB -= b.B; SA -= b.m; GB += b.B - 1; GA -= b.B;
-      }
-      budget -= 1;
-    }
-  }
-
   // drive: bitmask of lanes allowed to advance (instances; AcceLLM: any lane
   // of a pair selects the pair)
   KV_DEV_NOINLINE void advance(unsigned drive) {
@@ -1201,15 +1068,6 @@ struct Sim {
       // unified: only pure decode iterations (no co-batched prefill in flight, none pending)
       if constexpr (POL == KVSIM_POLICY_UNIFIED) go = go && Q_n == 0 && L_njob == 0 && L_nb > 0;
       else go = go && lane >= n_prefill && L_nb > 0;
-      const unsigned gm = simt::ballot(go);
-      if (gm != 0 && (gm & (gm - 1)) == 0) {
-        // one driving instance (the common case after a handled event): the
-        // whole warp runs its chain -- lanes compute the durations of the
-        // next 32 steps in parallel, the serial end-time recurrence runs
-        // warp-uniformly on broadcast durations
-        chain_coop(simt::ffs(gm) - 1, ht, hk, budget, steps, tok, tw, tmax);
-        go = false;
-      }
       if (go) {
         const int32_t B = L_nb;
         const double mr = L_ni > 0 ? L_min_ready : kInf;
@@ -1324,16 +1182,10 @@ struct Sim {
       a.kvmin = L_kvmin; a.dj = L_dj; a.dG = L_dG; a.de1 = L_de1; a.dpe = L_dpe;
       a.mr = L_ni > 0 ? L_min_ready : kInf;
       a.tw = 0; a.steps = 0; a.Kd = (double)a.skv;
-      // one driving pair (the common case after a handled event): the whole
-      // warp runs its chain (pair_chain_coop); else each driver lane runs its own
-      const unsigned dmask = simt::ballot(drv);
-      const bool coop = dmask != 0 && (dmask & (dmask - 1)) == 0;
-      const int dlane = coop ? simt::ffs(dmask) - 1 : 0;
       constexpr int64_t kOff = INT64_MIN / 4;  // rebalance test disabled
       int64_t GA = kOff, GB = kOff, SA = 0, SB = 0;
       int32_t rA = 0, rB = 0;
       double tlA = -1.0, tlB = -1.0;
-      ChainK Kc{0.0, 0.0, 1.0, 1.0, 0.0, 0};
       if (drv) {
         double pht = ht;
         int32_t phk = hk;
@@ -1388,8 +1240,7 @@ struct Sim {
         };
         tlA = tlim(kA, a.mr);
         tlB = b.stepping ? tlim(kB, b.mr) : -1.0;
-        Kc = K;
-        if (!coop) {
+        {
           for (;;) {
             if (a.stepping && (!b.stepping || !(b.e < a.e))) {  // ties: lower id (even lane)
               if (!(a.e < tlA) || rA <= 0 || budget <= 0 || GA >= 0 || SA < a.B || SB < a.m) break;
@@ -1404,7 +1255,6 @@ struct Sim {
           }
         }
       }
-      if (coop) pair_chain_coop(dlane, a, b, Kc, tlA, tlB, GA, GB, SA, SB, rA, rB, budget);
       if (drv) {
         {
           const int64_t ua = (int64_t)a.steps * a.B + (int64_t)b.steps * b.m;
