@@ -181,6 +181,43 @@ def test_resource_sweep_knees_and_failed_points(kvsim, tmp_path):
     knees = json.load(open(o / "report.json"))["knees"]
     assert {k["policy"] for k in knees} == {"accellm", "splitwise_static"}
     assert all(k["knee"] is not None and k["knee"] >= 40e9 for k in knees)
+    # every row equals the oracle's run of the same point
+    for x in rows:
+        p = make_point(policy=x["policy"], instances=4, rate=6.0, num_requests=600, workload="mixed", seed=0,
+                       device=(989e12, float(x["hbm_capacity"]), 3.35e12, 900e9))
+        ref = run_oracle(p, ev_cap=0, recs=False)
+        assert ref.status == int(x["status"])
+        if ref.status == 0:
+            assert float(x["jct_mean"]) == ref.summary.jct_mean and float(x["cost_eff"]) == ref.summary.cost_eff
+
+
+@pytest.mark.gpu
+def test_resource_sweep_link_bandwidth_knee(kvsim, tmp_path):  # SPEC.md:432-438,468 (acceptance #10)
+    import acceptance as A
+    bws = list(A.A10_BW)
+    cfg = {"policies": ["accellm", "splitwise_static"], "rate": 4, "instances": 4, "workload": "mixed",
+           "duration_s": 300, "warmup_s": 30, "num_requests": int(4 * 300 * 1.3) + 100, "seed": 1,
+           "resource": {"kind": "link_bandwidth", "values": bws}}
+    o = tmp_path / "o"
+    r = run(kvsim, "resource-sweep", "--config", write(tmp_path, "c.json", cfg), "--out", str(o))
+    assert r.returncode == 0, r.stderr
+    rows = list(csv.DictReader(open(o / "resource_sweep.csv")))
+    assert len(rows) == 2 * len(bws)
+    jct = {}
+    for x in rows:
+        p = A.desk_point(policy=x["policy"], instances=4, workload="mixed", rate=4.0, seed=1,
+                         device=(989e12, 80e9, 3.35e12, float(x["link_bandwidth"])))
+        ref = run_oracle(p, ev_cap=0, recs=False).summary
+        assert float(x["jct_mean"]) == ref.jct_mean and float(x["cost_eff"]) == ref.cost_eff
+        jct.setdefault(x["policy"], []).append((float(x["link_bandwidth"]), ref.jct_mean, ref.cost_eff))
+    # the CLI's knee (1% of best JCT and cost efficiency) from the oracle's rows
+    knees = {k["policy"]: k["knee"] for k in json.load(open(o / "report.json"))["knees"]}
+    for pol, g in jct.items():
+        bj, bc = min(j for _, j, _ in g), max(c for _, _, c in g)
+        assert knees[pol] == min(b for b, j, c in g if j <= 1.01 * bj and c >= 0.99 * bc)
+    # acceptance #10 at 4 req/s: JCT knees within 25% (SEMANTICS §9)
+    kj = {pol: min(b for b, j, _ in g if j <= 1.01 * min(x[1] for x in g)) for pol, g in jct.items()}
+    assert abs(kj["accellm"] / kj["splitwise_static"] - 1.0) <= 0.25
 
 
 @pytest.mark.gpu
