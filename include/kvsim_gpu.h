@@ -101,7 +101,11 @@ typedef struct kvsim_point_desc {
    * instance co-batches queued prompts into its next iteration
    * (docs/SEMANTICS.md §6 splitwise) */
   int32_t splitwise_cobatch;
-  int32_t reserved_i[5];
+  /* v2: the first token comes from the first decode step after the prefill
+   * instead of the prefill itself (SPEC.md:273 alternative; off = SPEC's
+   * default): decode_len tokens take decode_len decode steps */
+  int32_t first_token_decode;
+  int32_t reserved_i[4];
   double policy_timer_s;        /* 0 => 1.0 s timer period */
   double leveling_link_fraction;/* 0 => 0.10 of link capacity per timer period */
   double degraded_redundancy;   /* 0 => 0.5: enter when copies < this x live */

@@ -151,7 +151,8 @@ struct Req {
   double pf_start = kNaN;     // start of the job that produced the first token (queue wait)
   int32_t n_moves = 0, n_preempt = 0;
   bool done = false;
-  int64_t kv() const { return (int64_t)prompt + emitted - 1; }
+  int32_t kvo = -1;           // ft - 1: first token from the prefill (-1) or the first decode step (0)
+  int64_t kv() const { return (int64_t)prompt + emitted + kvo; }
   int64_t held() const { return kv() + (stepping ? 1 : 0); }
 };
 
@@ -211,6 +212,7 @@ struct Sim {
   // the dual instance itself).
   bool ext = false, deg_on = false, lvl_on = false;
   bool cobatch = false;  // splitwise high-load co-batching
+  bool ft = false;       // first token from the first decode step (SPEC.md:273 alternative)
   double timer_P = 1.0, red_thr = 0.5, exit_fill = 0.5, lvl_frac = 0.10, dual_frac = 1.0 / 3.0;
   int trig = 3;
   int64_t tick = 1;
@@ -235,6 +237,7 @@ struct Sim {
     } else Q.resize(n / 2);
     qtokens.assign(Q.size(), 0);
     cobatch = policy == KVSIM_POLICY_SPLITWISE && p.splitwise_cobatch != 0;
+    ft = p.first_token_decode != 0;
     if (policy == KVSIM_POLICY_ACCELLM && (p.accellm_flags & 3)) {
       ext = true;
       deg_on = (p.accellm_flags & KVSIM_ACCELLM_DEGRADED) != 0;
@@ -510,7 +513,7 @@ struct Sim {
     // splitwise co-batched prompts: first token, then join this batch
     for (int rid : X.job_reqs) {
       Req& r = R[rid];
-      emit(r, t);
+      if (!ft) emit(r, t);
       if (r.emitted == r.decode) { X.used -= r.kv(); finish_req(r, t); ++completed; }
       else keep.push_back(rid);
     }
@@ -575,7 +578,7 @@ struct Sim {
     }
     for (int rid : X.job_reqs) {
       Req& r = R[rid];
-      emit(r, t);
+      if (!ft) emit(r, t);
       if (r.emitted == r.decode) { X.used -= r.kv(); finish_req(r, t); ++completed; }
       else { r.primary = x; keep.push_back(rid); }
     }
@@ -636,7 +639,7 @@ struct Sim {
     std::vector<int64_t> per_dst(n, 0);
     for (int rid : X.job_reqs) {
       Req& r = R[rid];
-      emit(r, t);
+      if (!ft) emit(r, t);
       if (r.emitted == r.decode) {
         I[r.primary].used -= r.kv();
         finish_req(r, t);
@@ -817,7 +820,7 @@ struct Sim {
     std::vector<int> survivors;
     for (int rid : X.job_reqs) {
       Req& r = R[rid];
-      emit(r, t);
+      if (!ft) emit(r, t);
       if (r.emitted == r.decode) {
         X.used -= r.kv();
         finish_req(r, t);
@@ -1449,6 +1452,7 @@ int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace, k
     S.R[i].arrival = arr[i];
     S.R[i].prompt = pr[i];
     S.R[i].decode = de[i];
+    S.R[i].kvo = p->first_token_decode ? 0 : -1;
   }
   S.run();
   summarize(S, out, recs, inst);

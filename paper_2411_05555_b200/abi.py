@@ -43,7 +43,7 @@ class PointDesc(C.Structure):
         ("rate", C.c_double), ("duration_s", C.c_double), ("warmup_s", C.c_double),
         ("seed", C.c_uint64), ("num_requests", C.c_int64), ("user_tag", C.c_uint64),
         ("accellm_flags", C.c_int32), ("degraded_trigger_ticks", C.c_int32),
-        ("splitwise_cobatch", C.c_int32), ("reserved_i", C.c_int32 * 5),
+        ("splitwise_cobatch", C.c_int32), ("first_token_decode", C.c_int32), ("reserved_i", C.c_int32 * 4),
         ("policy_timer_s", C.c_double), ("leveling_link_fraction", C.c_double),
         ("degraded_redundancy", C.c_double), ("degraded_exit_fill", C.c_double),
         ("dual_copy_fraction", C.c_double), ("reserved_d", C.c_double * 2),
@@ -167,7 +167,8 @@ def make_point(*, model="llama2-70b", device="h100", policy="accellm", instances
                prefill_budget=8192, num_prefill=0, prompt=None, decode=None,
                trace_index=-1, user_tag=0, degraded=False, leveling=False, timer_s=0.0,
                trigger_ticks=0, leveling_fraction=0.0, degraded_redundancy=0.0,
-               degraded_exit_fill=0.0, dual_copy_fraction=0.0, cobatch=False) -> PointDesc:
+               degraded_exit_fill=0.0, dual_copy_fraction=0.0, cobatch=False,
+               first_token_decode=False) -> PointDesc:
     p = PointDesc()
     (p.param_count, p.num_layers, p.hidden_dim, p.num_kv_heads, p.head_dim,
      p.bytes_per_value) = MODELS[model] if isinstance(model, str) else model
@@ -207,6 +208,7 @@ def make_point(*, model="llama2-70b", device="h100", policy="accellm", instances
     p.degraded_exit_fill = degraded_exit_fill
     p.dual_copy_fraction = dual_copy_fraction
     p.splitwise_cobatch = 1 if cobatch else 0
+    p.first_token_decode = 1 if first_token_decode else 0
     return p
 
 

@@ -155,8 +155,8 @@ inline int validate_point(const kvsim_point_desc& p, char* err, size_t len) {
   if (p.trace_index < 0) {
     if (p.prompt_min < 1 || p.prompt_max < p.prompt_min || p.decode_min < 1 || p.decode_max < p.decode_min)
       return fail(KVSIM_E_INVALID, "workload ranges must satisfy 1 <= min <= max");
-    if (p.decode_max > 0x0fffffff || p.prompt_max > 0x0fffffff)
-      return fail(KVSIM_E_INVALID, "prompt/decode lengths must be < 2^28");
+    if (p.decode_max > 0x07ffffff || p.prompt_max > 0x07ffffff)
+      return fail(KVSIM_E_INVALID, "prompt/decode lengths must be < 2^27");
     if (!(p.rate >= 0)) return fail(KVSIM_E_INVALID, "rate must be >= 0");
   }
   if (p.num_requests < 0 || p.num_requests > 0x7ffffff0ll) return fail(KVSIM_E_INVALID, "num_requests out of range");

@@ -100,7 +100,8 @@ const char* const kKeys[] = {"model", "device", "num_devices", "memory_reserve_f
                              "arrival_process", "rate", "rates", "duration_s", "num_requests", "warmup_s", "seed",
                              "seeds", "efficiency", "link_aggregation", "trace", "sweep_instances",
                              "sweep_devices", "curves", "emit_records", "splitwise_cobatch", "degraded_mode",
-                             "inter_pair_leveling", "policy_timer_s", "output", "resource", "detail_metrics"};
+                             "inter_pair_leveling", "policy_timer_s", "output", "resource", "detail_metrics",
+                             "first_token_decode"};
 
 struct Resolved {
   jl::Value cfg;  // resolved config (defaults filled)
@@ -390,6 +391,11 @@ jl::Value resolve(const jl::Value& in, const std::string& cmd) {
     const double tt = c.find("degraded_mode")->find("trigger_ticks")->num;
     if (tt != std::floor(tt)) throw ConfigError("degraded_mode.trigger_ticks must be an integer");
   }
+  // first token from the first decode step (SPEC.md:273 alternative): off by default
+  if (const jl::Value* v = in.find("first_token_decode"))
+    if (v->kind != jl::Value::Bool) throw ConfigError("first_token_decode must be a boolean");
+  c.set("first_token_decode",
+        jl::Value::boolean(in.find("first_token_decode") ? in.find("first_token_decode")->b : false));
   // Splitwise high-load co-batching: off by default
   c.set("splitwise_cobatch", jl::Value::boolean(in.find("splitwise_cobatch") ? in.find("splitwise_cobatch")->b : false));
   c.set("emit_records", jl::Value::boolean(in.find("emit_records") && in.find("emit_records")->kind == jl::Value::Bool
@@ -664,6 +670,7 @@ kvsim_point_desc base_point(const jl::Value& c, const jl::Value& dev) {
   const jl::Value& lv = *c.find("inter_pair_leveling");
   p.accellm_flags = (dm.find("enabled")->b ? KVSIM_ACCELLM_DEGRADED : 0) | (lv.find("enabled")->b ? KVSIM_ACCELLM_LEVELING : 0);
   p.splitwise_cobatch = c.find("splitwise_cobatch")->b ? 1 : 0;
+  p.first_token_decode = c.find("first_token_decode")->b ? 1 : 0;
   p.degraded_trigger_ticks = (int32_t)dm.find("trigger_ticks")->num;
   p.degraded_redundancy = dm.find("redundancy_threshold")->num;
   p.degraded_exit_fill = dm.find("exit_fill")->num;

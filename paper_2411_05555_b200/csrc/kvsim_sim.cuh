@@ -36,7 +36,9 @@ inline long long emu_prof[32];
 #endif
 
 constexpr int kMaxInst = 32;
-constexpr int32_t kRemMask = 0x0fffffff;
+constexpr int32_t kRemMask = 0x07ffffff;
+// no token yet (first token from a decode step, PC.ft): the step sets first_token
+constexpr int32_t kFirst = 0x08000000;
 constexpr int32_t kJoin = 0x40000000;  // no decode step since joining the batch
 constexpr int32_t kCopy = 0x20000000;  // holds a redundant copy on the partner
 // joined from the incoming list (moved / handed off / leveled) and not yet
@@ -60,6 +62,9 @@ struct PointConst {
   int64_t lvl_budget, dual_budget;
   int32_t deg_on, lvl_on, trig;
   int32_t cobatch;  // splitwise high-load co-batching
+  // first token from the first decode step instead of the prefill
+  // (SPEC.md:273 alternative): kv = prompt + emitted + kvo, kvo = ft - 1
+  int32_t ft, kvo;
 };
 struct Counters {
   int64_t n_steps, n_prefills, n_moves, n_preempt, n_evict;
@@ -363,6 +368,8 @@ struct Sim {
     pc.exit_fill = d.degraded_exit_fill > 0.0 ? d.degraded_exit_fill : 0.5;
     pc.trig = d.degraded_trigger_ticks > 0 ? d.degraded_trigger_ticks : 3;
     pc.cobatch = POL == KVSIM_POLICY_SPLITWISE && d.splitwise_cobatch != 0;
+    pc.ft = d.first_token_decode != 0;
+    pc.kvo = pc.ft - 1;
     {
       const double lf = d.leveling_link_fraction > 0.0 ? d.leveling_link_fraction : 0.10;
       const double df = d.dual_copy_fraction > 0.0 ? d.dual_copy_fraction : 1.0 / 3.0;
@@ -470,8 +477,11 @@ struct Sim {
   // ------------------------------------------------------------- emission
   // token emission for a request leaving a prefill (first or recompute token)
   // by this lane; returns emitted count after.
+  // KV length offset: kv = prompt + emitted + kvo() (SEMANTICS §3)
+  KV_DEV int32_t kvo() const { return PC.kvo; }
   KV_DEV int32_t emit_prefill_token(int32_t rid, double t) {
     int32_t em = c_em()[rid];
+    if (PC.ft) return em;  // the prefill emits nothing; the first decode step does
     if (em == 0) {
       c_first()[rid] = t;
     } else {
@@ -558,15 +568,23 @@ struct Sim {
       const bool was_joiner = (rf & kJoin) != 0;
       const bool joiner = was_joiner && dj == 0;  // no step since joining
       const bool hasc = (rf & kCopy) != 0;
+      const bool first = (rf & kFirst) != 0;  // this step (or the first deferred one) emits its first token
       const bool done = act && rem == 0;
       const bool surv = act && rem != 0;
       const unsigned sm = simt::ballot(surv);
       const int32_t dst = wpos + simt::popc(sm & simt::lanemask_lt());
       const bool moved = surv && dst != j;
-      if (act && (DET || was_joiner || done || moved)) rid = rid_a[j];
+      if (act && (DET || was_joiner || done || moved || first)) rid = rid_a[j];
       double gap = 0.0;
       bool upd = false;
-      if (act) {
+      if (act && first) {  // no earlier token: no gap into the first one
+        c_first()[rid] = dj > 0 ? e1 : t;
+        if (dj > 0) {
+          if (G > tb) { tb = G; upd = true; }
+          gap = ksub(t, prev);
+          if (gap > tb) { tb = gap; upd = true; }
+        }
+      } else if (act) {
         if (dj > 0) {
           const double last0 = was_joiner ? c_last()[rid] : pe;
           double g1 = ksub(e1, last0);
@@ -578,7 +596,7 @@ struct Sim {
         if (gap > tb) { tb = gap; upd = true; }
       }
       if constexpr (DET) {
-        const bool inc = act && c_arr()[rid] >= PC.warmup;
+        const bool inc = act && !first && c_arr()[rid] >= PC.warmup;
         if (inc && joiner) tbt_entry(gap, 1);
         ncont += simt::popc(simt::ballot(inc && !joiner));
       }
@@ -668,12 +686,12 @@ struct Sim {
         const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
         const bool hasc = c_cpy()[rid] >= 0;
         b_rid(x)[k] = rid;
-        b_rem(x)[k] = (dl - em) | kJoin | kSettle | (hasc ? kCopy : 0);
-        b_kvb(x)[k] = pl + dl - 1;
+        b_rem(x)[k] = (dl - em) | kJoin | kSettle | (hasc ? kCopy : 0) | (em == 0 ? kFirst : 0);
+        b_kvb(x)[k] = pl + dl + kvo();
         b_tbt(x)[k] = c_tbt()[rid];
-        kvsum += (int64_t)pl + em - 1;
+        kvsum += (int64_t)pl + em + kvo();
         if (dl - em < minrem) minrem = dl - em;
-        if (hasc && (int64_t)pl + em - 1 < kvmin) kvmin = (int64_t)pl + em - 1;
+        if (hasc && (int64_t)pl + em + kvo() < kvmin) kvmin = (int64_t)pl + em + kvo();
       }
       ncopy += simt::popc(simt::ballot(go && c_cpy()[go ? rid : 0] >= 0));
       keep += simt::popc(sm);
@@ -763,7 +781,7 @@ struct Sim {
       for (int32_t j = lane; j < ni; j += 32) {
         const int32_t rid = i_rid(y)[j];
         if (c_cpy()[rid] == x) {
-          const int64_t kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+          const int64_t kv = (int64_t)c_pl()[rid] + c_em()[rid] + kvo();
           const uint64_t k = ((uint64_t)kv << 32) | (uint32_t)(0x7fffffff - rid);
           if (k > best) { best = k; bidx = j; bwhere = 2; by = y; }
         }
@@ -829,7 +847,7 @@ struct Sim {
       c_qlen()[rid] = qlen;
       c_npre()[rid] += 1;
     }
-    if (own(x)) { L_used -= kv; L_skv -= kv; L_final -= (int64_t)pl + dl - 1; }
+    if (own(x)) { L_used -= kv; L_skv -= kv; L_final -= (int64_t)pl + dl + kvo(); }
     if (rf & kCopy) {
       const int y = partner_of(x);
       if (own(y)) { L_used -= kv; L_copy_tok -= kv; }
@@ -983,9 +1001,15 @@ struct Sim {
     for (int32_t q = lane; q < B; q += 32) {
       const int32_t rf = rem_a[q];
       const double tb = tbt_a[q];
-      const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe;
-      double g1 = ksub(e1, last);
-      if (G > g1) g1 = G;
+      double g1;
+      if (rf & kFirst) {  // first token at the first deferred step end
+        c_first()[b_rid(x)[q]] = e1;
+        g1 = G;
+      } else {
+        const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe;
+        g1 = ksub(e1, last);
+        if (G > g1) g1 = G;
+      }
       rem_a[q] = ((rf & kRemMask) - j) | (rf & kCopy);
       if (g1 > tb) tbt_a[q] = g1;
     }
@@ -1467,15 +1491,16 @@ struct Sim {
       }
       const bool done = act && em == dl;
       const bool join = act && !done;
-      if (done) { c_done()[rid] = t; kvfree += (int64_t)pl + em - 1; }
+      if (done) { c_done()[rid] = t; kvfree += (int64_t)pl + em + kvo(); }
       const unsigned jm = simt::ballot(join);
       if (join) {
         const int32_t pos = nb + add + simt::popc(jm & simt::lanemask_lt());
         b_rid(x)[pos] = rid;
-        b_rem(x)[pos] = dl - em;
-        b_kvb(x)[pos] = pl + dl - 1;
+        // (ft: the prefill emitted nothing, so the last token, if any, predates it)
+        b_rem(x)[pos] = (dl - em) | (PC.ft ? kJoin : 0) | (em == 0 ? kFirst : 0);
+        b_kvb(x)[pos] = pl + dl + kvo();
         b_tbt(x)[pos] = c_tbt()[rid];
-        kvadd += (int64_t)pl + em - 1;
+        kvadd += (int64_t)pl + em + kvo();
         if (dl - em < minrem) minrem = dl - em;
       }
       add += simt::popc(jm);
@@ -1485,7 +1510,7 @@ struct Sim {
     kvfree = simt::warp_sum_nn(kvfree);
     minrem = simt::warp_min_i32(minrem);
     simt::sync();
-    count_tokens(k, t);
+    count_tokens(PC.ft ? 0 : k, t);
     if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
@@ -1579,7 +1604,7 @@ struct Sim {
         const int32_t d = j_dst(p)[i];
         const int32_t em = emit_prefill_token(rid, t);
         const int32_t dl = c_dl()[rid];
-        const int64_t kv = (int64_t)c_pl()[rid] + em - 1;
+        const int64_t kv = (int64_t)c_pl()[rid] + em + kvo();
         done = em == dl;
         if (done) {
           c_done()[rid] = t;
@@ -1592,7 +1617,7 @@ struct Sim {
       completed += simt::popc(simt::ballot(done));
     }
     simt::sync();
-    count_tokens(k, t);
+    count_tokens(PC.ft ? 0 : k, t);
     log(KVSIM_EV_PREFILL_DONE, p, k, completed, 0);
     // one transfer per destination, ascending id; lane d keeps the finish time
     double fin_mine = 0.0;
@@ -1626,7 +1651,7 @@ struct Sim {
         i_rid(d)[pos] = rid;
         i_ready(d)[pos] = fin_d;
         c_cpy()[rid] = -1;
-        simt::atomic_add_smem(&ws()->acc_b[d], (int64_t)c_pl()[rid] + c_dl()[rid] - 1);
+        simt::atomic_add_smem(&ws()->acc_b[d], (int64_t)c_pl()[rid] + c_dl()[rid] + kvo());
       }
     }
     simt::sync();
@@ -1723,7 +1748,7 @@ struct Sim {
         const int32_t pos = ni_y + moved + simt::popc(mm & simt::lanemask_lt());
         i_rid(y)[pos] = rid;
         i_ready(y)[pos] = ready;
-        kv_moved += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+        kv_moved += (int64_t)c_pl()[rid] + c_em()[rid] + kvo();
         if (ready < mn) mn = ready;
       }
       log_lanes(mv, KVSIM_EV_MOVE, x, rid, y, 0);
@@ -1970,7 +1995,7 @@ struct Sim {
         done = em == c_dl()[rid];
         if (done) {
           c_done()[rid] = t;
-          kvfree += (int64_t)c_pl()[rid] + em - 1;
+          kvfree += (int64_t)c_pl()[rid] + em + kvo();
         }
       }
       completed += simt::popc(simt::ballot(done));
@@ -1978,7 +2003,7 @@ struct Sim {
     kvfree = simt::warp_sum_nn(kvfree);
     simt::sync();
     if (own(x)) L_used -= kvfree;
-    count_tokens(k, t);
+    count_tokens(PC.ft ? 0 : k, t);
     log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
     if constexpr (EXT) {
       if (is_dual(x)) {
@@ -2005,7 +2030,7 @@ struct Sim {
       if (act) {
         rid = j_rid(x)[i];
         surv = c_em()[rid] != c_dl()[rid];
-        if (surv) kv = (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+        if (surv) kv = (int64_t)c_pl()[rid] + c_em()[rid] + kvo();
       }
       bool cp = false;
       if (!seq) {
@@ -2070,12 +2095,12 @@ struct Sim {
         if (hasc) c_fresh()[rid] = fin;
         const int32_t pos = nb + add + simt::popc(sm & simt::lanemask_lt());
         b_rid(x)[pos] = rid;
-        b_rem(x)[pos] = (dl - em) | kJoin | (hasc ? kCopy : 0);
-        b_kvb(x)[pos] = pl + dl - 1;
+        b_rem(x)[pos] = (dl - em) | kJoin | (hasc ? kCopy : 0) | (em == 0 ? kFirst : 0);
+        b_kvb(x)[pos] = pl + dl + kvo();
         b_tbt(x)[pos] = c_tbt()[rid];
-        kvadd += (int64_t)pl + em - 1;
+        kvadd += (int64_t)pl + em + kvo();
         if (dl - em < minrem) minrem = dl - em;
-        if (hasc && (int64_t)pl + em - 1 < kvmin) kvmin = (int64_t)pl + em - 1;
+        if (hasc && (int64_t)pl + em + kvo() < kvmin) kvmin = (int64_t)pl + em + kvo();
       }
       addc += simt::popc(simt::ballot(surv && c_cpy()[surv ? rid : 0] == y));
       add += simt::popc(sm);
@@ -2116,7 +2141,7 @@ struct Sim {
     }
     for (int32_t j = lane; j < ni; j += 32) {
       const int32_t rid = i_rid(x)[j];
-      if (c_cpy()[rid] == d) s += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+      if (c_cpy()[rid] == d) s += (int64_t)c_pl()[rid] + c_em()[rid] + kvo();
     }
     return simt::warp_sum_nn(s);
   }
@@ -2140,7 +2165,7 @@ struct Sim {
         rid = j_rid(d)[i];
         const int32_t em = c_em()[rid];
         surv = em != c_dl()[rid];
-        kv = (int64_t)c_pl()[rid] + em - 1;
+        kv = (int64_t)c_pl()[rid] + em + kvo();
       }
       int32_t dst = d;
       bool cp = false;
@@ -2194,7 +2219,7 @@ struct Sim {
           const int32_t pos = base + add + simt::popc(m & simt::lanemask_lt());
           i_rid(X)[pos] = rid;
           i_ready(X)[pos] = fin;
-          kvs += (int64_t)c_pl()[rid] + c_em()[rid] - 1;
+          kvs += (int64_t)c_pl()[rid] + c_em()[rid] + kvo();
         }
         add += simt::popc(m);
       }
@@ -2219,10 +2244,10 @@ struct Sim {
         const int32_t em = c_em()[rid], dl = c_dl()[rid], pl = c_pl()[rid];
         const int32_t pos = nb + add + simt::popc(m & simt::lanemask_lt());
         b_rid(d)[pos] = rid;
-        b_rem(d)[pos] = (dl - em) | kJoin;
-        b_kvb(d)[pos] = pl + dl - 1;
+        b_rem(d)[pos] = (dl - em) | kJoin | (em == 0 ? kFirst : 0);
+        b_kvb(d)[pos] = pl + dl + kvo();
         b_tbt(d)[pos] = c_tbt()[rid];
-        kvadd += (int64_t)pl + em - 1;
+        kvadd += (int64_t)pl + em + kvo();
         if (dl - em < minrem) minrem = dl - em;
       }
       add += simt::popc(m);

@@ -364,7 +364,7 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, co
       mn = std::min(mn, traces[k].prompt_len[i]);
       dm = std::max(dm, traces[k].decode_len[i]);
     }
-    if (dm > 0x0fffffff) return set_err(err, err_len, KVSIM_E_INVALID, "trace decode_len must be < 2^28");
+    if (dm > 0x07ffffff) return set_err(err, err_len, KVSIM_E_INVALID, "trace decode_len must be < 2^27");
     tmin[k] = traces[k].n ? mn : 1;
     tdmax[k] = dm;
   }

@@ -54,6 +54,8 @@ def random_small(i: int, max_req: int = 50):
                    warmup_s=r.choice([0.0, 0.0, 1.0]))
     if policy == "splitwise" and r.random() < 0.4:
         p.splitwise_cobatch = 1  # high-load co-batching
+    if (i * 7919) % 5 == 0:
+        p.first_token_decode = 1  # first token from the first decode step (SPEC.md:273 alternative)
     if r.random() < 0.5:
         # memory-starved: KV capacity of a few thousand tokens forces evictions/preemptions
         from paper_2411_05555_b200.abi import MODELS
@@ -85,6 +87,8 @@ def random_ext(i: int, max_req: int = 200):
                    trigger_ticks=r.choice([0, 1, 2]), leveling_fraction=r.choice([0.0, 0.5, 5.0]),
                    degraded_redundancy=r.choice([0.0, 0.9]), degraded_exit_fill=r.choice([0.0, 0.3, 0.9]),
                    dual_copy_fraction=r.choice([0.0, 0.5]))
+    if (i * 7919) % 4 == 1:
+        p.first_token_decode = 1
     if r.random() < 0.6:
         from paper_2411_05555_b200.abi import MODELS
         W = MODELS[model][0] * MODELS[model][5]

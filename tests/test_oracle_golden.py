@@ -168,3 +168,24 @@ def test_determinism():  # SPEC.md:227 byte-identical reruns
     b = run_oracle(p, ev_cap=0)
     assert bytes(a.summary) == bytes(b.summary)
     assert all(bytes(x) == bytes(y) for x, y in zip(a.recs, b.recs))
+
+
+def test_first_token_from_decode_flag_closed_form():
+    """SPEC.md:273 alternative (first_token_decode): the prefill emits no
+    token, decode_len tokens take decode_len decode steps. On the single
+    request it reproduces SPEC.md:225's engine example literally:
+    JCT = 36.6 ms + sum_{i=0..9} decode_step_latency([512+i]) ~ 141.3 ms."""
+    import ctypes as C
+    from configs import closed_form_point
+    from harness import oracle, run_oracle
+    L = oracle()
+    p = closed_form_point()
+    p.first_token_decode = 1
+    r = run_oracle(p, ev_cap=0)
+    q = r.recs[0]
+    pf = L.kvo_prefill_latency(C.byref(p), 512, 512 * 512)
+    dec = [L.kvo_decode_step_latency(C.byref(p), 1, 512 + i) for i in range(10)]
+    assert abs((q.first_token_s - q.arrival_s) - (pf + dec[0])) <= 1e-9 * (pf + dec[0])
+    jct = q.completion_s - q.arrival_s
+    assert abs(jct - (pf + sum(dec))) <= 1e-9 * jct
+    assert abs(jct - 0.1413) < 0.001 and r.summary.n_steps == 10 and r.summary.tokens_total == 10
