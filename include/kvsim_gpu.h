@@ -295,6 +295,14 @@ int kvsim_gpu_perf_batch(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t
                          const int32_t* pidx, const int32_t* op, const int64_t* s1,
                          const int64_t* s2, double* out, size_t n, char* err, size_t err_len);
 
+/* v2: throughput_curves (reference perfmodel.hpp:108-123; SPEC.md:101-109,
+ * 425-431) on the device: the (length x batch) grid of prefill (phase 0) or
+ * decode (phase 1) latencies through K1, tokens/s = tokens / latency.
+ * Row r = li * n_batch + bi. Host buffers of n_len * n_batch entries. */
+int kvsim_gpu_curves(kvsim_gpu_ctx* ctx, const kvsim_point_desc* p, const int64_t* lengths, size_t n_len,
+                     const int64_t* batch_sizes, size_t n_batch, int phase, double* latency_s,
+                     double* tokens_per_s, char* err, size_t err_len);
+
 /* Device trace generation (K2) for one point: n = min(num_requests, arrivals
  * before duration_s). Writes *n_out. Host buffers of capacity num_requests. */
 int kvsim_gpu_gen_trace(kvsim_gpu_ctx* ctx, const kvsim_point_desc* p, double* arrival_s,

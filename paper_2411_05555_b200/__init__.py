@@ -56,6 +56,9 @@ def load_library() -> C.CDLL:
     L.kvsim_gpu_run_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(PointDesc), C.c_size_t,
                                       C.POINTER(PointSummary), C.c_size_t, C.POINTER(MultiStats), C.c_char_p,
                                       C.c_size_t]
+    L.kvsim_gpu_curves.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.POINTER(C.c_int64), C.c_size_t,
+                                   C.POINTER(C.c_int64), C.c_size_t, C.c_int, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
     L.kvsim_gpu_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                        C.c_char_p, C.c_size_t]
     L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]
@@ -176,6 +179,18 @@ class KvSim:
         rc = self.lib.kvsim_gpu_perf_batch(self.h, P, len(points), a, o, x, y, out, n, self.err, 512)
         self._check(rc, "kvsim_gpu_perf_batch")
         return list(out)
+
+    def curves(self, point, lengths, batch_sizes, phase: str = "decode"):
+        """throughput_curves on the device (K1): [(length, batch, latency_s, tokens_per_s)]."""
+        nl, nb = len(lengths), len(batch_sizes)
+        Ls = (C.c_int64 * nl)(*lengths)
+        Bs = (C.c_int64 * nb)(*batch_sizes)
+        lat = (C.c_double * (nl * nb))()
+        tps = (C.c_double * (nl * nb))()
+        rc = self.lib.kvsim_gpu_curves(self.h, C.byref(point), Ls, nl, Bs, nb, 0 if phase == "prefill" else 1, lat,
+                                       tps, self.err, 512)
+        self._check(rc, "kvsim_gpu_curves")
+        return [(lengths[i // nb], batch_sizes[i % nb], lat[i], tps[i]) for i in range(nl * nb)]
 
     def gen_trace(self, point):
         cap = max(int(point.num_requests), 1)

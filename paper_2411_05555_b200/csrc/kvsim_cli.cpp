@@ -1067,6 +1067,12 @@ int cmd_main(const Args& a) {
     }
     if (lens.empty() || batches.empty()) throw ConfigError("curves: empty lengths or batch_sizes");
     const kvsim_point_desc& p = pts.at(0);
+    // the grid is evaluated on the device (K1, kvsim_gpu_curves); without a
+    // device, by the reference's host perfmodel API (the same math, bit for
+    // bit: csrc/kvsim_math.cuh is shared)
+    kvsim_gpu_ctx* ctx = nullptr;
+    char err[512];
+    const bool dev = kvsim_gpu_device_count() > 0 && kvsim_gpu_open(0, &ctx, err, sizeof err) == 0;
     kvsim::ModelSpec ms{"m", p.param_count, p.num_layers, p.hidden_dim, p.num_kv_heads, p.head_dim, p.bytes_per_value};
     kvsim::InstanceSpec is{{"d", p.peak_flops, p.hbm_capacity, p.hbm_bandwidth, p.link_bandwidth}, p.num_devices,
                            p.num_devices, p.memory_reserve_fraction};
@@ -1074,14 +1080,28 @@ int cmd_main(const Args& a) {
     std::string o = "phase,length,batch,latency_s,tokens_per_s\n";
     for (const char* ph : {"prefill", "decode"}) {
       if (phase != "both" && phase != ph) continue;
-      auto rows = kvsim::throughput_curves(ms, is, ef, lens, batches,
-                                           std::string(ph) == "prefill" ? kvsim::Phase::kPrefill : kvsim::Phase::kDecode);
-      for (auto& r : rows)
-        o += std::string(ph) + "," + std::to_string(r.length) + "," + std::to_string(r.batch) + "," + num(r.latency_s) +
-             "," + num(r.tokens_per_s) + "\n";
+      const bool pre = std::string(ph) == "prefill";
+      std::vector<double> lat(lens.size() * batches.size()), tps(lat.size());
+      if (dev) {
+        if (kvsim_gpu_curves(ctx, &p, lens.data(), lens.size(), batches.data(), batches.size(), pre ? 0 : 1, lat.data(),
+                             tps.data(), err, sizeof err) != 0)
+          throw std::runtime_error(err);
+      } else {
+        auto rows = kvsim::throughput_curves(ms, is, ef, lens, batches, pre ? kvsim::Phase::kPrefill : kvsim::Phase::kDecode);
+        for (size_t r = 0; r < rows.size(); ++r) { lat[r] = rows[r].latency_s; tps[r] = rows[r].tokens_per_s; }
+      }
+      for (size_t li = 0; li < lens.size(); ++li)
+        for (size_t bi = 0; bi < batches.size(); ++bi) {
+          const size_t r = li * batches.size() + bi;
+          o += std::string(ph) + "," + std::to_string(lens[li]) + "," + std::to_string(batches[bi]) + "," + num(lat[r]) +
+               "," + num(tps[r]) + "\n";
+        }
     }
+    if (ctx) kvsim_gpu_close(ctx);
     write_file(a.out + "/curves.csv", o);
-    write_file(a.out + "/meta.json", jl::dump(meta_json(cfg, a.cmd)) + "\n");
+    jl::Value m = meta_json(cfg, a.cmd);
+    m.set("evaluated_on", jl::Value::string(dev ? "gpu (K1 kvsim_perf_kernel)" : "host (perfmodel.hpp API)"));
+    write_file(a.out + "/meta.json", jl::dump(m) + "\n");
     return 0;
   }
   if (a.cmd == "gen-trace") {

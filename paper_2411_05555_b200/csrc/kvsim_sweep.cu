@@ -598,6 +598,32 @@ int kvsim_gpu_perf_batch(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n
   return KVSIM_OK;
 }
 
+int kvsim_gpu_curves(kvsim_gpu_ctx* c, const kvsim_point_desc* p, const int64_t* lengths, size_t n_len,
+                     const int64_t* batch_sizes, size_t n_batch, int phase, double* latency_s, double* tokens_per_s,
+                     char* err, size_t err_len) {
+  if (!c || !p || !lengths || !batch_sizes || !latency_s || !tokens_per_s)
+    return set_err(err, err_len, KVSIM_E_INVALID, "null argument");
+  if (n_len == 0 || n_batch == 0) return set_err(err, err_len, KVSIM_E_INVALID, "empty lengths or batch_sizes");
+  if (phase != 0 && phase != 1) return set_err(err, err_len, KVSIM_E_INVALID, "phase: 0 prefill, 1 decode");
+  const size_t n = n_len * n_batch;
+  std::vector<int32_t> pidx(n, 0), op(n, phase == 0 ? 0 : 1);
+  std::vector<int64_t> s1(n), s2(n);
+  for (size_t li = 0; li < n_len; ++li)
+    for (size_t bi = 0; bi < n_batch; ++bi) {
+      const int64_t L = lengths[li], b = batch_sizes[bi];
+      if (L < 1 || b < 1) return set_err(err, err_len, KVSIM_E_EMPTY_BATCH, phase == 0 ? "empty prefill batch" : "empty decode batch");
+      const size_t r = li * n_batch + bi;
+      if (phase == 0) { s1[r] = b * L; s2[r] = b * L * L; }  // prefill_latency of b prompts of length L
+      else { s1[r] = b; s2[r] = b * L; }                      // decode_step_latency of b requests at KV L
+    }
+  const int rc = kvsim_gpu_perf_batch(c, p, 1, pidx.data(), op.data(), s1.data(), s2.data(), latency_s, n, err, err_len);
+  if (rc != KVSIM_OK) return rc;
+  for (size_t r = 0; r < n; ++r) {
+    tokens_per_s[r] = (double)s1[r] / latency_s[r];  // s1 = tokens: b * L (prefill) or b (one decode step)
+  }
+  return KVSIM_OK;
+}
+
 int kvsim_gpu_gen_trace(kvsim_gpu_ctx* c, const kvsim_point_desc* p, double* arrival_s, int32_t* prompt_len,
                         int32_t* decode_len, int64_t* n_out, char* err, size_t err_len) {
   if (!c || !p) return set_err(err, err_len, KVSIM_E_INVALID, "null argument");

@@ -38,8 +38,9 @@ def test_struct_sizes_match_header(lib):
     src = r'''
 #include <stdio.h>
 #include "kvsim_gpu.h"
-int main(){printf("%zu %zu %zu %zu %zu\n", sizeof(kvsim_point_desc), sizeof(kvsim_point_summary),
-  sizeof(kvsim_request_record), sizeof(kvsim_event_record), sizeof(kvsim_trace_view));}
+int main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(kvsim_point_desc), sizeof(kvsim_point_summary),
+  sizeof(kvsim_request_record), sizeof(kvsim_event_record), sizeof(kvsim_trace_view),
+  sizeof(kvsim_instance_record), sizeof(kvsim_run_opts), sizeof(kvsim_multi_stats));}
 '''
     with tempfile.TemporaryDirectory() as d:
         open(os.path.join(d, "s.c"), "w").write(src)
@@ -47,7 +48,8 @@ int main(){printf("%zu %zu %zu %zu %zu\n", sizeof(kvsim_point_desc), sizeof(kvsi
                         os.path.join(d, "s")], check=True)
         out = subprocess.run([os.path.join(d, "s")], capture_output=True, text=True).stdout.split()
     want = [C.sizeof(pkg.PointDesc), C.sizeof(pkg.PointSummary), C.sizeof(pkg.RequestRecord),
-            C.sizeof(pkg.EventRecord), C.sizeof(pkg.TraceView)]
+            C.sizeof(pkg.EventRecord), C.sizeof(pkg.TraceView), C.sizeof(pkg.InstanceRecord),
+            C.sizeof(pkg.RunOpts), C.sizeof(pkg.MultiStats)]
     assert [int(x) for x in out] == want
 
 

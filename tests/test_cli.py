@@ -353,3 +353,25 @@ def test_run_multi_matches_single_launch():
     assert st.device_points[0] == len(pts) and st.device_launches[0] > 1 and st.device_seconds[0] > 0
     assert all(bytes(a) == bytes(b) for a, b in zip(one, multi))
     sim.close()
+
+
+@pytest.mark.gpu
+def test_curves_on_device_match_host_api(kvsim, tmp_path):
+    """cmd_curves on the device (K1 through kvsim_gpu_curves) equals the
+    reference's host perfmodel API (throughput_curves) bit for bit."""
+    import ctypes as C
+    from harness import oracle
+    cfg = {"model": "llama2-70b", "device": "910b2", "instances": 4,
+           "curves": {"phase": "both", "lengths": [100, 500, 1000], "batch_sizes": [1, 2, 8, 32, 128, 512]}}
+    o = tmp_path / "o"
+    assert run(kvsim, "curves", "--config", write(tmp_path, "c.json", cfg), "--out", str(o)).returncode == 0
+    assert json.load(open(o / "meta.json"))["evaluated_on"].startswith("gpu")
+    rows = list(csv.DictReader(open(o / "curves.csv")))
+    assert len(rows) == 2 * 3 * 6
+    L = oracle()
+    p = make_point(model="llama2-70b", device="910b2")
+    for r in rows:
+        Ln, b = int(r["length"]), int(r["batch"])
+        want = (L.kvo_prefill_latency(C.byref(p), b * Ln, b * Ln * Ln) if r["phase"] == "prefill"
+                else L.kvo_decode_step_latency(C.byref(p), b, b * Ln))
+        assert float(r["latency_s"]) == want
