@@ -56,9 +56,10 @@ def load_library() -> C.CDLL:
     L.kvsim_gpu_run_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.POINTER(PointDesc), C.c_size_t,
                                       C.POINTER(PointSummary), C.c_size_t, C.POINTER(MultiStats), C.c_char_p,
                                       C.c_size_t]
-    L.kvsim_gpu_curves.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.POINTER(C.c_int64), C.c_size_t,
-                                   C.POINTER(C.c_int64), C.c_size_t, C.c_int, C.POINTER(C.c_double),
-                                   C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
+    if hasattr(L, "kvsim_gpu_curves"):  # (absent only in older build variants, tools/ab_inproc.py)
+        L.kvsim_gpu_curves.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.POINTER(C.c_int64), C.c_size_t,
+                                       C.POINTER(C.c_int64), C.c_size_t, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
     L.kvsim_gpu_run_device.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                        C.c_char_p, C.c_size_t]
     L.kvsim_gpu_reserve.argtypes = [C.c_void_p, C.POINTER(PointDesc), C.c_size_t, C.c_char_p, C.c_size_t]

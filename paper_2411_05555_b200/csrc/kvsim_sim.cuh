@@ -477,11 +477,17 @@ struct Sim {
   // ------------------------------------------------------------- emission
   // token emission for a request leaving a prefill (first or recompute token)
   // by this lane; returns emitted count after.
+  // Optional SPEC variants (first_token_decode, splitwise_cobatch) are
+  // compiled into the LOG specialisation only; the sweep specialisation
+  // folds them out and sweep_warp routes points that use them to LOG.
+  static constexpr bool kFeat = LOG;
+  KV_DEV bool ft() const { return kFeat && PC.ft; }
+  KV_DEV bool cobatch() const { return kFeat && PC.cobatch; }
   // KV length offset: kv = prompt + emitted + kvo() (SEMANTICS §3)
-  KV_DEV int32_t kvo() const { return PC.kvo; }
+  KV_DEV int32_t kvo() const { return kFeat ? PC.kvo : -1; }
   KV_DEV int32_t emit_prefill_token(int32_t rid, double t) {
     int32_t em = c_em()[rid];
-    if (PC.ft) return em;  // the prefill emits nothing; the first decode step does
+    if (ft()) return em;  // the prefill emits nothing; the first decode step does
     if (em == 0) {
       c_first()[rid] = t;
     } else {
@@ -568,7 +574,7 @@ struct Sim {
       const bool was_joiner = (rf & kJoin) != 0;
       const bool joiner = was_joiner && dj == 0;  // no step since joining
       const bool hasc = (rf & kCopy) != 0;
-      const bool first = (rf & kFirst) != 0;  // this step (or the first deferred one) emits its first token
+      const bool first = kFeat && (rf & kFirst) != 0;  // this step (or the first deferred one) emits its first token
       const bool done = act && rem == 0;
       const bool surv = act && rem != 0;
       const unsigned sm = simt::ballot(surv);
@@ -889,7 +895,7 @@ struct Sim {
   KV_DEV_NOINLINE void step_start(int x, double t) {
     EMU_COUNT(2);
     if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
-      if (PC.cobatch) { sw_cobatch_start(x, t); return; }
+      if (cobatch()) { sw_cobatch_start(x, t); return; }
     }
     int32_t nb = get(L_nb, x);
     if (nb == 0) return;
@@ -1002,7 +1008,7 @@ struct Sim {
       const int32_t rf = rem_a[q];
       const double tb = tbt_a[q];
       double g1;
-      if (rf & kFirst) {  // first token at the first deferred step end
+      if (kFeat && (rf & kFirst)) {  // first token at the first deferred step end
         c_first()[b_rid(x)[q]] = e1;
         g1 = G;
       } else {
@@ -1070,7 +1076,7 @@ struct Sim {
     double ht = has_next ? t_next : kInf;
     int32_t hk = -1;  // arrivals precede instance events at equal time
     if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
-      if (PC.cobatch) return;  // co-batching points run the plain event loop
+      if (cobatch()) return;  // co-batching points run the plain event loop
       const bool all_busy = simt::ballot(lane < n_prefill && L_job == JOB_NONE) == 0;
       if (!all_busy) {
         if (get(Q_n, 0) != 0) return;
@@ -1497,7 +1503,7 @@ struct Sim {
         const int32_t pos = nb + add + simt::popc(jm & simt::lanemask_lt());
         b_rid(x)[pos] = rid;
         // (ft: the prefill emitted nothing, so the last token, if any, predates it)
-        b_rem(x)[pos] = (dl - em) | (PC.ft ? kJoin : 0) | (em == 0 ? kFirst : 0);
+        b_rem(x)[pos] = (dl - em) | (ft() ? kJoin : 0) | (em == 0 ? kFirst : 0);
         b_kvb(x)[pos] = pl + dl + kvo();
         b_tbt(x)[pos] = c_tbt()[rid];
         kvadd += (int64_t)pl + em + kvo();
@@ -1510,7 +1516,7 @@ struct Sim {
     kvfree = simt::warp_sum_nn(kvfree);
     minrem = simt::warp_min_i32(minrem);
     simt::sync();
-    count_tokens(PC.ft ? 0 : k, t);
+    count_tokens(ft() ? 0 : k, t);
     if (k > 0) if (lane == 0) ws()->ct.n_prefills += 1;
     if (own(x)) {
       L_job = JOB_NONE;
@@ -1579,7 +1585,7 @@ struct Sim {
       }
       log(KVSIM_EV_PREFILL_START, p, k, j_rid(p)[0], s1);
     }
-    if (PC.cobatch)  // idle decode instances (ascending id) take overflow prompts
+    if (cobatch())  // idle decode instances (ascending id) take overflow prompts
       for (int d = n_prefill; d < n && sw_overflow(); ++d)
         if (get(L_job, d) == JOB_NONE) sw_cobatch_start(d, t);
   }
@@ -1617,7 +1623,7 @@ struct Sim {
       completed += simt::popc(simt::ballot(done));
     }
     simt::sync();
-    count_tokens(PC.ft ? 0 : k, t);
+    count_tokens(ft() ? 0 : k, t);
     log(KVSIM_EV_PREFILL_DONE, p, k, completed, 0);
     // one transfer per destination, ascending id; lane d keeps the finish time
     double fin_mine = 0.0;
@@ -2003,7 +2009,7 @@ struct Sim {
     kvfree = simt::warp_sum_nn(kvfree);
     simt::sync();
     if (own(x)) L_used -= kvfree;
-    count_tokens(PC.ft ? 0 : k, t);
+    count_tokens(ft() ? 0 : k, t);
     log(KVSIM_EV_PREFILL_DONE, x, k, completed, 0);
     if constexpr (EXT) {
       if (is_dual(x)) {
@@ -2610,7 +2616,7 @@ struct Sim {
         } else {
           if (policy == KVSIM_POLICY_UNIFIED) {
             unified_end(x, t);
-          } else if (POL == KVSIM_POLICY_SPLITWISE && PC.cobatch) {
+          } else if (POL == KVSIM_POLICY_SPLITWISE && cobatch()) {
             unified_end(x, t);  // decode members + co-batched prompts (no restart)
             join(x, t);
             step_start(x, t);
@@ -2908,6 +2914,8 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
     const int64_t pt = a.order != nullptr ? a.order[p] : (int64_t)p;
     const int32_t pol = a.pts[pt].policy;
     const bool ext = pol == KVSIM_POLICY_ACCELLM && (a.pts[pt].accellm_flags & 3) != 0;
+    // optional SPEC variants run in the LOG specialisation (kFeat)
+    const bool feat = a.pts[pt].first_token_decode != 0 || a.pts[pt].splitwise_cobatch != 0;
 #if !defined(KVSIM_EMU)
     if (a.ptime != nullptr && lane == 0) {  // stored at once: no register live across the point
       unsigned long long t0;
@@ -2921,9 +2929,9 @@ KV_DEV void sweep_warp(const SweepArgs* ap, WarpScratch* w, int32_t slot) {
       else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, true, false, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_UNIFIED, true, false, true>(ap, w, slot, pt);
     } else if (ext) {
-      if (a.ev != nullptr) run_point<KVSIM_POLICY_ACCELLM, true, true>(ap, w, slot, pt);
+      if (a.ev != nullptr || feat) run_point<KVSIM_POLICY_ACCELLM, true, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_ACCELLM, false, true>(ap, w, slot, pt);
-    } else if (a.ev != nullptr) {
+    } else if (a.ev != nullptr || feat) {
       if (pol == KVSIM_POLICY_SPLITWISE) run_point<KVSIM_POLICY_SPLITWISE, true>(ap, w, slot, pt);
       else if (pol == KVSIM_POLICY_ACCELLM) run_point<KVSIM_POLICY_ACCELLM, true>(ap, w, slot, pt);
       else run_point<KVSIM_POLICY_UNIFIED, true>(ap, w, slot, pt);
