@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #define KV_DEV inline
+#define KV_HD_INLINE inline
 #define KV_DEV_NOINLINE inline
 // Fiber-based warp: the 32 lanes are user-level contexts on one OS thread and
 // run round-robin between primitives (one full round per primitive), so the
@@ -130,6 +131,7 @@ inline double floor_d(double x) { return __builtin_floor(x); }
 }  // namespace simt
 #else
 #define KV_DEV __device__ __forceinline__
+#define KV_HD_INLINE __host__ __device__ __forceinline__
 #define KV_DEV_NOINLINE __device__ __noinline__
 namespace simt {
 __device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,13 +33,15 @@ constexpr int kWarpsPerBlock = 4;
 // ------------------------------------------------------------------ kernels
 // MINB = minimum resident blocks per SM requested from ptxas (register cap
 // 65536 / (128 * MINB)); selected at context open (KVSIM_MINB, default below).
-template <int MINB>
+// FULL = false: the lean sweep kernel (plain points only); true: every
+// specialisation (events, detail metrics, AcceLLM extensions, SPEC variants).
+template <int MINB, bool FULL>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(const __grid_constant__ SweepArgs a) {
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(kvsim_smem);
   const int w = threadIdx.x >> 5;
   const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
   if (slot >= a.slots) return;
-  kvsim_dev::sweep_warp(&a, &scratch[w], (int32_t)slot);
+  kvsim_dev::sweep_warp<FULL>(&a, &scratch[w], (int32_t)slot);
 }
 
 __global__ void kvsim_perf_kernel(const kvsim_point_desc* pts, const int32_t* pidx, const int32_t* op,
@@ -132,7 +135,9 @@ struct kvsim_gpu_ctx {
   SweepArgs reserved_args{};
   bool reserved = false;
   int64_t last_launches = 0;
-  void (*kernel)(SweepArgs) = nullptr;
+  void (*kernel)(SweepArgs) = nullptr;       // lean kernel (plain points)
+  void (*kernel_full)(SweepArgs) = nullptr;  // every specialisation
+  int64_t reserved_fast = 0;                 // kvsim_gpu_reserve: plain points first in `order`
   int minb = 3;
 };
 
@@ -141,13 +146,22 @@ namespace {
 using SweepFn = void (*)(SweepArgs);
 constexpr int kDefaultMinBlocks = 3;
 constexpr int kDefaultCarveout = 25;  // percent shared memory (KVSIM_CARVEOUT; -1 = driver default)
-SweepFn sweep_variant(int minb) {
+SweepFn sweep_variant(int minb, bool full) {
   // occupancy is not the limiter (instruction fetch is):
-  // 1-6 blocks/SM measured within 10% of each other, so two variants ship
-  switch (minb) {
-    case 3: return kvsim_sweep_kernel<3>;
-    default: return kvsim_sweep_kernel<2>;
-  }
+  // 2 vs 3 blocks/SM measured 5.91 vs 5.71 s on config 4, so two variants ship
+  if (full) return minb == 3 ? kvsim_sweep_kernel<3, true> : kvsim_sweep_kernel<2, true>;
+  return minb == 3 ? kvsim_sweep_kernel<3, false> : kvsim_sweep_kernel<2, false>;
+}
+
+// Stable partition of the launch order: points the lean kernel can run first
+// (returns their count); everything goes to the full kernel when the run
+// records events or detail metrics.
+int64_t split_order(std::vector<int64_t>& order, const kvsim_point_desc* pts, bool all_full) {
+  if (all_full) return 0;
+  std::stable_partition(order.begin(), order.end(), [&](int64_t i) { return !kvsim_dev::needs_full(pts[i]); });
+  int64_t k = 0;
+  for (int64_t i : order) k += kvsim_dev::needs_full(pts[i]) ? 0 : 1;
+  return k;
 }
 
 int set_err(char* err, size_t len, int code, const std::string& msg) {
@@ -186,12 +200,22 @@ int prepare_arena(kvsim_gpu_ctx* c, const kvsim_host::ArenaGeom& g, size_t n_pts
   return KVSIM_OK;
 }
 
-int launch_sweep(kvsim_gpu_ctx* c, SweepArgs& a, cudaStream_t s, char* err, size_t err_len) {
+// Launch the lean kernel over order[0, n_fast) and the full kernel over
+// order[n_fast, n_pts), back to back on stream s (same arena).
+int launch_sweep(kvsim_gpu_ctx* c, SweepArgs& a, int64_t n_fast, cudaStream_t s, char* err, size_t err_len) {
   const int blocks = (a.slots + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  KV_CUDA(cudaMemsetAsync(a.next_point, 0, sizeof(unsigned long long), s));
-  c->kernel<<<blocks, kWarpsPerBlock * 32, smem_bytes(), s>>>(a);
-  KV_CUDA(cudaGetLastError());
-  c->last_launches = 1;
+  const int64_t n = a.n_pts;
+  c->last_launches = 0;
+  for (int part = 0; part < 2; ++part) {
+    SweepArgs b = a;
+    b.order = a.order + (part ? n_fast : 0);
+    b.n_pts = part ? n - n_fast : n_fast;
+    if (b.n_pts <= 0) continue;
+    KV_CUDA(cudaMemsetAsync(b.next_point, 0, sizeof(unsigned long long), s));
+    (part ? c->kernel_full : c->kernel)<<<blocks, kWarpsPerBlock * 32, smem_bytes(), s>>>(b);
+    KV_CUDA(cudaGetLastError());
+    c->last_launches += 1;
+  }
   return KVSIM_OK;
 }
 
@@ -273,21 +297,25 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
     c->device = device;
     c->sms = prop.multiProcessorCount;
     c->minb = minb;
-    c->kernel = sweep_variant(c->minb);
+    c->kernel = sweep_variant(c->minb, false);
+    c->kernel_full = sweep_variant(c->minb, true);
     c->point_times = std::getenv("KVSIM_POINT_TIMES") != nullptr;
-    // the kernel image must actually load on this device
-    cudaFuncAttributes fa;
-    KV_CUDA(cudaFuncGetAttributes(&fa, c->kernel));
-    KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
     // L1/shared split (percent of the unified array given to shared memory),
     // KVSIM_CARVEOUT overrides; -1 leaves the driver default
     int carve = kDefaultCarveout;
     if (const char* e = std::getenv("KVSIM_CARVEOUT")) carve = std::atoi(e);
-    if (carve >= 0)
-      KV_CUDA(cudaFuncSetAttribute(c->kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    int bps = 1;
-    KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, c->kernel, kWarpsPerBlock * 32, smem_bytes()));
-    c->blocks_per_sm = bps > 0 ? bps : 1;
+    int bps_min = 1 << 30;
+    for (SweepFn k : {c->kernel, c->kernel_full}) {
+      // the kernel image must actually load on this device
+      cudaFuncAttributes fa;
+      KV_CUDA(cudaFuncGetAttributes(&fa, k));
+      KV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes()));
+      if (carve >= 0) KV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      int bps = 1;
+      KV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k, kWarpsPerBlock * 32, smem_bytes()));
+      bps_min = std::min(bps_min, bps);
+    }
+    c->blocks_per_sm = bps_min > 0 ? bps_min : 1;
     // resident blocks per SM actually used (<= the occupancy limit)
     if (const char* e = std::getenv("KVSIM_BLOCKS_PER_SM")) {
       const int want = std::atoi(e);
@@ -396,6 +424,7 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, co
   c->reserved = false;
   // points, order, record offsets
   std::vector<int64_t> order = kvsim_host::lpt_order(pts, n);
+  const int64_t n_fast = split_order(order, pts, (ev && ev_cap) || o.detail != 0);
   std::vector<int64_t> rec_off(n + 1, 0);
   for (size_t i = 0; i < n; ++i) rec_off[i + 1] = rec_off[i] + std::max<int64_t>(pts[i].num_requests, 0);
   KV_CUDA(c->pts.ensure(sizeof(kvsim_point_desc) * n));
@@ -440,7 +469,7 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, co
     a.ptime = (unsigned long long*)c->ptime.p;
     c->ptime_n = (int64_t)n;
   }
-  rc = launch_sweep(c, a, s, err, err_len);
+  rc = launch_sweep(c, a, n_fast, s, err, err_len);
   if (rc) return rc;
   KV_CUDA(cudaMemcpyAsync(out, c->out.p, sizeof(kvsim_point_summary) * n, cudaMemcpyDeviceToHost, s));
   if (recs && rec_off[n] > 0)
@@ -535,6 +564,7 @@ int kvsim_gpu_reserve(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n, c
   int rc = prepare_arena(c, g, n, err, err_len);
   if (rc) return rc;
   std::vector<int64_t> order = kvsim_host::lpt_order(pts, n);
+  c->reserved_fast = split_order(order, pts, false);
   KV_CUDA(c->order.ensure(sizeof(int64_t) * n));
   KV_CUDA(c->counter.ensure(sizeof(unsigned long long)));
   KV_CUDA(cudaMemcpy(c->order.p, order.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
@@ -561,7 +591,7 @@ int kvsim_gpu_run_device(kvsim_gpu_ctx* c, const kvsim_point_desc* d_pts, size_t
   SweepArgs a = c->reserved_args;
   a.pts = d_pts;
   a.out = d_out;
-  return launch_sweep(c, a, stream ? (cudaStream_t)stream : c->stream, err, err_len);
+  return launch_sweep(c, a, c->reserved_fast, stream ? (cudaStream_t)stream : c->stream, err, err_len);
 }
 
 int kvsim_gpu_perf_batch(kvsim_gpu_ctx* c, const kvsim_point_desc* pts, size_t n_pts, const int32_t* pidx,

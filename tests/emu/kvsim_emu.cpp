@@ -49,6 +49,13 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
   std::vector<int64_t> rec_off((size_t)n + 1, 0);
   for (int64_t i = 0; i < n; ++i) rec_off[i + 1] = rec_off[i] + std::max<int64_t>(pts[i].num_requests, 0);
   std::vector<int64_t> order = kvsim_host::lpt_order(pts, (size_t)n);
+  // the same split as the GPU host: plain points through sweep_warp<false>
+  // (the lean kernel), the rest through sweep_warp<true>
+  int64_t n_fast = 0;
+  if (!(ev && ev_cap) && !detail) {
+    std::stable_partition(order.begin(), order.end(), [&](int64_t i) { return !kvsim_dev::needs_full(pts[i]); });
+    for (int64_t i : order) n_fast += kvsim_dev::needs_full(pts[i]) ? 0 : 1;
+  }
   unsigned long long counter = 0;
   a.pts = pts;
   a.order = order.data();
@@ -70,17 +77,27 @@ extern "C" int kvemu_run(const kvsim_point_desc* pts, int64_t n, const kvsim_tra
   a.detail = detail;
   std::vector<WarpScratch> scratch((size_t)slots);
   struct Job { SweepArgs* a; WarpScratch* s; int64_t slot; };
-  std::vector<Job> jobs;
-  for (int w = 0; w < slots; ++w) jobs.push_back(Job{&a, &scratch[w], w});
-  std::vector<std::thread> th;
-  for (int w = 0; w < slots; ++w)
-    th.emplace_back([&, w]() {
-      simt::run_warp([](void* p, int) {
-        Job* j = (Job*)p;
-        sweep_warp(j->a, j->s, (int32_t)j->slot);
-      }, &jobs[w]);
-    });
-  for (auto& t : th) t.join();
+  for (int part = 0; part < 2; ++part) {
+    SweepArgs b = a;
+    b.order = order.data() + (part ? n_fast : 0);
+    b.n_pts = part ? n - n_fast : n_fast;
+    if (b.n_pts <= 0) continue;
+    counter = 0;
+    std::vector<Job> jobs;
+    for (int w = 0; w < slots; ++w) jobs.push_back(Job{&b, &scratch[w], w});
+    std::vector<std::thread> th;
+    for (int w = 0; w < slots; ++w)
+      th.emplace_back([&, w]() {
+        simt::run_warp(part ? +[](void* p, int) {
+          Job* j = (Job*)p;
+          sweep_warp<true>(j->a, j->s, (int32_t)j->slot);
+        } : +[](void* p, int) {
+          Job* j = (Job*)p;
+          sweep_warp<false>(j->a, j->s, (int32_t)j->slot);
+        }, &jobs[w]);
+      });
+    for (auto& t : th) t.join();
+  }
   std::free(base);
   return KVSIM_OK;
 }
