@@ -169,9 +169,9 @@ struct Inst {
   int64_t used = 0, peak = 0;
   double busy_time = 0;
   bool switch_pending = false;
-  // idle-while-runnable: the current idle period began at
-  // idle_t (last job end) when the cluster's zero-live measure was idle_z
-  double idle_t = 0, idle_z = 0, idle_rb = 0;
+  // idle-while-runnable: while idle with a request waiting
+  // in a queue, the open interval started at irs
+  double irs = 0, idle_rb = 0;
   int role0 = DECODE;
   // inter-pair leveling: KV of migrated requests still held as the source of
   // in-flight transfers, released at the first boundary >= lvl_until (§6b)
@@ -197,9 +197,8 @@ struct Sim {
   int64_t n_events = 0, n_steps = 0, n_prefills = 0, n_moves = 0, n_preempt = 0, n_evict = 0;
   int64_t tokens_total = 0, tokens_window = 0, prefill_tokens = 0, mirror_tokens = 0;
   double now = 0;
-  // queue depth (requests waiting in prefill queues) and Z(t) = time in
-  // [warmup, t] with none waiting (idle-while-runnable, SEMANTICS §7)
-  double zero_since = 0, z_acc = 0;
+  // queue depth (requests waiting in prefill queues; idle-while-runnable
+  // intervals of idle instances open / close with it, SEMANTICS §7)
   int64_t qdepth = 0, qd_max = 0;
   double qd_area = 0, qd_tprev = 0;
   // detail runs: every TBT sample of a measured request (pooled percentiles)
@@ -277,9 +276,15 @@ struct Sim {
   void qd_change(int64_t delta) {
     qd_area = qd_area + (double)qdepth * (now - qd_tprev);
     qd_tprev = now;
-    if (qdepth == 0 && delta > 0) z_acc = z_acc + (clip(now) - clip(zero_since));
+    const bool opens = qdepth == 0 && delta > 0;
     qdepth += delta;
-    if (qdepth == 0) zero_since = now;
+    const bool closes = qdepth == 0;
+    if (opens || closes)
+      for (auto& x : I)
+        if (x.job == NONE) {
+          if (opens) x.irs = now;
+          else x.idle_rb = x.idle_rb + (clip(now) - clip(x.irs));
+        }
     if (qdepth > qd_max) qd_max = qdepth;
   }
   void push_back(int q, int rid) { Q[q].push_back(rid); qtokens[q] += R[rid].qlen; qd_change(1); }
@@ -292,12 +297,9 @@ struct Sim {
   // ---- idle while runnable
   double clip(double t) const { return t > P.warmup_s ? t : P.warmup_s; }
   // Z(t): measure of [warmup, t] with no live request (t >= every change so far)
-  double zeta(double t) const { return qdepth == 0 ? z_acc + (clip(t) - clip(zero_since)) : z_acc; }
-  // a job starts on x at t: close x's idle period
+  // a job starts on x at t: close x's open idle-while-runnable interval
   void job_begin(Inst& X, double t) {
-    const double a = clip(t) - clip(X.idle_t);
-    const double b = zeta(t) - X.idle_z;
-    X.idle_rb = X.idle_rb + (a - b);
+    if (qdepth > 0) X.idle_rb = X.idle_rb + (clip(t) - clip(X.irs));
   }
 
   // token emission at time t (first token, recompute token or decode token)
@@ -319,11 +321,11 @@ struct Sim {
   }
   void finish_req(Req& r, double t) { r.done = true; r.done_t = t; }
 
-  // a job ends on x at t: busy time, and x's idle period (if any) starts here
+  // a job ends on x at t: busy time; with a request waiting, x's
+  // idle-while-runnable interval opens here
   void account_job(Inst& x, double t) {
     if (x.job_start >= P.warmup_s) x.busy_time += t - x.job_start;
-    x.idle_t = t;
-    x.idle_z = zeta(t);
+    if (qdepth > 0) x.irs = t;
   }
 
   // ---- memory helpers (§5)
@@ -1288,9 +1290,10 @@ int64_t nearest_rank(int64_t n, int pct) { return (pct * n + 99) / 100 - 1; }
 void summarize(Sim& S, kvsim_point_summary* out, kvsim_request_record* recs, kvsim_instance_record* inst) {
   const kvsim_point_desc& p = S.P;
   std::memset(out, 0, sizeof(*out));
-  // instances idle at the end: their idle period runs to the makespan
+  // instances idle at the end while requests wait (only a failed point):
+  // their open interval closes at the makespan
   for (auto& x : S.I)
-    if (x.job == NONE) S.job_begin(x, S.now);
+    if (x.job == NONE && S.qdepth > 0) x.idle_rb = x.idle_rb + (S.clip(S.now) - S.clip(x.irs));
   if (inst) {
     for (int i = 0; i < S.n; ++i)
       inst[i] = kvsim_instance_record{S.I[i].busy_time, S.I[i].idle_rb, S.I[i].peak, S.I[i].role0, 0};

@@ -178,12 +178,12 @@ struct Sim {
   double L_lvl_until;
   int32_t G_mode, G_cnt;
   int64_t tick;
-  // idle while runnable: this lane's instance has been idle
-  // since L_idle_t, when the zero-queue measure was L_idle_z
-  double L_idle_t, L_idle_z, L_idle_rb;
-  // uniform: queue depth (waiting requests) and its zero measure Z since the warm-up
+  // idle while runnable: while this lane's instance is idle
+  // and a request waits in a queue, the open interval started at L_irs
+  double L_irs, L_idle_rb;
+  // uniform: queue depth (waiting requests) and its time integral
   int64_t qdepth, qd_max;
-  double zero_since, z_acc, qd_area, qd_tprev;
+  double qd_area, qd_tprev;
 
   // per-slot arena offsets, computed once (the accessors below run on every
   // arena access; recomputing slot * capacity from the parameter block each
@@ -302,13 +302,18 @@ struct Sim {
 
   // ------------------------------------------------------------- queues
   // queue depth series: area += depth * (now - previous change)
-  // (also the zero-queue measure Z used by idle_runnable, SEMANTICS §7)
+  // (and the idle-while-runnable intervals of idle instances, SEMANTICS §7:
+  // they open when the queue becomes non-empty and close when it empties)
   KV_DEV void qd_change(int64_t delta) {
     qd_area = kadd(qd_area, kmul((double)qdepth, ksub(now, qd_tprev)));
     qd_tprev = now;
-    if (qdepth == 0 && delta > 0) z_acc = kadd(z_acc, ksub(clip(now), clip(zero_since)));
+    const bool opens = qdepth == 0 && delta > 0;
     qdepth += delta;
-    if (qdepth == 0) zero_since = now;
+    const bool closes = qdepth == 0;
+    if ((opens || closes) && lane < n && L_job == JOB_NONE) {
+      if (opens) L_irs = now;
+      else L_idle_rb = kadd(L_idle_rb, ksub(clip(now), clip(L_irs)));
+    }
     if (qdepth > qd_max) qd_max = qdepth;
   }
   KV_DEV void q_push_back(int q, int32_t rid, int64_t len) {
@@ -425,9 +430,9 @@ struct Sim {
     L_lvl_until = 0.0;
     G_mode = G_cnt = 0;
     tick = 1;
-    L_idle_t = L_idle_z = L_idle_rb = 0.0;
+    L_irs = L_idle_rb = 0.0;
     qdepth = qd_max = 0;
-    zero_since = z_acc = qd_area = qd_tprev = 0.0;
+    qd_area = qd_tprev = 0.0;
     // directed links (splitwise; AcceLLM EXT)
     if (policy == KVSIM_POLICY_SPLITWISE || EXT)
       for (int i = lane; i < n * n; i += 32) link_()[i] = 0.0;
@@ -514,25 +519,17 @@ struct Sim {
   }
   // ---- idle while runnable (SEMANTICS §7)
   KV_DEV double clip(double t) const { return t > PC.warmup ? t : PC.warmup; }
-  // Z(t): measure of [warm-up, t] with no request waiting in a prefill queue
-  KV_DEV double zeta(double t) const { return qdepth == 0 ? kadd(z_acc, ksub(clip(t), clip(zero_since))) : z_acc; }
-  // a job starts on x at t: close x's idle period
+  // a job starts on x at t: close x's open idle-while-runnable interval
   KV_DEV void job_begin(int x, double t) {
-    const double z = zeta(t);
-    if (own(x)) {
-      const double a = ksub(clip(t), clip(L_idle_t));
-      const double b = ksub(z, L_idle_z);
-      L_idle_rb = kadd(L_idle_rb, ksub(a, b));
-    }
+    if (own(x) && qdepth > 0) L_idle_rb = kadd(L_idle_rb, ksub(clip(t), clip(L_irs)));
   }
-  // a job ends on x at t: busy time; x's idle period (if any) starts here
+  // a job ends on x at t: busy time; with a request waiting, x's
+  // idle-while-runnable interval opens here
   KV_DEV void account_job(int x, double t) {
     double js = get(L_job_start, x);
-    const double z = zeta(t);
     if (own(x)) {
       if (js >= PC.warmup) L_busy_time = kadd(L_busy_time, ksub(t, js));
-      L_idle_t = t;
-      L_idle_z = z;
+      if (qdepth > 0) L_irs = t;
     }
   }
 
@@ -2730,9 +2727,9 @@ struct Sim {
       s.n_timer_ticks = ct.n_ticks;
       s.n_mode_switches = ct.n_modes;
       const int64_t peak = simt::warp_max(lane < n ? L_peak : (int64_t)0);
-      // instances idle at the end: their idle period runs to the makespan
-      for (int x = 0; x < n; ++x)
-        if (get(L_job, x) == JOB_NONE) job_begin(x, t_last);
+      // instances idle at the end while requests wait (only a failed point):
+      // their open interval closes at the makespan
+      if (qdepth > 0 && lane < n && L_job == JOB_NONE) L_idle_rb = kadd(L_idle_rb, ksub(clip(t_last), clip(L_irs)));
       double busy = 0.0, irb = 0.0;
       for (int x = 0; x < n; ++x) {
         busy = kadd(busy, get(L_busy_time, x));
