@@ -65,6 +65,7 @@ inline ArenaGeom size_arena(const kvsim_point_desc* pts, size_t n, const std::ve
     // entries <= decode steps + individual gaps, each <= the TBT samples N (dmax - 1)
     if (detail) g.Tcap = std::max<int64_t>(g.Tcap, 2 * N * std::max<int64_t>(dmax - 1, 0) + 64);
   }
+  g.Bcap = (g.Bcap + 3) & ~(int64_t)3;  // 16-byte vector access of the batch SoA (flush_slow)
   return g;
 }
 

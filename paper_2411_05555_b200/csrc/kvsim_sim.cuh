@@ -995,26 +995,40 @@ struct Sim {
     if (get(L_dj, x) == 0) return;
     flush_slow(x);
   }
+  // Vectorised SoA pass: each lane takes 4 consecutive members per round
+  // (one 16-byte load of their remaining-token words, two of their TBT
+  // maxima; Bcap is a multiple of 4 and the arrays 16-byte aligned, so the
+  // slots past B in the last vector are unused and written back unchanged).
   KV_DEV_NOINLINE void flush_slow(int x) {
     const int32_t j = get(L_dj, x);
     const double e1 = get(L_de1, x), pe = get(L_dpe, x), G = get(L_dG, x);
     const int32_t B = get(L_nb, x);
     int32_t* rem_a = b_rem(x);
     double* tbt_a = b_tbt(x);
-    for (int32_t q = lane; q < B; q += 32) {
-      const int32_t rf = rem_a[q];
-      const double tb = tbt_a[q];
-      double g1;
-      if (kFeat && (rf & kFirst)) {  // first token at the first deferred step end
-        c_first()[b_rid(x)[q]] = e1;
-        g1 = G;
-      } else {
-        const double last = (rf & kJoin) ? c_last()[b_rid(x)[q]] : pe;
-        g1 = ksub(e1, last);
-        if (G > g1) g1 = G;
+    for (int32_t q0 = 4 * lane; q0 < B; q0 += 128) {
+      kv_int4 r4 = *reinterpret_cast<const kv_int4*>(rem_a + q0);
+      kv_double2 t01 = *reinterpret_cast<const kv_double2*>(tbt_a + q0);
+      kv_double2 t23 = *reinterpret_cast<const kv_double2*>(tbt_a + q0 + 2);
+      int32_t rf[4] = {r4.x, r4.y, r4.z, r4.w};
+      double tb[4] = {t01.x, t01.y, t23.x, t23.y};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (q0 + k >= B) break;
+        double g1;
+        if (kFeat && (rf[k] & kFirst)) {  // first token at the first deferred step end
+          c_first()[b_rid(x)[q0 + k]] = e1;
+          g1 = G;
+        } else {
+          const double last = (rf[k] & kJoin) ? c_last()[b_rid(x)[q0 + k]] : pe;
+          g1 = ksub(e1, last);
+          if (G > g1) g1 = G;
+        }
+        rf[k] = ((rf[k] & kRemMask) - j) | (rf[k] & kCopy);
+        if (g1 > tb[k]) tb[k] = g1;
       }
-      rem_a[q] = ((rf & kRemMask) - j) | (rf & kCopy);
-      if (g1 > tb) tbt_a[q] = g1;
+      *reinterpret_cast<kv_int4*>(rem_a + q0) = kv_int4{rf[0], rf[1], rf[2], rf[3]};
+      *reinterpret_cast<kv_double2*>(tbt_a + q0) = kv_double2{tb[0], tb[1]};
+      *reinterpret_cast<kv_double2*>(tbt_a + q0 + 2) = kv_double2{tb[2], tb[3]};
     }
     simt::sync();
     if (own(x)) { L_dj = 0; L_dG = 0.0; }

@@ -265,3 +265,13 @@ KV_DEV T warp_incl_scan(T v) {
 }
 KV_DEV unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 }  // namespace simt
+
+// 16-byte vector types for the vectorised SoA passes (CUDA's int4 / double2
+// on the device; plain aligned structs for the host emulator)
+#if defined(KVSIM_EMU)
+struct alignas(16) kv_int4 { int32_t x, y, z, w; };
+struct alignas(16) kv_double2 { double x, y; };
+#else
+typedef int4 kv_int4;
+typedef double2 kv_double2;
+#endif
