@@ -1,4 +1,4 @@
-"""Attribute an ncu source-page capture of kvsim_sweep_kernel<2> to kvsim_sim.cuh
+"""Attribute an ncu source-page capture of kvsim_sweep_kernel<MINB[, FULL]> to kvsim_sim.cuh
 functions (instructions executed, warp-stall samples, no_instruction stalls).
 
   ncu -i REPORT --page source --csv --print-source sass > sass.csv
@@ -13,8 +13,9 @@ import collections, csv, re, sys
 
 def main(sass_csv, dis_txt, sim_cuh):
     rows = list(csv.reader(open(sass_csv)))
-    minb = re.search(r"kvsim_sweep_kernel<\(int\)(\d+)>", rows[0][1]).group(1)
-    tag = f"ILi{minb}EE"
+    m = re.search(r"kvsim_sweep_kernel<\(int\)(\d+)(?:, \(bool\)(\d))?>", rows[0][1])
+    minb, full = m.group(1), m.group(2)
+    tag = f"ILi{minb}EE" if full is None else f"ILi{minb}ELb{full}EE"
     dis = open(dis_txt).read().split("\n")
     start = [i for i, l in enumerate(dis) if l.startswith(".text._Z18kvsim_sweep_kernel" + tag)][0]
     off2src, cur = {}, None
