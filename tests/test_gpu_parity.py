@@ -245,3 +245,17 @@ def test_rebalance_exhaustive_gpu(sim):
         assert after[0] <= before[0] and after[1] <= before[1]
         if prompts == [1000, 1000, 100, 100]:
             assert after == exhaustive_best(prompts) == (0, 0)
+
+
+def test_lean_and_full_kernels_in_one_run(sim):
+    """Without event logs, plain points run in the lean kernel and points
+    with AcceLLM extensions / SPEC variants in the full kernel (two launches
+    of one run): every summary still equals the oracle's."""
+    from configs import random_ext
+    pts = [random_small(3000 + i, max_req=200) for i in range(60)] + [random_ext(900 + i) for i in range(20)]
+    summ = sim.run(pts)
+    assert sim.last_launches() == 2
+    for p, s in zip(pts, summ):
+        ref = run_oracle(p, ev_cap=0, recs=False)
+        assert not diff_results(ref, Result(s, None, None), events=False), (p.policy, p.first_token_decode,
+                                                                           p.splitwise_cobatch, p.accellm_flags)
