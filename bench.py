@@ -248,7 +248,13 @@ def main():
     n_gpu = max(args.gpus, world)
     import torch
     import paper_2411_05555_b200 as pkg
-    sims = [pkg.KvSim(d) for d in range(n_gpu)]
+    # KVSIM_VIRTUAL_GPUS=1 maps the N contexts onto the visible devices
+    # round-robin: a functional check of the N>1 path on a smaller box, never
+    # a scaling number
+    ndev = torch.cuda.device_count()
+    if n_gpu > ndev and os.environ.get("KVSIM_VIRTUAL_GPUS") != "1":
+        raise SystemExit(f"--gpus {n_gpu} but only {ndev} visible device(s)")
+    sims = [pkg.KvSim(d % max(ndev, 1)) for d in range(n_gpu)]
     sim = sims[0]
     pts = config4_points(0, args.rates, args.requests)
     n = len(pts)
