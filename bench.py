@@ -13,11 +13,12 @@ index (9,996 points, ~1e8 simulated requests). A step = one full sweep.
          threads over a bounded sample of the same points
 
 Multi-GPU (--gpus N, or torchrun with N ranks): ONE process drives all N
-GPUs with one host thread each (kvsim_gpu_run_multi: guided chunks over the
-cost-sorted points, summaries gathered in host memory, no collective, SURVEY
-§8e); the same config-4 sweep is split over the N GPUs (strong scaling).
-Under torchrun, ranks other than 0 exit without work. Every run also times a
-BASELINE config-5 subsample (`config5_slice`) on the same GPUs.
+GPUs with one host thread each (kvsim_gpu_run_multi: points dealt by cost,
+summaries gathered in host memory, no collective). `value` is
+weak scaling: N config-4 grids with disjoint seeds in one sweep over the N
+GPUs. Under torchrun, ranks other than 0 exit without work. Every run also
+times a fixed BASELINE config-5 subsample (`config5_slice`, strong scaling:
+the same 9,014 points on 1 or N GPUs).
 """
 from __future__ import annotations
 
@@ -256,9 +257,10 @@ def main():
         raise SystemExit(f"--gpus {n_gpu} but only {ndev} visible device(s)")
     sims = [pkg.KvSim(d % max(ndev, 1)) for d in range(n_gpu)]
     sim = sims[0]
-    pts = config4_points(0, args.rates, args.requests)
+    # weak scaling: N copies of the config-4 grid with disjoint seeds, one
+    # sweep sharded over the N GPUs by kvsim_gpu_run_multi
+    pts = [p for r in range(n_gpu) for p in config4_points(r * 1_000_000, args.rates, args.requests)]
     n = len(pts)
-    bad_reqs = 0
     with ClockSampler(0) as clk:
         if n_gpu == 1:
             # device-resident: points and summaries in HBM (torch owns the memory)
@@ -357,11 +359,12 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": "simulated requests/s", "n_gpus": n_gpu,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: requests generated on device by the seeded counter-based RNG (SEMANTICS §2)",
-        "config": {"workload": workload, "points": n, "requests_per_step": reqs,
-                   "parallelism": f"points sharded over {n_gpu} GPU(s) by one process (host thread per GPU, "
-                                  f"guided chunks, no collective), warp per point",
+        "config": {"workload": workload + (f", x{n_gpu} grids with disjoint seeds (weak scaling)" if n_gpu > 1 else ""),
+                   "points": n, "requests_per_step": reqs,
+                   "parallelism": f"one sweep sharded over {n_gpu} GPU(s) by one process (host thread per GPU, "
+                                  f"LPT-dealt points, no collective), warp per point",
                    "l2": "arena working set >> 126 MB L2 and rewritten every step (no flush needed)"},
         "gpu_launches": launches,
         "events_per_step": events,

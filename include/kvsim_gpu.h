@@ -252,7 +252,7 @@ int kvsim_gpu_run_ex(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
  * chunks >= min_chunk) and runs each through kvsim_gpu_run_ex; summaries
  * land at their point index, so `out` is byte-identical for any number of
  * devices. No collective: results are gathered in host memory.
- * min_chunk 0 = automatic: with at most 4 waves of resident warps per device
+ * min_chunk 0 = automatic: with at most 16 waves of resident warps per device
  * the points are dealt once (greedy LPT on the cost estimate, one launch per
  * device), else guided chunks of >= 2 waves. Generated traces only
  * (trace_index < 0). stats is nullable. */

@@ -11,8 +11,8 @@
 // remaining / (2 G)) points, so the expensive points go out first in large
 // chunks and the tail of the sweep is cut into small ones. Every chunk is
 // one kernel launch whose own tail leaves warps idle, so min_chunk should
-// cover a few waves of resident warps (kvsim_gpu_run_multi: 2 x slots,
-// capped at n / G so every device gets work).
+// cover a few waves of resident warps (kvsim_gpu_run_multi: 2 x slots);
+// up to 16 waves per device the points are dealt once instead (make_static).
 #pragma once
 #include <stdint.h>
 
@@ -43,7 +43,7 @@ struct ShardPlan {
   std::vector<std::vector<int64_t>> fixed;
 };
 
-// Few points per device (below a few waves of resident warps): one launch
+// Few points per device (up to 16 waves of resident warps): one launch
 // per device, points dealt by greedy LPT on the cost estimate (most
 // expensive first, each to the least-loaded device), so launches end
 // together instead of stacking per-launch tails.

@@ -503,10 +503,10 @@ int kvsim_gpu_run_multi(kvsim_gpu_ctx* const* ctxs, int n_ctx, const kvsim_point
     if (pts[i].trace_index >= 0) return set_err(err, err_len, KVSIM_E_INVALID, "multi-device runs use generated traces");
   const size_t slots = (size_t)ctxs[0]->sms * ctxs[0]->blocks_per_sm * kWarpsPerBlock;
   // one device: a single launch (the kernel orders its points LPT itself)
-  const bool dynamic = min_chunk != 0 || (n_ctx > 1 && n > 4 * slots * (size_t)n_ctx);
+  const bool dynamic = min_chunk != 0 || (n_ctx > 1 && n > 16 * slots * (size_t)n_ctx);
   if (min_chunk == 0) min_chunk = 2 * slots;  // dynamic default: two waves of resident warps
   kvsim_host::ShardPlan plan = kvsim_host::make_plan(pts, n, n_ctx, min_chunk);
-  if (!dynamic) kvsim_host::make_static(plan, pts);  // few points per device: one LPT-balanced launch each
+  if (!dynamic) kvsim_host::make_static(plan, pts);  // up to 16 waves per device: one LPT-balanced launch each
   std::vector<cudaEvent_t> ev0(n_ctx, nullptr), ev1(n_ctx, nullptr);
   std::vector<int64_t> launches(n_ctx, 0);
   std::vector<char> started(n_ctx, 0);
