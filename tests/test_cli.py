@@ -108,6 +108,17 @@ def test_run_records_match_oracle(kvsim, tmp_path):
     rows = list(csv.DictReader(open(out / "summary.csv")))
     assert float(rows[0]["jct_mean"]) == ref.summary.jct_mean
     assert (out / "events.jsonl").stat().st_size > 0
+    # `run` reports the full MetricsReport: pooled TBT
+    # percentiles (detail run), queue wait per request, per-instance records
+    det = run_oracle(p, ev_cap=0, detail=True)
+    assert got["summary"]["tbt_p50"] == det.summary.tbt_p50 and got["summary"]["tbt_p95"] == det.summary.tbt_p95
+    assert got["summary"]["ttft_queue_mean"] == det.summary.ttft_queue_mean
+    for q, rr in zip(got["requests"], det.recs):
+        assert q["queue_wait_s"] == rr.prefill_start_s - rr.arrival_s
+    inst = got["instances_detail"]
+    assert len(inst) == 4
+    for x, ir in zip(inst, det.inst):
+        assert x["busy_s"] == ir.busy_s and x["idle_runnable_s"] == ir.idle_runnable_s
     meta = json.load(open(out / "meta.json"))
     assert meta["config"]["seeds"] == [3] and len(meta["config_hash"]) == 16
 
