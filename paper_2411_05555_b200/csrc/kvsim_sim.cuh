@@ -15,6 +15,8 @@
 // batches). The code compiles both for sm_100a and, with KVSIM_EMU, for the
 // host SIMT emulator used by the CPU test-suite.
 #pragma once
+#include <new>
+
 #include "kvsim_gpu.h"
 #include "kvsim_math.cuh"
 #include "kvsim_simt.cuh"
@@ -127,7 +129,23 @@ struct SweepArgs {
   double* link;            // [slot][Imax][Imax] directed link busy-until
   unsigned long long* next_point;
 };
-
+// Shared memory of a sweep block (device builds):
+//   dynamic: [kWarpsPerBlock x WarpScratch][kWarpsPerBlock * 32 x Sim]
+//            (one Sim object per lane, AoS; 472 B = 118 words, so a warp's
+//            same-field accesses are conflict-free for 8-byte fields)
+//   static:  kvsim_args_smem, the block's copy of the kernel parameters, so
+//            arena base pointers are LDS of a fixed address instead of
+//            generic loads from the parameter space.
+// -DKVSIM_SIM_STACK keeps the round-1 layout (Sim on the per-thread stack,
+// i.e. local memory; parameters through a pointer) for A/B runs.
+constexpr int kWarpsPerBlock = 4;
+#if !defined(KVSIM_EMU) && !defined(KVSIM_SIM_STACK)
+#define KVSIM_SIM_SMEM 1
+__shared__ SweepArgs kvsim_args_smem;
+#define AR kvsim_args_smem
+#else
+#define AR (*A)
+#endif
 #define PC (ws()->pc)
 // One specialisation per policy: every `policy == ...` test folds at compile
 // time, so a warp only ever executes (and caches) its own policy's code.
@@ -217,35 +235,35 @@ struct Sim {
 #endif
     return p;
   }
-  KV_DEV double* c_arr() const { return gp(A->c_arr + o_c); }
-  KV_DEV double* c_last() const { return gp(A->c_last + o_c); }
-  KV_DEV double* c_tbt() const { return gp(A->c_tbt + o_c); }
-  KV_DEV double* c_fresh() const { return gp(A->c_fresh + o_c); }
-  KV_DEV double* c_first() const { return gp(A->c_first + o_c); }
-  KV_DEV double* c_done() const { return gp(A->c_done + o_c); }
-  KV_DEV double* c_qs() const { return gp(A->c_qs + o_c); }
-  KV_DEV int32_t* c_pl() const { return gp(A->c_pl + o_c); }
-  KV_DEV int32_t* c_dl() const { return gp(A->c_dl + o_c); }
-  KV_DEV int32_t* c_qlen() const { return gp(A->c_qlen + o_c); }
-  KV_DEV int32_t* c_em() const { return gp(A->c_em + o_c); }
-  KV_DEV int32_t* c_cpy() const { return gp(A->c_cpy + o_c); }
-  KV_DEV int32_t* c_nmv() const { return gp(A->c_nmv + o_c); }
-  KV_DEV int32_t* c_npre() const { return gp(A->c_npre + o_c); }
+  KV_DEV double* c_arr() const { return gp(AR.c_arr + o_c); }
+  KV_DEV double* c_last() const { return gp(AR.c_last + o_c); }
+  KV_DEV double* c_tbt() const { return gp(AR.c_tbt + o_c); }
+  KV_DEV double* c_fresh() const { return gp(AR.c_fresh + o_c); }
+  KV_DEV double* c_first() const { return gp(AR.c_first + o_c); }
+  KV_DEV double* c_done() const { return gp(AR.c_done + o_c); }
+  KV_DEV double* c_qs() const { return gp(AR.c_qs + o_c); }
+  KV_DEV int32_t* c_pl() const { return gp(AR.c_pl + o_c); }
+  KV_DEV int32_t* c_dl() const { return gp(AR.c_dl + o_c); }
+  KV_DEV int32_t* c_qlen() const { return gp(AR.c_qlen + o_c); }
+  KV_DEV int32_t* c_em() const { return gp(AR.c_em + o_c); }
+  KV_DEV int32_t* c_cpy() const { return gp(AR.c_cpy + o_c); }
+  KV_DEV int32_t* c_nmv() const { return gp(AR.c_nmv + o_c); }
+  KV_DEV int32_t* c_npre() const { return gp(AR.c_npre + o_c); }
   KV_DEV int64_t bofs(int x) const { return o_b + x * Bcap_; }
   KV_DEV int64_t jofs(int x) const { return o_j + x * Jcap_; }
 
   // ------------------------------------------------------------ accessors
-  KV_DEV int32_t* b_rid(int x) { return gp(A->b_rid + bofs(x)); }
-  KV_DEV int32_t* b_rem(int x) { return gp(A->b_rem + bofs(x)); }
-  KV_DEV int32_t* b_kvb(int x) { return gp(A->b_kvb + bofs(x)); }
-  KV_DEV double* b_tbt(int x) { return gp(A->b_tbt + bofs(x)); }
-  KV_DEV int32_t* i_rid(int x) { return gp(A->i_rid + bofs(x)); }
-  KV_DEV double* i_ready(int x) { return gp(A->i_ready + bofs(x)); }
-  KV_DEV int32_t* j_rid(int x) { return gp(A->j_rid + jofs(x)); }
-  KV_DEV int32_t* j_dst(int x) { return gp(A->j_dst + jofs(x)); }
-  KV_DEV int32_t* ring(int q) { return gp(A->q_rid + o_q + q * Ncap_); }
-  KV_DEV double* link_() { return gp(A->link + (int64_t)slot * A->Imax * A->Imax); }
-  KV_DEV kvsim_event_record* evlog() const { return A->ev ? A->ev + point * A->ev_cap : nullptr; }
+  KV_DEV int32_t* b_rid(int x) { return gp(AR.b_rid + bofs(x)); }
+  KV_DEV int32_t* b_rem(int x) { return gp(AR.b_rem + bofs(x)); }
+  KV_DEV int32_t* b_kvb(int x) { return gp(AR.b_kvb + bofs(x)); }
+  KV_DEV double* b_tbt(int x) { return gp(AR.b_tbt + bofs(x)); }
+  KV_DEV int32_t* i_rid(int x) { return gp(AR.i_rid + bofs(x)); }
+  KV_DEV double* i_ready(int x) { return gp(AR.i_ready + bofs(x)); }
+  KV_DEV int32_t* j_rid(int x) { return gp(AR.j_rid + jofs(x)); }
+  KV_DEV int32_t* j_dst(int x) { return gp(AR.j_dst + jofs(x)); }
+  KV_DEV int32_t* ring(int q) { return gp(AR.q_rid + o_q + q * Ncap_); }
+  KV_DEV double* link_() { return gp(AR.link + (int64_t)slot * AR.Imax * AR.Imax); }
+  KV_DEV kvsim_event_record* evlog() const { return AR.ev ? AR.ev + point * AR.ev_cap : nullptr; }
 
   template <class T>
   KV_DEV T get(T v, int x) { return simt::shfl(v, x); }
@@ -276,7 +294,7 @@ struct Sim {
   }
 
   KV_DEV void put_event(int64_t k, double t, int kind, int inst, int a, int b, int64_t c) {
-    if (k < A->ev_cap) {
+    if (k < AR.ev_cap) {
       kvsim_event_record r;
       r.t = t; r.kind = kind; r.inst = inst; r.a = a; r.b = b; r.c = c;
       evlog()[k] = r;
@@ -352,7 +370,7 @@ struct Sim {
   // ------------------------------------------------------------ point init
   KV_DEV bool init_point(int64_t p) {
     point = p;
-    const kvsim_point_desc& d = A->pts[p];
+    const kvsim_point_desc& d = AR.pts[p];
     PointConst pc;
     pc.f = make_perf(d);
     n = d.num_instances;
@@ -382,21 +400,21 @@ struct Sim {
       pc.dual_budget = (int64_t)kmul(df, (double)pc.f.cap);
     }
     status = KVSIM_OK;
-    const int64_t nreq = d.num_requests < A->Ncap ? d.num_requests : A->Ncap;
+    const int64_t nreq = d.num_requests < AR.Ncap ? d.num_requests : AR.Ncap;
     int32_t evd = pc.dmax;
     if (d.trace_index >= 0) {
-      const int64_t off = A->tr_off[d.trace_index];
-      pc.tr_arr = A->tr_arr + off; pc.tr_pl = A->tr_pl + off; pc.tr_dl = A->tr_dl + off;
-      const int64_t tn = A->tr_n[d.trace_index];
+      const int64_t off = AR.tr_off[d.trace_index];
+      pc.tr_arr = AR.tr_arr + off; pc.tr_pl = AR.tr_pl + off; pc.tr_dl = AR.tr_dl + off;
+      const int64_t tn = AR.tr_n[d.trace_index];
       pc.n_limit = tn < nreq ? tn : nreq;
-      evd = A->tr_dmax[d.trace_index];
+      evd = AR.tr_dmax[d.trace_index];
     } else {
       pc.tr_arr = nullptr; pc.tr_pl = nullptr; pc.tr_dl = nullptr;
       pc.n_limit = pc.rate > 0.0 ? nreq : 0;
     }
     pc.event_budget = 4 * pc.n_limit * ((int64_t)(evd > 1 ? evd : 1) + 2) + 4096;
     // validity (perfmodel validate())
-    if (n < 1 || n > kMaxInst || n > A->Imax || d.policy != POL) status = KVSIM_E_INVALID;
+    if (n < 1 || n > kMaxInst || n > AR.Imax || d.policy != POL) status = KVSIM_E_INVALID;
     else if (!geometry_fits(d)) status = KVSIM_E_INVALID;
     else if (policy == KVSIM_POLICY_ACCELLM && (n & 1)) status = KVSIM_E_ODD_INSTANCES;
     else if (policy == KVSIM_POLICY_SPLITWISE && (n < 2 || n_prefill >= n)) status = KVSIM_E_INVALID;
@@ -448,8 +466,8 @@ struct Sim {
   // (kvsim_arena.hpp size_arena); a device-resident caller could pass points
   // that differ from its reservation, so this is re-checked per point
   KV_DEV_NOINLINE bool geometry_fits(const kvsim_point_desc& d) const {
-    if (d.num_requests < 0 || d.num_requests > A->Ncap) return false;
-    if (d.trace_index >= 0) return A->tr_off != nullptr;  // traces: sized by the host from the trace itself
+    if (d.num_requests < 0 || d.num_requests > AR.Ncap) return false;
+    if (d.trace_index >= 0) return AR.tr_off != nullptr;  // traces: sized by the host from the trace itself
     if (d.decode_max > kRemMask || d.prompt_max > kRemMask) return false;
     const int64_t N = d.num_requests;
     const int64_t pmin = d.prompt_min > 0 ? d.prompt_min : 1;
@@ -457,7 +475,7 @@ struct Sim {
     const int64_t cap = f.fits ? f.cap : 0;
     const int64_t budget = d.prefill_token_budget > 0 ? d.prefill_token_budget : 8192;
     const int64_t nb = cap / pmin + 2, nj = budget / pmin + 1;
-    return (N < nb ? N : nb) <= A->Bcap && (N < nj ? N : nj) <= A->Jcap;
+    return (N < nb ? N : nb) <= AR.Bcap && (N < nj ? N : nj) <= AR.Jcap;
   }
 
   // arrival generator (SEMANTICS §2); uniform across lanes
@@ -512,9 +530,9 @@ struct Sim {
   // detail runs: one TBT entry (gap shared by cnt samples); divergent-safe
   KV_DEV void tbt_entry(double gap, int32_t cnt) {
     const int64_t k = simt::atomic_add_smem(&ws()->ct.t_n, (int64_t)1);
-    if (k < A->Tcap) {
-      gp(A->t_val + (int64_t)slot * A->Tcap)[k] = gap;
-      gp(A->t_cnt + (int64_t)slot * A->Tcap)[k] = cnt;
+    if (k < AR.Tcap) {
+      gp(AR.t_val + (int64_t)slot * AR.Tcap)[k] = gap;
+      gp(AR.t_cnt + (int64_t)slot * AR.Tcap)[k] = cnt;
     }
   }
   // ---- idle while runnable (SEMANTICS §7)
@@ -2716,7 +2734,7 @@ struct Sim {
       char* z = reinterpret_cast<char*>(&s);
       for (unsigned i = 0; i < sizeof(s); ++i) z[i] = 0;
     }
-    const kvsim_point_desc& d = A->pts[point];
+    const kvsim_point_desc& d = AR.pts[point];
     const double kNaN = as_f64(0x7ff8000000000000ull);
     const double kInf = as_f64(0x7ff0000000000000ull);
     s.status = status;
@@ -2755,14 +2773,14 @@ struct Sim {
         const double area = kadd(qd_area, kmul((double)qdepth, ksub(t_last, qd_tprev)));
         s.queue_depth_avg = t_last > 0.0 ? kdiv(area, t_last) : kNaN;
       }
-      if (A->inst != nullptr && lane < n) {
+      if (AR.inst != nullptr && lane < n) {
         kvsim_instance_record ir;
         ir.busy_s = L_busy_time;
         ir.idle_runnable_s = L_idle_rb;
         ir.peak_kv_tokens = L_peak;
         ir.initial_role = (policy == KVSIM_POLICY_SPLITWISE && lane < n_prefill) ? ROLE_PREFILL : ROLE_DECODE;
         ir.reserved = 0;
-        A->inst[point * KVSIM_MAX_INSTANCES + lane] = ir;
+        AR.inst[point * KVSIM_MAX_INSTANCES + lane] = ir;
       }
       s.peak_kv_tokens = peak;
       s.busy_s_total = busy;
@@ -2770,8 +2788,8 @@ struct Sim {
       s.link_prefill_gb = kdiv(kmul((double)ct.pf_tokens, PC.f.kvb), 1e9);
       s.link_mirror_gb = kdiv(kmul((double)ct.mir_tokens, PC.f.kvb), 1e9);
       // records (parity configs)
-      if (A->recs != nullptr) {
-        kvsim_request_record* R = A->recs + A->rec_off[point];
+      if (AR.recs != nullptr) {
+        kvsim_request_record* R = AR.recs + AR.rec_off[point];
         for (int64_t i = lane; i < N; i += 32) {
           const bool dn = c_em()[i] == c_dl()[i];
           kvsim_request_record r;
@@ -2868,9 +2886,9 @@ struct Sim {
       s.tbt_p50 = s.tbt_p95 = kNaN;
       if constexpr (DET) {
         const int64_t ne = ws()->ct.t_n;
-        if (n_tbt > 0 && ne <= A->Tcap && n_tbt < (int64_t)0xffffffffll) {
-          const double* tv = gp(A->t_val + (int64_t)slot * A->Tcap);
-          const int32_t* tc = gp(A->t_cnt + (int64_t)slot * A->Tcap);
+        if (n_tbt > 0 && ne <= AR.Tcap && n_tbt < (int64_t)0xffffffffll) {
+          const double* tv = gp(AR.t_val + (int64_t)slot * AR.Tcap);
+          const int32_t* tc = gp(AR.t_cnt + (int64_t)slot * AR.Tcap);
           int64_t wsum = 0;
           for (int64_t i = lane; i < ne; i += 32) wsum += tc[i];
           wsum = simt::warp_sum_nn(wsum);
@@ -2893,8 +2911,8 @@ struct Sim {
     }
     simt::sync();
     if (lane == 0) {
-      A->out[point] = s;
-      if (A->ev_count != nullptr) A->ev_count[point] = ws()->ct.ev_n;
+      AR.out[point] = s;
+      if (AR.ev_count != nullptr) AR.ev_count[point] = ws()->ct.ev_n;
     }
     simt::sync();
   }
@@ -2903,9 +2921,19 @@ struct Sim {
 // One point, simulated by the policy-specialised core.
 template <int P, bool LOG, bool EXT = false, bool DET = false>
 KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot, int64_t pt) {
+#if defined(KVSIM_SIM_SMEM)
+  // the lane's Sim object in dynamic shared memory after the warp scratch
+  // blocks (local memory held it in round 1: 568 B stack frame, ~2,200 LDL/STL)
+  using S = Sim<P, LOG, EXT, DET>;
+  S* sim = reinterpret_cast<S*>(kvsim_smem + sizeof(WarpScratch) * kWarpsPerBlock) + threadIdx.x;
+  new (sim) S(ap, w, slot);
+  if (sim->init_point(pt)) sim->run();
+  sim->finalize();
+#else
   Sim<P, LOG, EXT, DET> sim(ap, w, slot);
   if (sim.init_point(pt)) sim.run();
   sim.finalize();
+#endif
 }
 
 // Persistent warp loop: pull points from a global counter (policy-major LPT

@@ -26,9 +26,7 @@
 using kvsim_dev::SweepArgs;
 using kvsim_dev::WarpScratch;
 
-namespace {
-constexpr int kWarpsPerBlock = 4;
-}
+using kvsim_dev::kWarpsPerBlock;
 
 // ------------------------------------------------------------------ kernels
 // MINB = minimum resident blocks per SM requested from ptxas (register cap
@@ -40,8 +38,16 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(
   WarpScratch* scratch = reinterpret_cast<WarpScratch*>(kvsim_smem);
   const int w = threadIdx.x >> 5;
   const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+#if defined(KVSIM_SIM_SMEM)
+  // block-shared copy of the parameters (kvsim_sim.cuh: AR)
+  if (threadIdx.x == 0) kvsim_dev::kvsim_args_smem = a;
+  __syncthreads();
+  if (slot >= a.slots) return;
+  kvsim_dev::sweep_warp<FULL>(&kvsim_dev::kvsim_args_smem, &scratch[w], (int32_t)slot);
+#else
   if (slot >= a.slots) return;
   kvsim_dev::sweep_warp<FULL>(&a, &scratch[w], (int32_t)slot);
+#endif
 }
 
 __global__ void kvsim_perf_kernel(const kvsim_point_desc* pts, const int32_t* pidx, const int32_t* op,
@@ -145,12 +151,30 @@ namespace {
 
 using SweepFn = void (*)(SweepArgs);
 constexpr int kDefaultMinBlocks = 3;
-constexpr int kDefaultCarveout = 25;  // percent shared memory (KVSIM_CARVEOUT; -1 = driver default)
+// percent of the unified L1/shared array given to shared memory
+// (KVSIM_CARVEOUT; -1 = driver default): the Sim objects need ~213 KB per SM
+// at 3 blocks; with the round-1 stack layout 25% (more L1 for local memory)
+#if defined(KVSIM_SIM_SMEM)
+constexpr int kDefaultCarveout = 100;
+#else
+constexpr int kDefaultCarveout = 25;
+#endif
+// A/B builds (tools/build_variant.sh) may replace the second variant with
+// another occupancy (-DKVSIM_MINB_ALT=4) and alias the full kernel to the
+// lean one (-DKVSIM_LEAN_ONLY: plain sweeps only, a much faster build).
+#ifndef KVSIM_MINB_ALT
+#define KVSIM_MINB_ALT 2
+#endif
+#ifdef KVSIM_LEAN_ONLY
+constexpr bool kFullImage = false;
+#else
+constexpr bool kFullImage = true;
+#endif
 SweepFn sweep_variant(int minb, bool full) {
   // occupancy is not the limiter (instruction fetch is):
   // 2 vs 3 blocks/SM measured 5.91 vs 5.71 s on config 4, so two variants ship
-  if (full) return minb == 3 ? kvsim_sweep_kernel<3, true> : kvsim_sweep_kernel<2, true>;
-  return minb == 3 ? kvsim_sweep_kernel<3, false> : kvsim_sweep_kernel<2, false>;
+  if (full) return minb == 3 ? kvsim_sweep_kernel<3, kFullImage> : kvsim_sweep_kernel<KVSIM_MINB_ALT, kFullImage>;
+  return minb == 3 ? kvsim_sweep_kernel<3, false> : kvsim_sweep_kernel<KVSIM_MINB_ALT, false>;
 }
 
 // Stable partition of the launch order: points the lean kernel can run first
@@ -178,7 +202,18 @@ int set_err(char* err, size_t len, int code, const std::string& msg) {
                      std::string(#call) + ": " + cudaGetErrorString(_e));                     \
   } while (0)
 
+#if defined(KVSIM_SIM_SMEM)
+// dynamic shared memory per block: warp scratch + one Sim object per lane
+// (every specialisation has the same fields)
+constexpr size_t kSimBytes = sizeof(kvsim_dev::Sim<KVSIM_POLICY_ACCELLM, true, true, true>);
+static_assert(sizeof(kvsim_dev::Sim<KVSIM_POLICY_UNIFIED, false>) == kSimBytes &&
+                  sizeof(kvsim_dev::Sim<KVSIM_POLICY_SPLITWISE, false>) == kSimBytes &&
+                  sizeof(kvsim_dev::Sim<KVSIM_POLICY_ACCELLM, false>) == kSimBytes,
+              "Sim specialisations share one layout");
+size_t smem_bytes() { return sizeof(WarpScratch) * kWarpsPerBlock + kSimBytes * kWarpsPerBlock * 32; }
+#else
 size_t smem_bytes() { return sizeof(WarpScratch) * kWarpsPerBlock; }
+#endif
 
 // Choose the number of arena slots (= resident warps) and allocate the arena.
 int prepare_arena(kvsim_gpu_ctx* c, const kvsim_host::ArenaGeom& g, size_t n_pts, char* err, size_t err_len) {
@@ -289,7 +324,7 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   int minb = kDefaultMinBlocks;
   if (const char* e = std::getenv("KVSIM_MINB")) {
     minb = std::atoi(e);
-    if (minb != 2 && minb != 3)
+    if (minb != KVSIM_MINB_ALT && minb != 3)
       return set_err(err, err_len, KVSIM_E_INVALID, "KVSIM_MINB must be 2 or 3 (the shipped kernel variants)");
   }
   auto* c = new kvsim_gpu_ctx();
