@@ -139,6 +139,9 @@ struct SweepArgs {
 // -DKVSIM_SIM_STACK keeps the round-1 layout (Sim on the per-thread stack,
 // i.e. local memory; parameters through a pointer) for A/B runs.
 constexpr int kWarpsPerBlock = 4;
+#ifndef KVSIM_PAIR_PAR
+#define KVSIM_PAIR_PAR 1
+#endif
 #if !defined(KVSIM_EMU) && !defined(KVSIM_SIM_STACK)
 #define KVSIM_SIM_SMEM 1
 __shared__ SweepArgs kvsim_args_smem;
@@ -1098,6 +1101,209 @@ struct Sim {
     c.dj += 1;
     c.steps += 1;
   }
+#if KVSIM_PAIR_PAR
+  // ---- member-parallel AcceLLM pair chains
+  // The serial merged loop (KVSIM_PAIR_PAR=0) advances both members of a pair
+  // on the even lane, one step end at a time in (time, id) order, and stops at the first
+  // step end whose tests fail. A member's step times depend only on its own
+  // state; the members interact only through the stop tests (the KV slack of
+  // each member, which the partner's mirror lines also consume, the
+  // rebalance gaps, the event budget). Here each member runs its own chain on
+  // its own lane under member-local limits that imply those tests for any
+  // interleaving (a chain may always stop early: the event loop then handles
+  // the step end exactly):
+  //   KV slack / budget: both members take at most C steps, with C such that
+  //   C (B_a + m_b) <= cap - used_a, C (B_b + m_a) <= cap - used_b, 2C <= budget;
+  //   rebalance gap: a's gap grows by B_a - 1 per own step and only shrinks
+  //   with partner steps, so the own steps alone bound it.
+  // A pair's merged chain ends at the earlier of the two members' first
+  // untaken step ends; the member whose taken steps reach past the partner's
+  // is re-run with that bound (at most one of the two). (Emulator, config-4
+  // AcceLLM points: 2.3-2.8 re-runs and 9-10 pair chains per simulated
+  // request; the member-local bounds add ~5% handled step ends.)
+  struct PChain {
+    double e, js, busy, dG, de1, dpe, link, mfin;
+    int32_t k, tw;
+  };
+  template <bool DOLOG>
+  KV_DEV PChain pair_member_run(int32_t nmax, double tl, double comp, double mlat, int32_t m, int32_t B) {
+    PChain c;
+    c.e = L_busy_until; c.js = L_job_start; c.busy = L_busy_time;
+    c.dG = L_dG; c.de1 = L_de1; c.dpe = L_dpe; c.link = L_link; c.mfin = L_mirror_fin;
+    c.k = 0; c.tw = 0;
+    if (!(nmax > 0 && c.e < tl)) return c;
+    const double Wb = PC.f.W, kvb = PC.f.kvb, mden = PC.f.mem_den, mrcp = PC.f.mem_rcp, warmup = PC.warmup;
+    const int64_t skv0 = L_skv;
+    const double Bd = (double)B;
+    double Kd = (double)skv0;
+    double e = c.e, js = c.js, busy = c.busy, dG = c.dG, link = c.link;
+    int32_t k = 0, tw = 0;
+    {  // first chained step: gap against the previous step end (lean_step)
+      const double prev = L_prev_end;
+      const double st = ksub(e, js);
+      if (js >= warmup) busy = kadd(busy, st);
+      if (e >= warmup) tw += 1;
+      if (L_dj == 0) { c.de1 = e; c.dpe = prev; }
+      else { const double g = js == prev ? st : ksub(e, prev); if (g > dG) dG = g; }
+      if (m > 0) {
+        link = kadd(e > link ? e : link, mlat);
+        if constexpr (DOLOG) log_one(e, KVSIM_EV_TRANSFER, lane, lane ^ 1, 1, m);
+      }
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+      Kd = kadd(Kd, Bd);
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + B);
+      js = e;
+      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      k = 1;
+    }
+    // steady state: js == prev, one difference is the busy increment and the gap
+    while (k < nmax && e < tl) {
+      const double st = ksub(e, js);
+      if (js >= warmup) busy = kadd(busy, st);
+      if (st > dG) dG = st;
+      if (e >= warmup) tw += 1;
+      if (m > 0) {
+        link = kadd(e > link ? e : link, mlat);
+        if constexpr (DOLOG) log_one(e, KVSIM_EV_TRANSFER, lane, lane ^ 1, 1, m);
+      }
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+      Kd = kadd(Kd, Bd);
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k + 1) * B);
+      js = e;
+      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      k += 1;
+    }
+    c.e = e; c.js = js; c.busy = busy; c.dG = dG; c.link = link;
+    if (m > 0) c.mfin = link;
+    c.k = k; c.tw = tw;
+    return c;
+  }
+  // pc: this lane's pair is a chain candidate (pair-uniform); accumulates the
+  // lane's counters.
+  KV_DEV void pair_par(bool pc, double ht, int32_t hk, int64_t budget, int64_t& steps, int64_t& tok, int64_t& tw,
+                       int64_t& mir, double& tmax) {
+    const double kInf = as_f64(0x7ff0000000000000ull);
+    const int y = lane ^ 1;
+    const bool isb = (lane & 1) != 0;
+    // partner state (all lanes stay converged through the shuffles; lanes of
+    // other pairs run empty chains)
+    const int32_t p_job = simt::shfl(L_job, y), p_nb = simt::shfl(L_nb, y), p_ni = simt::shfl(L_ni, y);
+    const int32_t p_role = simt::shfl(L_role, y), p_m = simt::shfl(L_ncopy, y);
+    const double p_e = simt::shfl(L_busy_until, y), p_mr = simt::shfl(L_min_ready, y);
+    const int64_t p_used = simt::shfl(L_used, y), p_sk = simt::shfl(L_skv + L_skv_in, y);
+    const bool st_me = L_job == JOB_STEP, st_p = p_job == JOB_STEP;
+    // the next arrival, and the non-stepping members' own events
+    double pht = ht;
+    int32_t phk = hk;
+    auto fold = [&](bool stepping, int32_t job, double e, int32_t role, int32_t ni, double mr, int32_t id) {
+      if (stepping) return;
+      double yt = kInf;
+      int32_t yk = 0;
+      if (job == JOB_PREFILL) { yt = e; yk = 2 * 64 + id; }
+      else if (role == ROLE_DECODE && ni > 0) { yt = mr; yk = 64 + id; }
+      if (yt < pht || (yt == pht && yk < phk)) { pht = yt; phk = yk; }
+    };
+    fold(st_me, L_job, L_busy_until, L_role, L_ni, L_min_ready, lane);
+    fold(st_p, p_job, p_e, p_role, p_ni, p_mr, y);
+    // B as the serial loop has it in its tests (a's zeroed when a is not stepping)
+    const int32_t B = L_nb;
+    const int32_t Bme = (!isb && !st_me) ? 0 : B, Bp = (isb && !st_p) ? 0 : p_nb;
+    // own limit: remaining-token count and the rebalance gap G0 + i (B - 1) < 0
+    // (the partner's steps only lower G)
+    int64_t lim = st_me ? (int64_t)L_minrem - 1 : 0;
+    if (p_role == ROLE_DECODE && L_kvmin != INT64_MAX) {
+      const int64_t cz = (int64_t)Bme + L_ni - Bp - p_ni;
+      if (cz >= 1) {
+        const int64_t dz = (L_skv + L_skv_in + Bme) - p_sk;
+        const int64_t G = (cz >= 2 ? dz : dz - 1) - (L_kvmin + 1);
+        if (G >= 0) lim = 0;
+        else if (Bme > 1 && G + (lim - 1) * (Bme - 1) >= 0) {
+          const int64_t q = (-G - 1) / (Bme - 1) + 1;
+          if (q < lim) lim = q;
+        }
+      }
+    }
+    // KV slack and event budget: at most C steps per member with
+    // C (B_me + m_p) <= cap - used_me and C (B_p + m_me) <= cap - used_p
+    // (a member that is not stepping contributes B = 0), 2 C <= budget
+    const int64_t cap = PC.f.cap;
+    const int64_t d1 = (int64_t)(st_me ? B : 0) + p_m, s1 = cap - L_used;
+    const int64_t d2 = (int64_t)(st_p ? p_nb : 0) + L_ncopy, s2 = cap - p_used;
+    int64_t C = budget > 0 ? budget >> 1 : 0;
+    if (lim > 0x7fffffff) lim = 0x7fffffff;
+    const int64_t p_lim = simt::shfl((int32_t)lim, y);
+    int64_t want = lim > p_lim ? lim : p_lim;  // the larger member limit
+    if (want > C) want = C;
+    // the slack only matters up to `want` steps: divide only when it binds
+    if (d1 * want > s1) { const int64_t c1 = s1 > 0 ? s1 / d1 : 0; if (c1 < C) C = c1; }
+    if (d2 * want > s2) { const int64_t c2 = s2 > 0 ? s2 / d2 : 0; if (c2 < C) C = c2; }
+    const bool use = pc;
+    int64_t nmax = lim < C ? lim : C;
+    if (!use || !st_me || nmax < 0) nmax = 0;
+    if (nmax > 0x7fffffff) nmax = 0x7fffffff;
+    // this member's chain, bounded by the next outside event and its own incoming
+    const int32_t key = 3 * 64 + lane, pkey = 3 * 64 + y;
+    double tl = pht;
+    {
+      const double mr = L_ni > 0 ? L_min_ready : kInf;
+      bool strict = !(key < phk);
+      if (mr <= tl) { tl = mr; strict = true; }
+      if (!strict && tl < kInf) tl = as_f64(as_u64(tl) + 1);
+    }
+    double comp = 0.0, mlat = 0.0;
+    if (nmax > 0) {
+      comp = comp_floor(B);
+      mlat = transfer_latency(PC.f, kmul((double)L_ncopy, PC.f.kvb));
+    }
+    // pass 0: own limits; the pair's chain ends at the earlier first untaken
+    // step end, so a member whose steps reach past the partner's runs again
+    // (pass 1) with that bound (LOG: every member runs pass 1, logging)
+    PChain c;
+    bool redo = false;
+    for (int pass = 0;; ++pass) {
+      if (LOG && pass == 1) c = pair_member_run<LOG>((int32_t)nmax, tl, comp, mlat, L_ncopy, B);
+      else c = pair_member_run<false>((int32_t)nmax, tl, comp, mlat, L_ncopy, B);
+      if (pass == 1) break;
+      const double p_stop = simt::shfl(c.e, y);
+      if (st_p) {  // my steps must precede the partner's stop event in (time, id) order
+        const double bnd = key < pkey && p_stop < kInf ? as_f64(as_u64(p_stop) + 1) : p_stop;
+        if (bnd < tl) tl = bnd;
+      }
+      redo = c.k > 0 && !(c.js < tl);
+      if (!(LOG || redo)) break;
+    }
+    const int32_t kp = simt::shfl(c.k, y);
+#if defined(KVSIM_EMU) && defined(KVSIM_EMU_PROFILE)
+    {  // emulator-only: pairs taken here / sent to the serial loop, re-runs, steps
+      auto add = [](int i, long long v) { __atomic_fetch_add(&emu_prof[i], v, __ATOMIC_RELAXED); };
+      if (use && !isb) add(21, 1);
+      if (use && redo) add(23, 1);
+      if (use) add(24, c.k);
+      if (use && !isb && st_me && st_p) add(26, 1);
+      if (use && !isb) add(27, (long long)(c.k > kp ? c.k : kp));
+    }
+#endif
+    if (!use) return;
+    // commit (the ledgers only grow in a chain: the peak is the final value)
+    L_used += (int64_t)c.k * B + (int64_t)kp * p_m;
+    if (L_used > L_peak) L_peak = L_used;
+    L_copy_tok += (int64_t)kp * p_m;
+    if (c.k > 0) {
+      L_busy_until = c.e; L_job_start = c.js; L_busy_time = c.busy; L_prev_end = c.js;
+      L_link = c.link; L_mirror_fin = c.mfin;
+      L_dG = c.dG; L_de1 = c.de1; L_dpe = c.dpe;
+      L_skv += (int64_t)c.k * B;
+      L_minrem -= c.k;
+      if (L_kvmin != INT64_MAX) L_kvmin += c.k;
+      L_dj += c.k;
+      steps = c.k;
+      tok = (int64_t)c.k * B;
+      tw = (int64_t)c.tw * B;
+      mir = (int64_t)c.k * L_ncopy;
+      tmax = c.js;
+    }
+  }
+#endif
   // drive: bitmask of lanes allowed to advance (instances; AcceLLM: any lane
   // of a pair selects the pair)
   KV_DEV_NOINLINE void advance(unsigned drive) {
@@ -1198,6 +1404,7 @@ struct Sim {
     } else {
       // AcceLLM: the even lane of each pair drives both members in merged order
       const int pl = lane | 1;  // partner lane (valid for even lanes)
+      bool pcand = false;
       {
         const int32_t pj = simt::shfl(L_job, pl), pp = simt::shfl(L_pend, pl);
         const int32_t qn = simt::shfl(Q_n, (lane >> 1) & 31);
@@ -1209,7 +1416,12 @@ struct Sim {
         const bool cand = !(lane & 1) && lane < n && (((drive >> lane) | (drive >> (lane + 1))) & 1) && qok &&
                           !L_pend && !pp && (L_job == JOB_STEP || pj == JOB_STEP);
         if (simt::ballot(cand) == 0) return;
+        pcand = cand;
       }
+#if KVSIM_PAIR_PAR
+      // member-parallel pair chains (pair_par)
+      pair_par(simt::shfl((int32_t)pcand, lane & ~1) != 0, ht, hk, budget, steps, tok, tw, mir, tmax);
+#else
       MemberChain b;
       b.stepping = simt::shfl(L_job, pl) == JOB_STEP;
       const int32_t bjob = simt::shfl(L_job, pl);
@@ -1330,6 +1542,9 @@ struct Sim {
         }
         if (!a.stepping) a.B = L_nb;
         steps = a.steps + b.steps;
+#if defined(KVSIM_EMU) && defined(KVSIM_EMU_PROFILE)
+        __atomic_fetch_add(&emu_prof[25], (long long)steps, __ATOMIC_RELAXED);
+#endif
         tok = (int64_t)a.steps * a.B + (int64_t)b.steps * b.B;
         tw = a.tw + b.tw;
         mir = (int64_t)a.steps * a.m + (int64_t)b.steps * b.m;
@@ -1358,6 +1573,7 @@ struct Sim {
         L_peak = bpeak;
         L_copy_tok = bct;
       }
+#endif
     }
     const unsigned am = simt::ballot(steps > 0);
     if (am != 0 && (am & (am - 1)) == 0) {  // one chain advanced (the common case): plain adds

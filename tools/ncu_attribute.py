@@ -55,6 +55,7 @@ def main(sass_csv, dis_txt, sim_cuh):
     base = int(rows[2][ia], 16)
     inst, samp, noi = collections.Counter(), collections.Counter(), collections.Counter()
     execd = []
+    per = []  # (executed count, function) per SASS instruction
     for r in rows[2:]:
         if len(r) <= ino:
             continue
@@ -65,6 +66,7 @@ def main(sass_csv, dis_txt, sim_cuh):
         samp[k] += int(r[iss] or 0)
         noi[k] += int(r[ino] or 0)
         execd.append(n)
+        per.append((n, k))
     ti, ts, tn = sum(inst.values()), sum(samp.values()), sum(noi.values())
     print(f"instructions executed {ti:.3e}; stall samples {ts}; no_instruction share {tn / ts:.3f}")
     print(f"{'function':28s} {'samples':>8s} {'inst':>7s} {'no_inst':>8s}")
@@ -79,6 +81,18 @@ def main(sass_csv, dis_txt, sim_cuh):
             print(f"{marks[0]:.2f} of executed instructions in the {i + 1} hottest SASS instructions "
                   f"({(i + 1) * 16 / 1024:.0f} KB)")
             marks.pop(0)
+    # hot footprint by function: SASS bytes among the instructions that make
+    # up 90% of all executed instructions
+    per.sort(key=lambda t: -t[0])
+    acc, foot = 0, collections.Counter()
+    for n, k in per:
+        if acc >= 0.9 * ti:
+            break
+        acc += n
+        foot[k] += 16
+    print("hot footprint (90% of executed instructions) by function, bytes:")
+    for k, v in foot.most_common(25):
+        print(f"  {k:28s} {v:7d}")
 
 
 if __name__ == "__main__":

@@ -5,13 +5,13 @@
 #   <tag>_metrics.csv   selected raw metrics (time, issue, stalls, caches, DRAM, L2)
 #   <tag>_attr.txt      per-function executed instructions / stall samples
 #   <tag>_sass_cols.txt column names of the source page (for reference)
-# usage: tools/profile_slice.sh TAG [RATES] [REQUESTS]
+# usage: tools/profile_slice.sh TAG [RATES] [REQUESTS] [POLICY]
 set -u
-TAG=${1:-slice}; RATES=${2:-84}; REQ=${3:-10000}
+TAG=${1:-slice}; RATES=${2:-84}; REQ=${3:-10000}; POL=${4:-}
 O=gpurun_out
-python tools/ncu_slice.py $RATES $REQ > $O/${TAG}_plain.log 2>&1
+python tools/ncu_slice.py $RATES $REQ $POL > $O/${TAG}_plain.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:kvsim_sweep -s 0 -c 1 -o /tmp/$TAG \
-    python tools/ncu_slice.py $RATES $REQ > $O/${TAG}_ncu.log 2>&1
+    python tools/ncu_slice.py $RATES $REQ $POL > $O/${TAG}_ncu.log 2>&1
 ncu -i /tmp/$TAG.ncu-rep --page raw --csv > /tmp/${TAG}_raw.csv 2>/dev/null
 python - /tmp/${TAG}_raw.csv > $O/${TAG}_metrics.csv <<'PY'
 import csv, sys, re
@@ -30,7 +30,7 @@ for h, u, v in zip(hdr, units, vals):
 PY
 ncu -i /tmp/$TAG.ncu-rep --page source --csv --print-source sass > /tmp/${TAG}_sass.csv 2>/dev/null
 head -1 /tmp/${TAG}_sass.csv | tr ',' '\n' > $O/${TAG}_sass_cols.txt
-mkdir -p /tmp/cub && (cd /tmp/cub && cuobjdump -xelf all $GRAFT_REPO_ROOT/paper_2411_05555_b200/_build/libkvsim_gpu.so > /dev/null)
+mkdir -p /tmp/cub && (cd /tmp/cub && cuobjdump -xelf all ${KVSIM_LIB:-$GRAFT_REPO_ROOT/paper_2411_05555_b200/_build/libkvsim_gpu.so} > /dev/null)
 nvdisasm -g -c /tmp/cub/kvsim_sweep.sm_100a.cubin > /tmp/${TAG}_dis.txt 2>/dev/null
 python tools/ncu_attribute.py /tmp/${TAG}_sass.csv /tmp/${TAG}_dis.txt paper_2411_05555_b200/csrc/kvsim_sim.cuh > $O/${TAG}_attr.txt 2>&1
 ls -la $O
