@@ -1156,10 +1156,10 @@ struct Sim {
       e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
       k = 1;
     }
-    // steady state: js == prev, one difference is the busy increment and the gap
-    while (k < nmax && e < tl) {
+    // steady state: js == prev, one difference is the busy increment and the
+    // gap; first the steps that started before the measurement window
+    while (k < nmax && e < tl && js < warmup) {
       const double st = ksub(e, js);
-      if (js >= warmup) busy = kadd(busy, st);
       if (st > dG) dG = st;
       if (e >= warmup) tw += 1;
       if (m > 0) {
@@ -1173,6 +1173,24 @@ struct Sim {
       e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
       k += 1;
     }
+    // inside the window (times only grow): every step adds busy time and ends in it
+    const int32_t kw = k;
+    while (k < nmax && e < tl) {
+      const double st = ksub(e, js);
+      busy = kadd(busy, st);
+      if (st > dG) dG = st;
+      if (m > 0) {
+        link = kadd(e > link ? e : link, mlat);
+        if constexpr (DOLOG) log_one(e, KVSIM_EV_TRANSFER, lane, lane ^ 1, 1, m);
+      }
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+      Kd = kadd(Kd, Bd);
+      if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k + 1) * B);
+      js = e;
+      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      k += 1;
+    }
+    tw += k - kw;
     c.e = e; c.js = js; c.busy = busy; c.dG = dG; c.link = link;
     if (m > 0) c.mfin = link;
     c.k = k; c.tw = tw;
@@ -1372,22 +1390,39 @@ struct Sim {
           if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + B);
           js = e;
           e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
-          k = 1;
           // steady state: the step that just ended started at the previous
           // end (js == prev), so one difference is both the busy increment
-          // and the members' gap
-          while (k < nmax && e < tl) {
+          // and the members' gap. 32-bit counters (nmax < 2^31).
+          const int32_t nm = (int32_t)nmax;
+          int32_t k32 = 1, ntw32 = (int32_t)ntw;
+          // steps that started before the measurement window
+          while (k32 < nm && e < tl && js < warmup) {
             const double st = ksub(e, js);
-            if (js >= warmup) busy = kadd(busy, st);
             if (st > dG) dG = st;
-            if (e >= warmup) ntw += 1;
+            if (e >= warmup) ntw32 += 1;
             if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
             Kd = kadd(Kd, Bd);
-            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (k + 1) * B);
+            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k32 + 1) * B);
             js = e;
             e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
-            k += 1;
+            k32 += 1;
           }
+          // inside the window (times only grow): every step adds to the busy
+          // time and ends in the window
+          const int32_t kw = k32;
+          while (k32 < nm && e < tl) {
+            const double st = ksub(e, js);
+            busy = kadd(busy, st);
+            if (st > dG) dG = st;
+            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_END, lane, B, 0, 0);
+            Kd = kadd(Kd, Bd);
+            if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k32 + 1) * B);
+            js = e;
+            e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+            k32 += 1;
+          }
+          k = k32;
+          ntw = ntw32 + (k32 - kw);
           prev = js;
           const int64_t grow = k * B;
           L_busy_until = e; L_job_start = js; L_busy_time = busy; L_prev_end = prev;
