@@ -41,9 +41,20 @@ def build_cuda(force=False):
     os.makedirs(OUT, exist_ok=True)
     lib = os.path.join(OUT, "libkvsim_gpu.so")
     if force or _stale(lib, _csrc_deps()):
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
-              "-Xptxas", "-v", "-I" + INC, "-shared", "-o", lib,
-              os.path.join(CSRC, "kvsim_sweep.cu"), os.path.join(CSRC, "perfmodel.cpp")])
+        # the lean (kvsim_sweep.cu) and full (kvsim_sweep_full.cu) kernel
+        # translation units compile in parallel, then link into one library
+        flags = [*ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                 "-Xptxas", "-v", "-I" + INC]
+        objs, procs = [], []
+        for src in ("kvsim_sweep.cu", "kvsim_sweep_full.cu", "perfmodel.cpp"):
+            obj = os.path.join(OUT, src.replace(".", "_") + ".o")
+            cmd = [NVCC, *flags, "-c", "-o", obj, os.path.join(CSRC, src)]
+            print("+", " ".join(cmd), file=sys.stderr)
+            procs.append(subprocess.Popen(cmd))
+            objs.append(obj)
+        if any(p.wait() != 0 for p in procs):
+            raise subprocess.CalledProcessError(1, "nvcc")
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs])
     return lib
 
 

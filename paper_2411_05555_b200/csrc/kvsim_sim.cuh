@@ -150,6 +150,17 @@ __shared__ SweepArgs kvsim_args_smem;
 #define AR (*A)
 #endif
 #define PC (ws()->pc)
+// Event handlers and the helpers they call on every handled event. The lean
+// sweep kernel inlines them into the event loop (kvsim_sweep.cu): a call
+// costs more than the larger code (in-process A/B on config 4: 5.19 s with
+// the handlers outlined, 4.25 s inlined). The full kernel
+// (kvsim_sweep_full.cu: events, detail metrics, extensions) keeps them
+// outlined (KVSIM_OUTLINE_HANDLERS), which bounds its compile time.
+#if defined(KVSIM_OUTLINE_HANDLERS)
+#define KV_DEV_HANDLER KV_DEV_NOINLINE
+#else
+#define KV_DEV_HANDLER KV_DEV
+#endif
 // One specialisation per policy: every `policy == ...` test folds at compile
 // time, so a warp only ever executes (and caches) its own policy's code.
 // EXT: AcceLLM with the policy timer (degraded mode / inter-pair leveling,
@@ -482,7 +493,7 @@ struct Sim {
   }
 
   // arrival generator (SEMANTICS §2); uniform across lanes
-  KV_DEV_NOINLINE void gen_next() {
+  KV_DEV_HANDLER void gen_next() {
     has_next = false;
     if (next_rid >= PC.n_limit) return;
     double t;
@@ -563,7 +574,7 @@ struct Sim {
     int32_t nb_old, completed, m_copies, copy_done, minrem;
     int64_t kv_done, copy_free, kvmin;
   };
-  KV_DEV_NOINLINE StepOut step_loop(int x, double t) {
+  KV_DEV_HANDLER StepOut step_loop(int x, double t) {
     EMU_COUNT(0);
     StepOut o;
     const int32_t nb = get(L_nb, x);
@@ -677,7 +688,7 @@ struct Sim {
     if (get(L_min_ready, x) > t) return;
     join_slow(x, t);
   }
-  KV_DEV_NOINLINE void join_slow(int x, double t) {
+  KV_DEV_HANDLER void join_slow(int x, double t) {
     EMU_COUNT(1);
     flush(x);
     const int32_t ni = get(L_ni, x);
@@ -787,7 +798,7 @@ struct Sim {
   }
   // largest redundant copy held on instance x (max kv, ties lowest rid)
   KV_DEV Found largest_copy_on(int x) { return largest_copy_on_from(x, clients_of(x)); }
-  KV_DEV_NOINLINE Found largest_copy_on_from(int x, unsigned clients) {
+  KV_DEV_HANDLER Found largest_copy_on_from(int x, unsigned clients) {
     uint64_t best = 0;
     int32_t bidx = -1, bwhere = 0, by = -1;
     for (unsigned cm = clients; cm; cm &= cm - 1) {
@@ -824,7 +835,7 @@ struct Sim {
     r.kv = (int64_t)(wbest >> 32);
     return r;
   }
-  KV_DEV_NOINLINE void evict(int x, const Found& v) {
+  KV_DEV_HANDLER void evict(int x, const Found& v) {
     EMU_COUNT(14);
     const int y = v.y;
     int64_t held = v.kv;
@@ -842,7 +853,7 @@ struct Sim {
   }
 
   // ------------------------------------------------------ preemption (P9)
-  KV_DEV_NOINLINE void preempt_newest(int x) {
+  KV_DEV_HANDLER void preempt_newest(int x) {
     EMU_COUNT(15);
     flush(x);
     const int32_t nb = get(L_nb, x);
@@ -897,7 +908,7 @@ struct Sim {
       simt::sync();
     }
   }
-  KV_DEV_NOINLINE double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
+  KV_DEV_HANDLER double prefill_transfer(int s, int d, int64_t s1, double t_start, double t_done) {
     const double busy = link_get(s, d);
     const double tail = kadd(t_done, transfer_latency(PC.f, kmul((double)s1, PC.f.kvb_layer)));
     const double start = t_start > busy ? t_start : busy;
@@ -910,7 +921,7 @@ struct Sim {
   }
 
   // ------------------------------------------- decode step (splitwise/accellm)
-  KV_DEV_NOINLINE void step_start(int x, double t) {
+  KV_DEV_HANDLER void step_start(int x, double t) {
     EMU_COUNT(2);
     if constexpr (POL == KVSIM_POLICY_SPLITWISE) {
       if (cobatch()) { sw_cobatch_start(x, t); return; }
@@ -961,7 +972,7 @@ struct Sim {
 
   }
 
-  KV_DEV_NOINLINE void step_end(int x, double t) {
+  KV_DEV_HANDLER void step_end(int x, double t) {
     EMU_COUNT(3);
     account_job(x, t);
     if (lane == 0) ws()->ct.n_steps += 1;
@@ -1020,7 +1031,7 @@ struct Sim {
   // (one 16-byte load of their remaining-token words, two of their TBT
   // maxima; Bcap is a multiple of 4 and the arrays 16-byte aligned, so the
   // slots past B in the last vector are unused and written back unchanged).
-  KV_DEV_NOINLINE void flush_slow(int x) {
+  KV_DEV_HANDLER void flush_slow(int x) {
     const int32_t j = get(L_dj, x);
     const double e1 = get(L_de1, x), pe = get(L_dpe, x), G = get(L_dG, x);
     const int32_t B = get(L_nb, x);
@@ -1324,7 +1335,7 @@ struct Sim {
 #endif
   // drive: bitmask of lanes allowed to advance (instances; AcceLLM: any lane
   // of a pair selects the pair)
-  KV_DEV_NOINLINE void advance(unsigned drive) {
+  KV_DEV_HANDLER void advance(unsigned drive) {
     const double kInf = as_f64(0x7ff0000000000000ull);
     double ht = has_next ? t_next : kInf;
     int32_t hk = -1;  // arrivals precede instance events at equal time
@@ -1632,7 +1643,7 @@ struct Sim {
     simt::sync();
   }
   // ------------------------------------------------------------- unified
-  KV_DEV_NOINLINE void unified_start(int x, double t) {
+  KV_DEV_HANDLER void unified_start(int x, double t) {
     EMU_COUNT(17);
     int32_t nb = get(L_nb, x);
     while (get(L_used, x) + nb > PC.f.cap) {
@@ -1752,7 +1763,7 @@ struct Sim {
     log(KVSIM_EV_STEP_START, x, nb, k, K);
   }
 
-  KV_DEV_NOINLINE void unified_end(int x, double t) {
+  KV_DEV_HANDLER void unified_end(int x, double t) {
     EMU_COUNT(18);
     account_job(x, t);
     if (lane == 0) ws()->ct.n_steps += 1;
@@ -1812,7 +1823,7 @@ struct Sim {
   }
 
   // ------------------------------------------------------------ splitwise
-  KV_DEV_NOINLINE void sw_try_start(double t) {
+  KV_DEV_HANDLER void sw_try_start(double t) {
     EMU_COUNT(19);
     for (int p = 0; p < n_prefill; ++p) {
       if (get(L_job, p) != JOB_NONE) continue;
@@ -1870,7 +1881,7 @@ struct Sim {
         if (get(L_job, d) == JOB_NONE) sw_cobatch_start(d, t);
   }
 
-  KV_DEV_NOINLINE void sw_prefill_done(int p, double t) {
+  KV_DEV_HANDLER void sw_prefill_done(int p, double t) {
     EMU_COUNT(20);
     account_job(p, t);
     if (lane == 0) ws()->ct.n_prefills += 1;
@@ -1955,7 +1966,7 @@ struct Sim {
     return get(L_used, x) - get(L_copy_tok, x) + len <= PC.f.cap;
   }
   // move every request whose primary is x and that holds a copy on x^1
-  KV_DEV_NOINLINE void move_all_to_partner(int x, double t) {
+  KV_DEV_HANDLER void move_all_to_partner(int x, double t) {
     EMU_COUNT(8);
     const int y = partner_of(x);
     if (y < 0) return;  // a degraded group's dual instance: its requests stall
@@ -2070,7 +2081,7 @@ struct Sim {
     }
   }
 
-  KV_DEV_NOINLINE void acc_start_job(int x, double t) {
+  KV_DEV_HANDLER void acc_start_job(int x, double t) {
     EMU_COUNT(13);
     const int q = qid(x >> 1);
     const int32_t h = get(Q_head, q);
@@ -2128,7 +2139,7 @@ struct Sim {
     log(KVSIM_EV_PREFILL_START, x, k, k ? j_rid(x)[0] : -1, s1);
   }
 
-  KV_DEV_NOINLINE bool try_switch(int x, double t) {
+  KV_DEV_HANDLER bool try_switch(int x, double t) {
     EMU_COUNT(12);
     if (!head_admissible(x)) return false;
     if (own(x)) L_pend = 0;
@@ -2143,7 +2154,7 @@ struct Sim {
     if (get(Q_n, q) == 0) return;
     ensure_prefill_slow(q, t);
   }
-  KV_DEV_NOINLINE void ensure_prefill_slow(int q, double t) {
+  KV_DEV_HANDLER void ensure_prefill_slow(int q, double t) {
     EMU_COUNT(11);
     if (get(Q_n, q) == 0) return;
     if (degraded_pair(q)) {  // the dual instance is the group's only prefill instance
@@ -2176,7 +2187,7 @@ struct Sim {
     if (load_of(x) - load_of(y) < 1) return;
     rebalance_slow(x, t);
   }
-  KV_DEV_NOINLINE void rebalance_slow(int x, double t) {
+  KV_DEV_HANDLER void rebalance_slow(int x, double t) {
     EMU_COUNT(6);
     flush(x);
     const int y = x ^ 1;
@@ -2210,7 +2221,7 @@ struct Sim {
     }
   }
   // move batch slot idx of x to y's incoming (zero-byte label swap)
-  KV_DEV_NOINLINE void move_one(int x, int32_t idx, double t) {
+  KV_DEV_HANDLER void move_one(int x, int32_t idx, double t) {
     EMU_COUNT(7);
     const int y = x ^ 1;
     const int32_t rid = b_rid(x)[idx];
@@ -2240,7 +2251,7 @@ struct Sim {
     log(KVSIM_EV_MOVE, x, rid, y, 0);
   }
 
-  KV_DEV_NOINLINE void acc_boundary(int x, double t) {
+  KV_DEV_HANDLER void acc_boundary(int x, double t) {
     EMU_COUNT(9);
     if constexpr (EXT) {
       if (own(x) && L_lvl_hold > 0 && t >= L_lvl_until) { L_used -= L_lvl_hold; L_lvl_hold = 0; }
@@ -2259,7 +2270,7 @@ struct Sim {
     step_start(x, t);
   }
 
-  KV_DEV_NOINLINE void acc_prefill_done(int x, double t) {
+  KV_DEV_HANDLER void acc_prefill_done(int x, double t) {
     EMU_COUNT(10);
     flush(x);
     account_job(x, t);
@@ -2780,7 +2791,7 @@ struct Sim {
   }
 
   // -------------------------------------------------------------- arrival
-  KV_DEV_NOINLINE void arrive(double t) {
+  KV_DEV_HANDLER void arrive(double t) {
     EMU_COUNT(16);
     const int64_t rid64 = next_rid;
     const int32_t rid = (int32_t)rid64;

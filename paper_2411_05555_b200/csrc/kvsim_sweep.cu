@@ -29,26 +29,16 @@ using kvsim_dev::WarpScratch;
 using kvsim_dev::kWarpsPerBlock;
 
 // ------------------------------------------------------------------ kernels
-// MINB = minimum resident blocks per SM requested from ptxas (register cap
-// 65536 / (128 * MINB)); selected at context open (KVSIM_MINB, default below).
-// FULL = false: the lean sweep kernel (plain points only); true: every
-// specialisation (events, detail metrics, AcceLLM extensions, SPEC variants).
-template <int MINB, bool FULL>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, MINB) kvsim_sweep_kernel(const __grid_constant__ SweepArgs a) {
-  WarpScratch* scratch = reinterpret_cast<WarpScratch*>(kvsim_smem);
-  const int w = threadIdx.x >> 5;
-  const int64_t slot = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
-#if defined(KVSIM_SIM_SMEM)
-  // block-shared copy of the parameters (kvsim_sim.cuh: AR)
-  if (threadIdx.x == 0) kvsim_dev::kvsim_args_smem = a;
-  __syncthreads();
-  if (slot >= a.slots) return;
-  kvsim_dev::sweep_warp<FULL>(&kvsim_dev::kvsim_args_smem, &scratch[w], (int32_t)slot);
-#else
-  if (slot >= a.slots) return;
-  kvsim_dev::sweep_warp<FULL>(&a, &scratch[w], (int32_t)slot);
+// K3: kvsim_kernel.cuh; this translation unit instantiates the lean kernel
+// (handlers inlined), kvsim_sweep_full.cu the full one (handlers outlined).
+#include "kvsim_kernel.cuh"
+template __global__ void kvsim_sweep_kernel<3, false>(const __grid_constant__ SweepArgs);
+#ifdef KVSIM_MINB_ALT
+template __global__ void kvsim_sweep_kernel<KVSIM_MINB_ALT, false>(const __grid_constant__ SweepArgs);
 #endif
-}
+// kvsim_sweep_full.cu
+using SweepFn = void (*)(SweepArgs);
+SweepFn kvsim_full_kernel(int minb);
 
 __global__ void kvsim_perf_kernel(const kvsim_point_desc* pts, const int32_t* pidx, const int32_t* op,
                                   const int64_t* s1, const int64_t* s2, double* out, int64_t n) {
@@ -149,7 +139,6 @@ struct kvsim_gpu_ctx {
 
 namespace {
 
-using SweepFn = void (*)(SweepArgs);
 constexpr int kDefaultMinBlocks = 3;
 // percent of the unified L1/shared array given to shared memory
 // (KVSIM_CARVEOUT; -1 = driver default): the Sim objects need ~213 KB per SM
@@ -159,22 +148,21 @@ constexpr int kDefaultCarveout = 100;
 #else
 constexpr int kDefaultCarveout = 25;
 #endif
-// A/B builds (tools/build_variant.sh) may replace the second variant with
-// another occupancy (-DKVSIM_MINB_ALT=4) and alias the full kernel to the
-// lean one (-DKVSIM_LEAN_ONLY: plain sweeps only, a much faster build).
-#ifndef KVSIM_MINB_ALT
-#define KVSIM_MINB_ALT 2
-#endif
-#ifdef KVSIM_LEAN_ONLY
-constexpr bool kFullImage = false;
-#else
-constexpr bool kFullImage = true;
-#endif
+// Shipped: MINB = 3 (3 blocks of 4 warps per SM; registers and the shared
+// Sim objects both allow 3). A/B builds (tools/build_variant.sh) may add a
+// lean kernel with another occupancy (-DKVSIM_MINB_ALT=N, selected with
+// KVSIM_MINB=N) and drop the full kernel (-DKVSIM_LEAN_ONLY: plain sweeps
+// only, a much faster build). Measured: 2 blocks 5.91 vs 3 blocks 5.71 s
+// (round 2, before the shared-memory Sim), 4-6 blocks slower (spills).
 SweepFn sweep_variant(int minb, bool full) {
-  // occupancy is not the limiter (instruction fetch is):
-  // 2 vs 3 blocks/SM measured 5.91 vs 5.71 s on config 4, so two variants ship
-  if (full) return minb == 3 ? kvsim_sweep_kernel<3, kFullImage> : kvsim_sweep_kernel<KVSIM_MINB_ALT, kFullImage>;
-  return minb == 3 ? kvsim_sweep_kernel<3, false> : kvsim_sweep_kernel<KVSIM_MINB_ALT, false>;
+#ifdef KVSIM_LEAN_ONLY
+  full = false;
+#endif
+  if (full) return kvsim_full_kernel(minb);
+#ifdef KVSIM_MINB_ALT
+  if (minb == KVSIM_MINB_ALT) return kvsim_sweep_kernel<KVSIM_MINB_ALT, false>;
+#endif
+  return kvsim_sweep_kernel<3, false>;
 }
 
 // Stable partition of the launch order: points the lean kernel can run first
@@ -324,8 +312,12 @@ int kvsim_gpu_open(int device, kvsim_gpu_ctx** out, char* err, size_t err_len) {
   int minb = kDefaultMinBlocks;
   if (const char* e = std::getenv("KVSIM_MINB")) {
     minb = std::atoi(e);
+#ifdef KVSIM_MINB_ALT
     if (minb != KVSIM_MINB_ALT && minb != 3)
-      return set_err(err, err_len, KVSIM_E_INVALID, "KVSIM_MINB must be 2 or 3 (the shipped kernel variants)");
+#else
+    if (minb != 3)
+#endif
+      return set_err(err, err_len, KVSIM_E_INVALID, "KVSIM_MINB: this build ships the 3-blocks-per-SM kernels only");
   }
   auto* c = new kvsim_gpu_ctx();
   const int rc = [&]() -> int {
