@@ -31,7 +31,7 @@ def main(sass_csv, dis_txt, sim_cuh):
             off2src[int(m.group(1), 16)] = cur
     funcs = []
     for i, l in enumerate(open(sim_cuh), 1):
-        m = re.match(r"\s+KV_DEV(?:_NOINLINE)? [\w:<>,\* &]+?\b(\w+)\(", l)
+        m = re.match(r"\s+KV_DEV\w* [\w:<>,\* &]+?\b(\w+)\(", l)
         if m:
             funcs.append((i, m.group(1)))
 
