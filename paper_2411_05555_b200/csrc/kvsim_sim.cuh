@@ -1367,8 +1367,8 @@ struct Sim {
         const double mr = L_ni > 0 ? L_min_ready : kInf;
         const double comp = comp_floor(B);
         const int32_t key = 3 * 64 + lane;
-        // the chain runs on register copies (the Sim object itself lives in
-        // local memory because its cold paths are outlined)
+        // the chain runs on register copies of the lane's fields (the Sim
+        // object lives in shared memory)
         const double Wb = PC.f.W, kvb = PC.f.kvb, mden = PC.f.mem_den, mrcp = PC.f.mem_rcp;
         double e = L_busy_until, js = L_job_start, busy = L_busy_time, prev = L_prev_end;
         double dG = L_dG, de1 = L_de1, dpe = L_dpe;
@@ -3203,8 +3203,8 @@ KV_DEV_NOINLINE void run_point(const SweepArgs* ap, WarpScratch* w, int32_t slot
 // Points that need the full specialisations (event log, detail metrics,
 // AcceLLM timer extensions, optional SPEC variants); the host launches the
 // others through the lean FULL=false kernel, whose image holds only the
-// three plain sweep specialisations (a smaller instruction footprint:
-// in-process A/B on config 4, 5.79 -> 5.63 s).
+// three plain sweep specialisations with their handlers inlined
+// (kvsim_sweep.cu; the full kernel is kvsim_sweep_full.cu).
 KV_HD_INLINE bool needs_full(const kvsim_point_desc& d) {
   return (d.policy == KVSIM_POLICY_ACCELLM && (d.accellm_flags & 3) != 0) || d.first_token_decode != 0 ||
          d.splitwise_cobatch != 0;
