@@ -3,6 +3,8 @@
 independent CPU oracle bit for bit — summaries, per-request records and the
 decision/event log — on the SPEC closed form, BASELINE config 1 and the
 SPEC.md:469 randomized small-config suite (with memory-starved variants)."""
+import os
+
 import pytest
 
 from configs import closed_form_point, config1, config2, config3, random_small
@@ -95,3 +97,23 @@ def test_sweep_specialisation_no_log(chunk):
         if d:
             bad.append((p.policy, p.num_instances, p.num_requests, d[:4]))
     assert not bad, bad
+
+
+def test_serial_pair_chain_variant(tmp_path):
+    """The serial merged AcceLLM pair loop (-DKVSIM_PAIR_PAR=0, kept as the
+    reference formulation of the member-parallel pair chains) still matches
+    the oracle bit for bit, event logs included."""
+    import subprocess
+    import harness
+    src = os.path.join(harness.ROOT, "tests", "emu", "kvsim_emu.cpp")
+    so = str(tmp_path / "libkvsim_emu_serial_pairs.so")
+    subprocess.run(["g++", "-DKVSIM_EMU", "-DKVSIM_PAIR_PAR=0", "-O2", "-std=gnu++20", "-ffp-contract=off", "-fPIC",
+                    "-shared", "-I" + os.path.join(harness.ROOT, "include"), "-o", so, src, "-lpthread"], check=True)
+    saved = (harness._emu, harness.EMU_SO)
+    harness._emu, harness.EMU_SO = None, so
+    try:
+        pts = [config2("accellm", r, n=80) for r in (6.0, 12.0, 18.0)]
+        pts += [p for p in (random_small(i) for i in range(100)) if p.policy == 2][:30]
+        check(pts)
+    finally:
+        harness._emu, harness.EMU_SO = saved
