@@ -94,6 +94,15 @@ def ncu_traffic():
         return None
 
 
+def ncu_inst_per_launch():
+    """Warp instructions per launch (smsp__inst_executed.sum) of the config-4
+    sweep kernel from the same committed ncu capture, or None."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, NCU_TRAFFIC_FILE)))["smsp__inst_executed.sum"])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -356,6 +365,21 @@ def main():
                          f"threads (CPU oracle, one point per thread)"}
         parity = parity_check(summ, S_cpu)
 
+    # the binding resource: warp-instruction issue. Achieved =
+    # the committed ncu capture's warp instructions per launch / this run's
+    # per-launch time; peak = one warp instruction per scheduler per cycle
+    # (4 per SM) at the median SM clock sampled during the timed region
+    issue = None
+    inst = ncu_inst_per_launch()
+    clk_s = clk.summary()
+    if workload_is_config4 and n_gpu == 1 and inst and clk_s.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        ach = inst / kernel_s
+        peak = sms * 4 * clk_s["sm_mhz"] * 1e6
+        issue = {"achieved": ach, "peak": peak, "unit": "warp instructions/s", "frac": ach / peak,
+                 "inst_per_launch": inst, "source": NCU_TRAFFIC_FILE + " (smsp__inst_executed.sum) / this run's time",
+                 "inst_per_simulated_request": inst / max(reqs, 1)}
+
     line = {
         "metric": metric, "value": value, "unit": "simulated requests/s", "n_gpus": n_gpu,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": kernel_s * 1e3,
@@ -378,6 +402,7 @@ def main():
                      "algorithmic_bytes_per_launch": bytes_alg,
                      "note": "algorithmic bytes per SURVEY §8d (40 B/request + 8 B/decode iteration), per GPU; "
                              "the kernel is bound by instruction issue/fetch, not HBM (DESIGN.md §7)"},
+        "issue": issue,
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
