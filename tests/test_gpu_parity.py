@@ -259,3 +259,23 @@ def test_lean_and_full_kernels_in_one_run(sim):
         ref = run_oracle(p, ev_cap=0, recs=False)
         assert not diff_results(ref, Result(s, None, None), events=False), (p.policy, p.first_token_decode,
                                                                            p.splitwise_cobatch, p.accellm_flags)
+
+
+def test_random_configs_lean_kernel_records(sim):
+    """Plain random points (memory-starved half of the time) without event
+    logs run in the lean kernel, whose handlers are inlined into the event
+    loop and whose AcceLLM pairs chain member-parallel: summaries,
+    per-request and per-instance records bit-identical to the oracle."""
+    pts = [random_small(5000 + i, max_req=400) for i in range(600)]
+    pts = [p for p in pts if p.first_token_decode == 0 and p.splitwise_cobatch == 0]
+    summ, recs, _ = sim.run(pts, records=True, instances=True)
+    assert sim.last_launches() == 1
+    inst = sim.last_instances
+    bad = []
+    for i, p in enumerate(pts):
+        ref = run_oracle(p, ev_cap=0, recs=True)
+        d = diff_results(ref, Result(summ[i], recs[i], None, inst=inst[i] if summ[i].status == 0 else None),
+                         events=False)
+        if d:
+            bad.append((i, p.policy, p.num_requests, d[:4]))
+    assert not bad, bad
