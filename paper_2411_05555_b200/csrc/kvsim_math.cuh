@@ -178,6 +178,36 @@ KV_HD double kdiv_rcp(double n, double d, double rd) {
   return kdiv(n, d);
 }
 
+// Step chains divide an increasing numerator by a fixed d, starting from a
+// quotient qmin verified by kdiv_rcp. Threshold for kdiv_chain:
+// T = d ulp(qmin) / 2 (d ulp(qmin) / 4 when qmin is a power of two), or 0
+// (every quotient then takes the IEEE division) when qmin or T leave the
+// normal range the test needs.
+KV_HD double kdiv_chain_thr(double qmin, double d) {
+  const uint64_t qb = as_u64(qmin);
+  const uint64_t ex = (qb >> 52) & 0x7ffull;
+  if (ex <= 55 || ex >= 0x7ff) return 0.0;
+  const uint64_t sh = (qb & 0x000fffffffffffffull) == 0 ? 54 : 53;
+  const double T = kmul(d, as_f64((ex - sh) << 52));
+  return T >= 0x1p-1022 && T < as_f64(0x7ff0000000000000ull) ? T : 0.0;
+}
+// RN(n / d) for a quotient not below qmin. q1 (one Newton correction of
+// n rd) is accepted iff |n - q1 d| < T and q1 >= qmin. That implies the
+// kdiv_rcp test (|r1| < d ulp(q1) / 2, since ulp(q1) >= ulp(qmin)) and also
+// covers a power-of-two q1: q1 > qmin then lies in a higher binade than
+// qmin, so T <= d ulp(q1) / 4, half the gap to q1's lower neighbour (and
+// q1 == qmin uses the quarter-ulp T). The test is a loop-invariant compare
+// instead of kdiv_rcp's per-quotient exponent arithmetic; failures take the
+// IEEE division.
+KV_HD double kdiv_chain(double n, double d, double rd, double T, double qmin) {
+  const double q0 = kmul(n, rd);
+  const double q1 = kfma(kfma(-q0, d, n), rd, q0);
+  const double r1 = kfma(-q1, d, n);
+  const double ar = r1 < 0.0 ? -r1 : r1;
+  if (ar < T && q1 >= qmin) return q1;
+  return kdiv(n, d);
+}
+
 // ----------------------------------------------------------- cost model (§1)
 struct Perf {
   double kvb;        // bytes of K+V per token, all layers

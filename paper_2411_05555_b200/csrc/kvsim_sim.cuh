@@ -1148,6 +1148,7 @@ struct Sim {
     const double Bd = (double)B;
     double Kd = (double)skv0;
     double e = c.e, js = c.js, busy = c.busy, dG = c.dG, link = c.link;
+    double q0;  // the first step's verified quotient
     int32_t k = 0, tw = 0;
     {  // first chained step: gap against the previous step end (lean_step)
       const double prev = L_prev_end;
@@ -1164,9 +1165,12 @@ struct Sim {
       Kd = kadd(Kd, Bd);
       if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + B);
       js = e;
-      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      q0 = kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp);
+      e = kadd(e, kvsim_math::kmax(q0, comp));
       k = 1;
     }
+    // later quotients only grow: the cheap loop-invariant acceptance test
+    const double T = kdiv_chain_thr(q0, mden);
     // steady state: js == prev, one difference is the busy increment and the
     // gap; first the steps that started before the measurement window
     while (k < nmax && e < tl && js < warmup) {
@@ -1181,7 +1185,7 @@ struct Sim {
       Kd = kadd(Kd, Bd);
       if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k + 1) * B);
       js = e;
-      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      e = kadd(e, kvsim_math::kmax(kdiv_chain(kadd(Wb, kmul(Kd, kvb)), mden, mrcp, T, q0), comp));
       k += 1;
     }
     // inside the window (times only grow): every step adds busy time and ends in it
@@ -1198,7 +1202,7 @@ struct Sim {
       Kd = kadd(Kd, Bd);
       if constexpr (DOLOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k + 1) * B);
       js = e;
-      e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+      e = kadd(e, kvsim_math::kmax(kdiv_chain(kadd(Wb, kmul(Kd, kvb)), mden, mrcp, T, q0), comp));
       k += 1;
     }
     tw += k - kw;
@@ -1400,7 +1404,10 @@ struct Sim {
           Kd = kadd(Kd, Bd);
           if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + B);
           js = e;
-          e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+          const double q0 = kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp);
+          e = kadd(e, kvsim_math::kmax(q0, comp));
+          // later quotients only grow: the cheap loop-invariant acceptance test
+          const double T = kdiv_chain_thr(q0, mden);
           // steady state: the step that just ended started at the previous
           // end (js == prev), so one difference is both the busy increment
           // and the members' gap. 32-bit counters (nmax < 2^31).
@@ -1415,7 +1422,7 @@ struct Sim {
             Kd = kadd(Kd, Bd);
             if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k32 + 1) * B);
             js = e;
-            e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+            e = kadd(e, kvsim_math::kmax(kdiv_chain(kadd(Wb, kmul(Kd, kvb)), mden, mrcp, T, q0), comp));
             k32 += 1;
           }
           // inside the window (times only grow): every step adds to the busy
@@ -1429,7 +1436,7 @@ struct Sim {
             Kd = kadd(Kd, Bd);
             if constexpr (LOG) log_one(e, KVSIM_EV_STEP_START, lane, B, 0, skv0 + (int64_t)(k32 + 1) * B);
             js = e;
-            e = kadd(e, kvsim_math::kmax(kdiv_rcp(kadd(Wb, kmul(Kd, kvb)), mden, mrcp), comp));
+            e = kadd(e, kvsim_math::kmax(kdiv_chain(kadd(Wb, kmul(Kd, kvb)), mden, mrcp, T, q0), comp));
             k32 += 1;
           }
           k = k32;
