@@ -320,21 +320,47 @@ def main():
     achieved = bytes_alg / kernel_s / 1e9 / n_gpu  # per GPU
     events = sum(s.n_events for s in summ)
 
-    # e2e: through the reference-facing C-ABI with host buffers
+    # e2e: the reference-facing C-ABI call itself (kvsim_gpu_run, or
+    # kvsim_gpu_run_multi for N GPUs) on page-locked host buffers from
+    # kvsim_gpu_host_alloc, as the C++ CLI calls it: every step copies the
+    # points host->device, simulates, and copies the summaries back inside
+    # the call. (Filling the host buffers from Python objects is the
+    # caller's, outside the timed region.)
     e2e = None
     if not args.no_e2e:
+        L = pkg.load_library()
+        L.kvsim_gpu_host_alloc.restype = C.c_void_p
+        L.kvsim_gpu_host_alloc.argtypes = [C.c_size_t]
+        L.kvsim_gpu_host_free.argtypes = [C.c_void_p]
         h2d = n * C.sizeof(PointDesc)
         d2h = n * C.sizeof(PointSummary)
+        hp, hs = L.kvsim_gpu_host_alloc(h2d), L.kvsim_gpu_host_alloc(d2h)
+        if not hp or not hs:
+            raise SystemExit("kvsim_gpu_host_alloc failed")
+        HP = (PointDesc * n).from_address(hp)
+        HS = (PointSummary * n).from_address(hs)
+        C.memmove(hp, (PointDesc * n)(*pts), h2d)
+        err = C.create_string_buffer(512)
+        H = (C.c_void_p * n_gpu)(*[s_.h.value for s_ in sims])
+        mst = pkg.MultiStats()
         tt = []
         for i in range(max(1, args.steps)):
             t0 = time.perf_counter()
-            s2 = sim.run(pts) if n_gpu == 1 else pkg.run_multi(sims, pts)[0]
+            if n_gpu == 1:
+                rc = L.kvsim_gpu_run(sim.h, HP, n, None, 0, HS, None, None, 0, None, err, 512)
+            else:
+                rc = L.kvsim_gpu_run_multi(H, n_gpu, HP, n, HS, 0, C.byref(mst), err, 512)
             tt.append(time.perf_counter() - t0)
-        assert all(bytes(a) == bytes(b) for a, b in zip(s2, summ)), "e2e results differ from the timed run"
+            if rc != 0:
+                raise SystemExit(f"e2e C-ABI call failed [{rc}]: {err.value.decode()}")
+        assert all(bytes(HS[i]) == bytes(summ[i]) for i in range(n)), "e2e results differ from the timed run"
+        L.kvsim_gpu_host_free(hp)
+        L.kvsim_gpu_host_free(hs)
         e2e = {"value": reqs * len(tt) / sum(tt), "unit": "simulated requests/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h,
-               "path": "kvsim_gpu_run (host buffers)" if n_gpu == 1 else
-                       f"kvsim_gpu_run_multi over {n_gpu} GPUs (host buffers, one host thread per GPU)"}
+               "seconds_per_call": [round(x, 4) for x in tt],
+               "path": ("kvsim_gpu_run" if n_gpu == 1 else f"kvsim_gpu_run_multi over {n_gpu} GPUs") +
+                       " on page-locked host buffers (kvsim_gpu_host_alloc), wall clock per call"}
 
     # BASELINE config 5 slice (70B, 8 instances, mixed, 3
     # policies x {H100, 910B2} x 250 rates x 667 seeds, 100k requests each):
