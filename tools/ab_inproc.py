@@ -3,7 +3,8 @@ in the same process, a full config-4 warm-up sweep each, then R rounds of
 alternating timed sweeps. Less noisy than one process per variant (clock and
 power state are shared). Usage: python tools/ab_inproc.py [R] [lib[:MINB] ...]
 (MINB = KVSIM_MINB for that context: resident blocks per SM; lib:MINB:CARVE
-also sets KVSIM_CARVEOUT, the shared-memory carveout percent)."""
+also sets KVSIM_CARVEOUT, the shared-memory carveout percent;
+lib:MINB:CARVE:BPS also KVSIM_BLOCKS_PER_SM, the blocks launched per SM)."""
 import glob, os, statistics, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2411_05555_b200 as pkg
@@ -15,7 +16,12 @@ pts = config4_points(0, 833, 10000)
 sims = {}
 for spec in libs:
     lib, _, rest = spec.partition(":")
-    minb, _, carve = rest.partition(":")
+    minb, _, rest = rest.partition(":")
+    carve, _, bps = rest.partition(":")
+    if bps:
+        os.environ["KVSIM_BLOCKS_PER_SM"] = bps
+    else:
+        os.environ.pop("KVSIM_BLOCKS_PER_SM", None)
     if carve:
         os.environ["KVSIM_CARVEOUT"] = carve
     else:
