@@ -839,7 +839,7 @@ struct Sim {
     r.kv = (int64_t)(wbest >> 32);
     return r;
   }
-  KV_DEV_COLD void evict(int x, const Found& v) {
+  KV_DEV_COLD void evict(int x, Found v) {
     EMU_COUNT(14);
     const int y = v.y;
     int64_t held = v.kv;
