@@ -379,6 +379,12 @@ def main():
               "value": c5r / dev_s, "e2e": c5r / wall, "unit": "simulated requests/s", "n_gpus": n_gpu,
               "ms": dev_s * 1e3, "failed_points": sum(1 for x in c5s if x.status != 0),
               "points_per_gpu": [int(st.device_points[i]) for i in range(n_gpu)]}
+        if not args.no_cpu:
+            # every 150th point of the slice (all policies, both devices)
+            # re-simulated on the CPU oracle, compared bit for bit
+            idx = list(range(0, len(c5p), 150))
+            S_c5, _ = oracle_sweep([c5p[i] for i in idx], n_cpu)
+            c5["parity"] = parity_check([c5s[i] for i in idx], S_c5)
 
     cpu, parity = None, None
     if n_gpu == 1 and not args.no_cpu:
