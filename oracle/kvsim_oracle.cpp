@@ -188,6 +188,11 @@ struct Sim {
   int64_t budget;
   std::vector<Req> R;
   int64_t N = 0;
+  // event budget (SEMANTICS §8): 4 n (dmax + 2) + 4096 with n the point's
+  // request limit and dmax the configured decode maximum (a trace: its own
+  // maximum over the whole trace), as the kernel computes it before any
+  // request exists; -1 = derive from the simulated requests
+  int64_t budget_cfg = -1;
   int64_t next_arrival = 0;
   std::vector<Inst> I;
   std::vector<std::deque<int>> Q;         // queues: unified per inst, splitwise 1, accellm per pair
@@ -372,6 +377,7 @@ struct Sim {
     r.primary = -1;
     r.copy = -1;
     r.qlen = r.prompt + r.emitted;
+    r.settling = false;  // leaves the batch: it rejoins through a prefill, not the incoming list (§6 settling)
     r.n_preempt += 1;
     ++n_preempt;
     log(KVSIM_EV_PREEMPT, x, rid, r.qlen, 0);
@@ -1145,7 +1151,7 @@ struct Sim {
   void run() {
     int64_t dmax = 1;
     for (int64_t i = 0; i < N; ++i) dmax = std::max<int64_t>(dmax, R[i].decode);
-    int64_t budget_events = 4 * N * (dmax + 2) + 4096;
+    int64_t budget_events = budget_cfg >= 0 ? budget_cfg : 4 * N * (dmax + 2) + 4096;
     for (;;) {
       double bt = kInf;
       int bk = 9, bid = 0;
@@ -1450,6 +1456,18 @@ int kvo_run_point_ex(const kvsim_point_desc* p, const kvsim_trace_view* trace, k
     N = gen_trace(*p, arr.data(), pr.data(), de.data(), p->num_requests);
   }
   S.N = N;
+  {
+    int64_t bn, bd;
+    if (trace) {
+      bn = std::min<int64_t>(trace->n, p->num_requests);
+      bd = 1;
+      for (int64_t i = 0; i < trace->n; ++i) bd = std::max<int64_t>(bd, trace->decode_len[i]);
+    } else {
+      bn = p->rate > 0.0 ? p->num_requests : 0;
+      bd = p->decode_max > 1 ? p->decode_max : 1;
+    }
+    S.budget_cfg = 4 * bn * (bd + 2) + 4096;
+  }
   S.R.resize(N);
   for (int64_t i = 0; i < N; ++i) {
     S.R[i].arrival = arr[i];
