@@ -2,18 +2,20 @@
 N random points (tests/configs.py random_small: all policies, memory-starved
 half of the time, SPEC variants) through the product library, summaries and
 request records compared bit for bit with the CPU oracle; then the same with
-event logs (full kernel). usage: python tools/stress_parity.py [N] [MAX_REQ] [SEED0]"""
+event logs (full kernel). usage: python tools/stress_parity.py [N] [MAX_REQ] [SEED0] [ext]
+(ext: AcceLLM timer-extension points, tests/configs.py random_ext)"""
 import os, sys
 R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, "tests"))
 import paper_2411_05555_b200 as pkg
-from configs import random_small
+from configs import random_ext, random_small
 from harness import Result, diff_results, run_oracle
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 MAXR = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 S0 = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
-pts = [random_small(S0 + i, max_req=MAXR) for i in range(N)]
+EXT = len(sys.argv) > 4 and sys.argv[4] == "ext"
+pts = [(random_ext if EXT else random_small)(S0 + i, max_req=MAXR) for i in range(N)]
 sim = pkg.KvSim(0)
 summ, recs, _ = sim.run(pts, records=True)
 bad = 0
