@@ -3,7 +3,8 @@ N random points (tests/configs.py random_small: all policies, memory-starved
 half of the time, SPEC variants) through the product library, summaries and
 request records compared bit for bit with the CPU oracle; then the same with
 event logs (full kernel). usage: python tools/stress_parity.py [N] [MAX_REQ] [SEED0] [ext]
-(ext: AcceLLM timer-extension points, tests/configs.py random_ext)"""
+(ext: AcceLLM timer-extension points, tests/configs.py random_ext;
+ detail: the records run as detail runs, pooled TBT percentiles + instance records)"""
 import os, sys
 R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, "tests"))
@@ -15,12 +16,15 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 MAXR = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 S0 = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
 EXT = len(sys.argv) > 4 and sys.argv[4] == "ext"
+DET = len(sys.argv) > 4 and sys.argv[4] == "detail"
 pts = [(random_ext if EXT else random_small)(S0 + i, max_req=MAXR) for i in range(N)]
 sim = pkg.KvSim(0)
-summ, recs, _ = sim.run(pts, records=True)
+summ, recs, _ = sim.run(pts, records=True, detail=DET, instances=DET)
+inst = sim.last_instances
 bad = 0
 for i, p in enumerate(pts):
-    d = diff_results(run_oracle(p, recs=True), Result(summ[i], recs[i], None), events=False)
+    got = Result(summ[i], recs[i], None, inst=inst[i] if DET and summ[i].status == 0 else None)
+    d = diff_results(run_oracle(p, recs=True, detail=DET, inst=DET), got, events=False)
     if d:
         bad += 1
         print(f"  point {i} (seed index {S0 + i}) policy {p.policy} inst {p.num_instances} reqs {p.num_requests} "
