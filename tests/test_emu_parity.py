@@ -117,3 +117,13 @@ def test_serial_pair_chain_variant(tmp_path):
         check(pts)
     finally:
         harness._emu, harness.EMU_SO = saved
+
+
+def test_stress_regressions():
+    """Two points a 3,000-point random GPU-vs-oracle stress run exposed
+    (tools/stress_parity.py): a preempted AcceLLM request re-prefilled while
+    still flagged as settling (memory-starved, 4 instances), and a
+    Splitwise livelock that trips the event budget (first-token-from-decode,
+    memory-starved). Both implementations must agree, including the budget
+    stop point (SEMANTICS §4, §6)."""
+    check([random_small(20249, max_req=400), random_small(20920, max_req=400)], ev=0)

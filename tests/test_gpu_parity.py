@@ -279,3 +279,9 @@ def test_random_configs_lean_kernel_records(sim):
         if d:
             bad.append((i, p.policy, p.num_requests, d[:4]))
     assert not bad, bad
+
+
+def test_stress_regressions_gpu(sim):
+    """The two points tools/stress_parity.py exposed (settling flag across a
+    preemption; event-budget stop point): GPU == oracle, records included."""
+    check(sim, [random_small(20249, max_req=400), random_small(20920, max_req=400)], ev=0)
