@@ -4,7 +4,8 @@ half of the time, SPEC variants) through the product library, summaries and
 request records compared bit for bit with the CPU oracle; then the same with
 event logs (full kernel). usage: python tools/stress_parity.py [N] [MAX_REQ] [SEED0] [ext]
 (ext: AcceLLM timer-extension points, tests/configs.py random_ext;
- detail: the records run as detail runs, pooled TBT percentiles + instance records)"""
+ detail: the records run as detail runs, pooled TBT percentiles + instance records;
+ big: random_small points with 6-32 instances and 8x the rate)"""
 import os, sys
 R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, R); sys.path.insert(0, os.path.join(R, "tests"))
@@ -18,6 +19,12 @@ S0 = int(sys.argv[3]) if len(sys.argv) > 3 else 20000
 EXT = len(sys.argv) > 4 and sys.argv[4] == "ext"
 DET = len(sys.argv) > 4 and sys.argv[4] == "detail"
 pts = [(random_ext if EXT else random_small)(S0 + i, max_req=MAXR) for i in range(N)]
+if len(sys.argv) > 4 and sys.argv[4] == "big":
+    import random as _r
+    for i, p in enumerate(pts):
+        r = _r.Random(S0 + i)
+        p.num_instances = r.choice([6, 8, 12, 16, 24, 32])
+        p.rate = p.rate * 8
 sim = pkg.KvSim(0)
 summ, recs, _ = sim.run(pts, records=True, detail=DET, instances=DET)
 inst = sim.last_instances
