@@ -275,7 +275,10 @@ int kvsim_gpu_run_device(kvsim_gpu_ctx* ctx, const kvsim_point_desc* d_pts, size
                          kvsim_point_summary* d_out, void* stream,
                          char* err, size_t err_len);
 /* Prepare (size + allocate) the arena for a device-resident run of these host
- * points so kvsim_gpu_run_device does no allocation inside a timed region. */
+ * points so kvsim_gpu_run_device does no allocation inside a timed region.
+ * The reservation lasts until the next kvsim_gpu_run / _run_ex on the same
+ * context (which re-sizes the arena for its own points); d_pts passed to
+ * kvsim_gpu_run_device must be the reserved points. */
 int kvsim_gpu_reserve(kvsim_gpu_ctx* ctx, const kvsim_point_desc* pts, size_t n,
                       char* err, size_t err_len);
 /* Kernel launches issued by the last run (for the bench's gpu_launches). */
